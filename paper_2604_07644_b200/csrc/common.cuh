@@ -1,0 +1,85 @@
+// Shared types and helpers for the GPU-SLS kernels (sm_100a).
+//
+// Internal storage convention: every n x n matrix kept on the device by the
+// solver (scan slot values, recorded aux, SLS grids) is row-major with a
+// padded leading dimension LDG = round_up(n, 4) and zero padding columns, so
+// rows can be moved with 16-byte vector accesses.  User-facing QP buffers are
+// dense row-major without padding (the reference layouts, lqr.py:53-68).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/gsls.h"
+
+namespace gsls {
+
+constexpr int kMaxN = 80;        // largest state dimension supported (75D humanoid + slack)
+constexpr int kMaxM = 24;        // largest input dimension (north star: n_u <= 23)
+
+__host__ __device__ inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
+__host__ __device__ inline int ldg_of(int n) { return round_up(n, 4); }
+// smem leading dimension: multiple of 4 (float4 rows) and == 4 mod 8 so rows
+// i and i+4 of a column fall in different banks.
+__host__ __device__ inline int lds_of(int n) {
+  int l = round_up(n, 4);
+  return (l % 8 == 4) ? l : l + 4;
+}
+__host__ __device__ inline size_t mat_elems(int n) { return (size_t)n * ldg_of(n); }
+
+// Per-instance error record written by kernels (first writer wins).
+struct ErrSlot {
+  int code;   // gsls_status_t
+  int where;  // stage / op / position
+  int aux;    // column j (SLS) or -1
+  int pad;
+};
+
+__device__ inline void raise_err(ErrSlot* e, int code, int where, int aux = -1) {
+  if (e == nullptr) return;
+  if (atomicCAS(&e->code, 0, code) == 0) {
+    e->where = where;
+    e->aux = aux;
+  }
+}
+
+__device__ inline float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ inline float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide max of non-negative values; `red` needs blockDim/32 floats.
+__device__ inline float block_max(float v, float* red) {
+  v = warp_max(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float r = 0.f;
+  const int nw = blockDim.x >> 5;
+  for (int i = 0; i < nw; ++i) r = fmaxf(r, red[i]);
+  __syncthreads();
+  return r;
+}
+
+}  // namespace gsls
+
+#define GSLS_CUDA_CHECK(expr)                                   \
+  do {                                                          \
+    cudaError_t _e = (expr);                                    \
+    if (_e != cudaSuccess) {                                    \
+      gsls::set_last_error(cudaGetErrorString(_e), __FILE__, __LINE__); \
+      return GSLS_ERR_CUDA;                                     \
+    }                                                           \
+  } while (0)
+
+namespace gsls {
+void set_last_error(const char* msg, const char* file, int line);
+}

@@ -1,0 +1,256 @@
+"""Generate golden fixtures by running the REAL reference (build container only).
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Imports ``scanmpc`` from /root/reference/pkg/src (read-only, never shipped),
+runs it on seeded inputs and stores inputs + outputs as small ``.npz`` files
+next to this script.  The GPU box never reads /root/reference; it only reads
+these fixtures.  Every fixture records the reference call it came from.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+from scanmpc import admm, lqr, models, reference, scan, sls, sqp  # noqa: E402
+
+import problems as P  # noqa: E402
+from paper_2604_07644_b200 import models as ours  # noqa: E402
+
+EX = scan.SequentialExecutor()
+FIELDS = ("A", "B", "b", "Q", "R", "S", "q", "r", "QN", "qN", "C", "D", "f", "CN", "fN", "dx0")
+
+
+def ref_qp(qp):
+    return lqr.LtvQpData(**{k: np.array(getattr(qp, k), float) for k in FIELDS})
+
+
+def qp_dict(qp, prefix="qp_"):
+    return {prefix + k: np.asarray(getattr(qp, k), float) for k in FIELDS}
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {name}.npz ({os.path.getsize(path) / 1024:.1f} KiB)")
+
+
+def traj_dict(t, prefix):
+    return {prefix + "x": t.x, prefix + "u": t.u, prefix + "dt": np.float64(t.dt)}
+
+
+def gen_scan():
+    rng = np.random.default_rng(5)
+    ints = rng.integers(-1000, 1000, size=300)
+    fwd = scan.inclusive_scan(ints.tolist(), lambda a, b: a + b, 0)
+    rev = scan.inclusive_scan(ints.tolist(), lambda a, b: a + b, 0, direction="reverse")
+    mats = rng.standard_normal((7, 2, 2))
+    suffix = scan.inclusive_scan(list(mats), lambda a, b: a @ b, np.eye(2), direction="reverse")
+    save("scan", ints=ints, fwd=np.array(fwd), rev=np.array(rev), mats=mats, suffix=np.array(suffix),
+         depths=np.array([[L, scan.scan_depth(L)] for L in (1, 2, 3, 8, 17, 26, 51, 1000, 2048)]))
+
+
+def gen_lqr():
+    out = {}
+    for tag, (nx, nu, N, seed) in {"r6": (6, 3, 64, 0), "r5": (5, 2, 29, 1), "r12": (12, 4, 100, 2),
+                                   "r61": (61, 12, 25, 3)}.items():
+        qp = P.random_ltv_qp(np.random.default_rng(seed), nx, nu, N)
+        sol = lqr.solve(ref_qp(qp), executor=EX)
+        # inputs are regenerated from the seed by the tests; store a checksum of them
+        out[f"{tag}_dims"] = np.array([nx, nu, N, seed])
+        out[f"{tag}_checksum"] = np.float64(sum(float(np.abs(getattr(qp, k)).sum()) for k in FIELDS))
+        for fld in ("dx", "du", "K", "k", "p"):
+            out[f"{tag}_{fld}"] = getattr(sol, fld)
+        out[f"{tag}_P0"] = sol.P[0]
+        out[f"{tag}_layers"] = np.int64(sol.scan_layers)
+    # cached replay with perturbed linear terms (test_lqr.py:250-260)
+    qp = P.random_ltv_qp(np.random.default_rng(1), 5, 2, 29)
+    _, cache = lqr.build_cache(ref_qp(qp), executor=EX, generation=0)
+    rng = np.random.default_rng(11)
+    q, r, qN = rng.standard_normal(qp.q.shape), rng.standard_normal(qp.r.shape), rng.standard_normal(qp.qN.shape)
+    fast = lqr.solve_cached(lqr.LqrLinearTerms(q, r, qN), cache, 0, executor=EX)
+    out.update(pert_q=q, pert_r=r, pert_qN=qN, pert_dx=fast.dx, pert_du=fast.du, pert_k=fast.k, pert_p=fast.p)
+    # scalar analytic + N=0
+    s = lqr.solve(ref_qp(P.scalar_qp()), executor=EX)
+    out.update(scalar_du=s.du, scalar_dx=s.dx)
+    save("lqr", **out)
+
+
+def gen_admm():
+    out = {}
+    st = admm.AdmmSettings(rho0=0.1, sigma=10, tol_primal=1e-4, tol_dual=1e-4, max_iter=4000)
+    qp = P.double_integrator()
+    res = admm.solve_qp(ref_qp(qp), st, executor=EX)
+    f = np.concatenate([qp.f.ravel(), qp.fN])
+    out.update({f"di_{k}": v for k, v in qp_dict(qp).items()})
+    out.update(di_dx=res.dx, di_du=res.du, di_lam=res.state.lam, di_z=res.state.z,
+               di_iters=np.int64(res.stats.iterations), di_rho=np.float64(res.stats.rho),
+               di_rho_changes=np.int64(res.stats.rho_changes), di_builds=np.int64(res.stats.cache_builds),
+               di_active=(res.state.z >= f - 1e-12), di_converged=np.bool_(res.stats.converged))
+    # batch of seeded initial offsets (SURVEY §8d cfg-A batch)
+    rng = np.random.default_rng(123)
+    x0s = rng.uniform(-5, 5, (8, 4))
+    its, dxs, dus, acts = [], [], [], []
+    for x0 in x0s:
+        r2 = admm.solve_qp(ref_qp(P.double_integrator(dx0=x0)), st, executor=EX)
+        its.append(r2.stats.iterations); dxs.append(r2.dx); dus.append(r2.du)
+        acts.append(r2.state.z >= f - 1e-12)
+    out.update(dib_x0=x0s, dib_iters=np.array(its), dib_dx=np.array(dxs), dib_du=np.array(dus),
+               dib_active=np.array(acts))
+    # random problems vs dense IP (test_admm.py:118-129)
+    rng = np.random.default_rng(0)
+    st6 = admm.AdmmSettings(tol_primal=1e-6, tol_dual=1e-6)
+    for i in range(3):
+        qp = P.random_ltv_qp(rng, 4, 2, 12, nc=3, nf=1)
+        res = admm.solve_qp(ref_qp(qp), st6, executor=EX)
+        H, g, Ai, bi, Ae, be = P.dense_form(qp)
+        _, obj, _ = reference.dense_qp(H, g, Ai, bi, Ae, be)
+        out.update({f"rnd{i}_{k}": v for k, v in qp_dict(qp).items()})
+        out.update({f"rnd{i}_dx": res.dx, f"rnd{i}_du": res.du, f"rnd{i}_lam": res.state.lam,
+                    f"rnd{i}_iters": np.int64(res.stats.iterations), f"rnd{i}_obj": np.float64(obj),
+                    f"rnd{i}_rho_changes": np.int64(res.stats.rho_changes)})
+    save("admm", **out)
+
+
+def pack_resp(resp, N, nx, nu, prefix):
+    return {prefix + "phix": P.pack_lower(resp.Phi_x, N, 1, N + 1, (nx, nx)),
+            prefix + "phiu": P.pack_lower(resp.Phi_u, N, 1, N, (nu, nx)),
+            prefix + "gain": P.pack_lower(resp.gains, N, 1, N, (nu, nx))}
+
+
+def gen_sls():
+    out = {}
+    # the selftest instance (cli.py:499-527)
+    rng = np.random.default_rng(0)
+    qp = P.selftest_lqr(rng)
+    nx, nu, N = 4, 2, 40
+    E = rng.standard_normal((N, nx, nx)) * 0.05
+    C = rng.standard_normal((N, 2, nx))
+    D = rng.standard_normal((N, 2, nu))
+    CN = rng.standard_normal((1, nx))
+    w = sls.SlsWeights.identity(nx, nu)
+    costs = sls.assemble_costs(None, C, D, CN, w)
+    resp = sls.synthesize(qp.A, qp.B, E, costs, executor=EX)
+    t = sls.tighten(resp, C, D, CN)
+    lam_s = np.abs(rng.standard_normal((N, 2))) * (rng.random((N, 2)) > 0.5)
+    lam_t = np.abs(rng.standard_normal(1))
+    du = sls.compute_duals(lam_s, lam_t, resp, C, D, CN, 1e-6)
+    costs2 = sls.assemble_costs(du, C, D, CN, sls.SlsWeights(2 * np.eye(nx), 3 * np.eye(nu), np.eye(nx)))
+    resp2 = sls.synthesize(qp.A, qp.B, E, costs2, executor=EX)
+    t2 = sls.tighten(resp2, C, D, CN)
+    out.update(A=qp.A, B=qp.B, E=E, C=C, D=D, CN=CN, lam_s=lam_s, lam_t=lam_t, h=t.h, hf=t.hf,
+               tau=P.pack_lower(du.tau, N, 1, N, (2,)), tau_term=du.tau_term,
+               beta=P.pack_lower(du.beta, N, 1, N, (2,)), beta_term=du.beta_term,
+               h2=t2.h, hf2=t2.hf, cost2=np.float64(sls.sls_cost(resp2, sls.SlsWeights(2 * np.eye(nx), 3 * np.eye(nu), np.eye(nx)))))
+    out.update(pack_resp(resp, N, nx, nu, "r1_"))
+    out.update(pack_resp(resp2, N, nx, nu, "r2_"))
+    # hand 2-stage scalar (test_reference.py:86-98)
+    save("sls", **out)
+
+
+def gen_models():
+    rng = np.random.default_rng(4)
+    out = {}
+    cases = {"dubins": (models.DubinsCar(obstacles=((1.0, 0.5, 0.3),)), ours.DubinsCar(obstacles=((1.0, 0.5, 0.3),))),
+             "quad": (models.PlanarQuadrotor(obstacles=((1.5, 0.0, 0.35),)), ours.PlanarQuadrotor(obstacles=((1.5, 0.0, 0.35),))),
+             "pend2": (models.NLinkPendulum(n_links=2), ours.NLinkPendulum(n_links=2)),
+             "pend4": (models.NLinkPendulum(n_links=4, e_rate=0.05), ours.NLinkPendulum(n_links=4, e_rate=0.05))}
+    for tag, (ref, _) in cases.items():
+        xs = rng.standard_normal((5, ref.nx)) * 0.5
+        us = rng.standard_normal((5, ref.nu))
+        out[f"{tag}_x"], out[f"{tag}_u"] = xs, us
+        out[f"{tag}_step"] = np.array([ref.step(x, u) for x, u in zip(xs, us)])
+        out[f"{tag}_A"] = np.array([ref.jacobians(x, u)[0] for x, u in zip(xs, us)])
+        out[f"{tag}_B"] = np.array([ref.jacobians(x, u)[1] for x, u in zip(xs, us)])
+        out[f"{tag}_g"] = np.array([ref.stage_constraints(x, u) for x, u in zip(xs, us)])
+        out[f"{tag}_C"] = np.array([ref.stage_constraint_jacobians(x, u)[0] for x, u in zip(xs, us)])
+        out[f"{tag}_D"] = np.array([ref.stage_constraint_jacobians(x, u)[1] for x, u in zip(xs, us)])
+        out[f"{tag}_E"] = np.array([ref.disturbance(x) for x in xs])
+        out[f"{tag}_gf"] = np.array([ref.terminal_constraints(x) for x in xs]).reshape(5, -1)
+    save("models", **out)
+
+
+def _rti_case(model, x0, N, st, rs, steps, tag, out):
+    nom = sqp.solve_nmpc(model, x0, st, sqp.initial_guess(model, x0, N, "rollout"), executor=EX)
+    warm, tau, u = nom.trajectory.shifted(), None, nom.trajectory.u[0]
+    x = np.asarray(x0, float)
+    for s in range(steps):
+        x = model.step(x, u)
+        r = sls.rti_robust_step(model, x, warm, tau, rs, executor=EX)
+        if s == steps - 1:
+            N_ = warm.N
+            out.update(traj_dict(warm, f"{tag}_prev_"))
+            out[f"{tag}_xbar0"] = x
+            out[f"{tag}_tau_in"] = P.pack_lower(tau.tau, N_, 1, N_, (model.nc,)) if tau else np.zeros(0)
+            out[f"{tag}_tau_term_in"] = tau.tau_term if tau else np.zeros(0)
+            out[f"{tag}_u0"] = r.u0
+            out.update(traj_dict(r.plan, f"{tag}_plan_"))
+            out[f"{tag}_h"], out[f"{tag}_hf"] = r.tightening.h, r.tightening.hf
+            out[f"{tag}_lam_s"], out[f"{tag}_lam_t"] = r.lam_stage, r.lam_terminal
+            out[f"{tag}_tau_out"] = P.pack_lower(r.tau.tau, N_, 1, N_, (model.nc,))
+            out[f"{tag}_tau_term_out"] = r.tau.tau_term
+            out[f"{tag}_admm_iters"] = np.int64(r.stats.admm_iterations)
+            out[f"{tag}_converged"] = np.bool_(r.stats.converged)
+            out[f"{tag}_cost"] = np.float64(r.stats.cost)
+            print(tag, "admm iters", r.stats.admm_iterations, "converged", r.stats.converged)
+        warm, tau, u = r.warm_start, r.tau, r.u0
+
+
+def gen_rti():
+    out = {}
+    # planar quadrotor (quadrotor_compare-like), N=20
+    quad_ref = models.PlanarQuadrotor(dt=0.05, thrust_max=30.0, goal=(2.6, 0, 0, 0, 0, 0),
+                                      obstacles=((1.5, 0.0, 0.35),))
+    st = sqp.SqpSettings(max_sqp_iters=50, kkt_tol=5e-4,
+                         admm=admm.AdmmSettings(rho0=10.0, tol_primal=2e-5, tol_dual=2e-5, max_iter=1500))
+    st_rti = sqp.SqpSettings(max_sqp_iters=30, kkt_tol=2e-3,
+                             admm=admm.AdmmSettings(rho0=10.0, tol_primal=1e-3, tol_dual=1e-3, max_iter=300))
+    rs = sls.RobustSettings(sqp=st_rti, weights=sls.SlsWeights(np.diag([20.0, 20, 1, 4, 4, 0.5]), 0.3 * np.eye(2),
+                                                               np.diag([20.0, 20, 1, 4, 4, 0.5])), eps=1e-4)
+    x0 = np.array([0.4, 0.3, 0, 0, 0, 0])
+    nom = sqp.solve_nmpc(quad_ref, x0, st, sqp.initial_guess(quad_ref, x0, 20), executor=EX)
+    print("quad nmpc", nom.stats)
+    warm, tau, u, x = nom.trajectory.shifted(), None, nom.trajectory.u[0], x0
+    for s in range(3):
+        x = quad_ref.step(x, u)
+        r = sls.rti_robust_step(quad_ref, x, warm, tau, rs, executor=EX)
+        if s == 2:
+            out.update(traj_dict(warm, "pq_prev_"))
+            out["pq_xbar0"] = x
+            out["pq_tau_in"] = P.pack_lower(tau.tau, 20, 1, 20, (quad_ref.nc,))
+            out["pq_tau_term_in"] = tau.tau_term
+            out["pq_u0"] = r.u0
+            out.update(traj_dict(r.plan, "pq_plan_"))
+            out["pq_h"], out["pq_hf"] = r.tightening.h, r.tightening.hf
+            out["pq_lam_s"], out["pq_lam_t"] = r.lam_stage, r.lam_terminal
+            out["pq_tau_out"] = P.pack_lower(r.tau.tau, 20, 1, 20, (quad_ref.nc,))
+            out["pq_tau_term_out"] = r.tau.tau_term
+            out["pq_admm_iters"] = np.int64(r.stats.admm_iterations)
+            print("pq admm iters", r.stats.admm_iterations, r.stats.converged)
+        warm, tau, u = r.warm_start, r.tau, r.u0
+
+    # synthetic legged plants (cfg D / E-RTI), N=25, our host model under the reference solver
+    for tag, mdl in (("q61", ours.quadruped61()), ("h75", ours.humanoid75())):
+        st = sqp.SqpSettings(max_sqp_iters=30, kkt_tol=1e-3,
+                             admm=admm.AdmmSettings(rho0=1.0, tol_primal=1e-3, tol_dual=1e-3, max_iter=500))
+        rs = sls.RobustSettings(sqp=st, eps=1e-4,
+                                weights=sls.SlsWeights(np.eye(mdl.nx), 10 * np.eye(mdl.nu), np.eye(mdl.nx)))
+        x0 = np.zeros(mdl.nx)
+        x0[0], x0[1] = -0.3, 0.05
+        _rti_case(mdl, x0, 25, st, rs, 2, tag, out)
+    save("rti", **out)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["scan", "lqr", "admm", "sls", "models", "rti"]
+    for w in which:
+        globals()["gen_" + w]()
