@@ -1,0 +1,191 @@
+/*
+ * gsls.h — C ABI of the B200-native GPU-SLS solver core (libgsls.so).
+ *
+ * Plain C: device pointers (float32, row-major, batch-major, the layouts of
+ * the reference's LtvQpData, /root/reference/pkg/src/scanmpc/lqr.py:53-68),
+ * sizes, and a cudaStream_t passed as void*.  No torch types.  Every entry
+ * point returns a gsls_status_t; details of the last failure (instance,
+ * stage, column) are read with gsls_last_error().
+ *
+ * Each function below names the reference interface it replaces.  The
+ * reference is a Python package with no FFI of its own; these are the
+ * calls its module-level entry points bind to (see INTEGRATION.md for the
+ * ctypes stubs).
+ */
+#ifndef GSLS_H_
+#define GSLS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GSLS_OK = 0,
+  GSLS_ERR_ARG = 1,               /* ValueError: bad shape/argument                       */
+  GSLS_ERR_CUDA = 2,              /* CUDA runtime failure                                   */
+  GSLS_ERR_SINGULAR_STAGE = 3,    /* lqr.SingularStageError (lqr.py:35, :213-215; sls.py:321-326) */
+  GSLS_ERR_ILL_CONDITIONED = 4,   /* lqr.IllConditionedCombineError (lqr.py:31, :229-232)   */
+  GSLS_ERR_CACHE_INVALIDATED = 5, /* lqr.CacheInvalidatedError (lqr.py:39, :426-427)        */
+  GSLS_ERR_NONFINITE = 6,         /* ArithmeticError non-finite dynamics (sqp.py:125-131)   */
+  GSLS_ERR_TOO_LARGE = 7,         /* dimensions beyond the compiled limits                  */
+  GSLS_ERR_NO_DEVICE = 8
+} gsls_status_t;
+
+/* labels carried with GSLS_ERR_SINGULAR_STAGE (error.aux2) */
+enum {
+  GSLS_LABEL_R = 1,            /* "singular R at stage i"                       lqr.py:323 */
+  GSLS_LABEL_R_BPB = 2,        /* "singular R + B'PB at stage i"                lqr.py:399 */
+  GSLS_LABEL_QU = 3,           /* "singular Qu block at (k=.., j=..)"           sls.py:258-261 */
+  GSLS_LABEL_QU_BPB = 4,       /* "singular Qu + B'PB block at (k=.., j=..)"    sls.py:288-293 */
+  GSLS_LABEL_NONFINITE_DYN = 5,
+  GSLS_LABEL_NONFINITE_CON = 6
+};
+
+typedef struct {
+  int32_t code;      /* gsls_status_t                                   */
+  int32_t instance;  /* batch index, -1 if not instance-specific         */
+  int32_t where;     /* stage k / scan op                                */
+  int32_t aux;       /* SLS column j, or -1                              */
+  int32_t aux2;      /* GSLS_LABEL_* for singular blocks                 */
+  char message[256];
+} gsls_error_t;
+
+/* Problem dimensions; one set per batch of independent instances. */
+typedef struct {
+  int32_t nx, nu, nc, nf, N; /* lqr.py:70-88 properties */
+  int32_t batch;
+} gsls_dims_t;
+
+/* Stagewise QP data (lqr.py:53-68), device, batch-major.  Precision split:
+ * matrices are float32 (they feed the fp32 factorization), vectors are
+ * float64 (the replay and the ADMM iterate run in fp64 — see DESIGN.md §3).
+ *   float32:  A (B,N,nx,nx) B (B,N,nx,nu) Q (B,N,nx,nx) R (B,N,nu,nu)
+ *             S (B,N,nu,nx) or NULL (= 0) QN (B,nx,nx) C (B,N,nc,nx)
+ *             D (B,N,nc,nu) CN (B,nf,nx)
+ *   float64:  b (B,N,nx) q (B,N,nx) r (B,N,nu) qN (B,nx) f (B,N,nc) fN (B,nf)
+ *             dx0 (B,nx) */
+typedef struct {
+  const float* A;
+  const float* B;
+  const double* b;
+  const float* Q;
+  const float* R;
+  const float* S;
+  const double* q;
+  const double* r;
+  const float* QN;
+  const double* qN;
+  const float* C;
+  const float* D;
+  const double* f;
+  const float* CN;
+  const double* fN;
+  const double* dx0;
+} gsls_qp_t;
+
+/* admm.AdmmSettings (admm.py:24-39). */
+typedef struct {
+  double rho0, rho_min, rho_max;
+  int32_t sigma;
+  double tol_primal, tol_dual;
+  int32_t max_iter;
+} gsls_admm_settings_t;
+
+/* admm.AdmmState (admm.py:42-55), device arrays, in/out (mutated in place,
+ * as the reference mutates its warm_start, admm.py:164/:186/:197).
+ * z, lam, y: (B, N*nc+nf) float64; rho, r_primal, r_dual: (B) float64;
+ * generation, iteration: (B) int32. */
+typedef struct {
+  double *z, *lam, *y;
+  double *rho, *r_primal, *r_dual;
+  int32_t *generation, *iteration;
+} gsls_admm_state_t;
+
+/* admm.AdmmStats (admm.py:58-67), device int32 arrays (B). */
+typedef struct {
+  int32_t *iterations, *converged, *rho_changes, *cache_builds;
+} gsls_admm_stats_t;
+
+typedef struct gsls_ctx gsls_ctx; /* workspace + LQR factorization cache for one dims */
+
+/* ---- context ---------------------------------------------------------- */
+int gsls_version(void);
+int gsls_last_error(gsls_error_t* out);
+int gsls_ctx_create(const gsls_dims_t* dims, gsls_ctx** out);
+int gsls_ctx_destroy(gsls_ctx* ctx);
+/* bytes of device memory held by the context */
+int64_t gsls_ctx_bytes(const gsls_ctx* ctx);
+
+/* ---- scan plan (scan.py:141-234 tree order), host-side, for inspection --
+ * Writes the combine ops of a scan of `length` elements: ops[3*i..3*i+2] =
+ * (dst, earlier, later) slot ids, layer_off[0..layers] offsets into ops,
+ * out_slot[0..length-1] (-1 = identity).  Returns number of ops in *n_ops. */
+int gsls_scan_plan(int32_t length, int32_t reverse, int32_t max_ops, int32_t* ops,
+                   int32_t* layer_off, int32_t* out_slot, int32_t* n_ops, int32_t* n_layers);
+
+/* ---- LQR (lqr.py) ------------------------------------------------------ */
+/* lqr.solve (lqr.py:366): full solve. Outputs (float64) dx (B,N+1,nx)
+ * du (B,N,nu) k (B,N,nu) p (B,N+1,nx); (float32) K (B,N,nu,nx)
+ * P (B,N+1,nx,nx); K/k/P/p may be NULL.
+ * Leaves the factorization cache in ctx stamped with `generation`. */
+int gsls_lqr_solve(gsls_ctx* ctx, const gsls_qp_t* qp, int32_t generation, double* dx, double* du,
+                   float* K, double* k, float* P, double* p, void* stream);
+/* lqr.build_cache (lqr.py:372) == gsls_lqr_solve with the cache kept. */
+/* lqr.solve_cached (lqr.py:419): replay with new linear terms only.
+ * q (B,N,nx) r (B,N,nu) qN (B,nx); generation must match the cache stamp. */
+int gsls_lqr_solve_cached(gsls_ctx* ctx, const gsls_qp_t* qp, const double* q, const double* r,
+                          const double* qN, int32_t generation, double* dx, double* du, double* k,
+                          double* p, void* stream);
+
+/* ---- ADMM QP (admm.py:153-203), batched -------------------------------- */
+/* Runs every instance to convergence / max_iter with per-instance rho,
+ * cache rebuilds on committed rho changes, exact reference control flow.
+ * dx (B,N+1,nx), du (B,N,nu) (float64) receive the last LQR iterate. */
+int gsls_admm_solve_qp(gsls_ctx* ctx, const gsls_qp_t* qp, const gsls_admm_settings_t* settings,
+                       gsls_admm_state_t* state, gsls_admm_stats_t* stats, double* dx, double* du,
+                       void* stream);
+
+/* Exports the last solve held by ctx: K (B,N,nu,nx) and P (B,N+1,nx,nx) of
+ * the current factorization, k (B,N,nu) and p (B,N+1,nx) of the last replay
+ * (the LqrSolution the reference returns in AdmmResult.solution, admm.py:203).
+ * Any output may be NULL. */
+int gsls_ctx_export_solution(gsls_ctx* ctx, float* K, double* k, float* P, double* p, void* stream);
+
+/* ---- SLS (sls.py) -------------------------------------------------------
+ * Per-instance SLS objects use a triangular CELL layout: cell(k, j) for
+ * 0 <= j < k <= N, index j*N - j*(j-1)/2 + (k-j-1), ncell = N(N+1)/2
+ * (gsls_sls_ncell).  Cells with k <= N-1 carry stage quantities (costs, gains,
+ * Phi^u, tau); cells with k = N carry the terminal ones (Qx_term, tau_term via
+ * column j).  Phi^x is defined on every cell. */
+int gsls_sls_ncell(int32_t N);
+/* sls.assemble_costs (sls.py:176-200): [C D]' diag(tau) [C D] + blkdiag(Qbar, Rbar)
+ * per cell, CN' diag(tau_term) CN + QbarN on terminal cells.  tau (B,ncell,nc)
+ * float64 or NULL (= unweighted, sls.py:189); tau_term (B,N,nf) or NULL.
+ * Qbar (nx,nx) Rbar (nu,nu) QbarN (nx,nx) float32, one set per instance when
+ * weights_per_instance != 0.  C, D, CN are taken from qp. */
+int gsls_sls_assemble(gsls_ctx* ctx, const gsls_qp_t* qp, const double* tau, const double* tau_term,
+                      const float* Qbar, const float* Rbar, const float* QbarN, int32_t weights_per_instance,
+                      void* stream);
+/* Explicit SlsCosts (sls.py:129-143) in cell layout: Qx (B,ncell,nx,nx) (terminal
+ * cells hold Qx_term), Qu (B,ncell,nu,nu), Qux (B,ncell,nu,nx), float32. */
+int gsls_sls_set_costs(gsls_ctx* ctx, const float* Qx, const float* Qu, const float* Qux, void* stream);
+/* sls.synthesize (sls.py:227-318) on the costs held by ctx; A, B from qp,
+ * E (B,N,nx,nx) float32.  The response stays on the device. */
+int gsls_sls_synthesize(gsls_ctx* ctx, const gsls_qp_t* qp, const float* E, void* stream);
+/* sls.tighten (sls.py:329-341): h (B,N,nc), hf (B,nf), float64. */
+int gsls_sls_tighten(gsls_ctx* ctx, double* h, double* hf, void* stream);
+/* sls.compute_duals (sls.py:150-173): lam_stage (B,N,nc) lam_term (B,nf) ->
+ * tau (B,ncell,nc), tau_term (B,N,nf) [beta, beta_term same shapes, may be
+ * NULL], float64.  use_response = 0 reproduces response=None (beta = 0). */
+int gsls_sls_duals(gsls_ctx* ctx, const double* lam_stage, const double* lam_term, double eps, int32_t use_response,
+                   double* tau, double* tau_term, double* beta, double* beta_term, void* stream);
+/* SlsResponse export (sls.py:51-92): Phi_x (B,ncell,nx,nx), Phi_u and gains
+ * (B,ncell,nu,nx) (zero on terminal cells), float32; any may be NULL. */
+int gsls_sls_export(gsls_ctx* ctx, float* phix, float* phiu, float* gains, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSLS_H_ */

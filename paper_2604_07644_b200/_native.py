@@ -1,0 +1,123 @@
+"""ctypes binding of libgsls.so (the C ABI in include/gsls.h).
+
+The library is built in-tree by ``__graft_entry__.build()``.  There is no
+CPU fallback: importing the product path without the library, or without a
+CUDA device, raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgsls.so")
+
+c_int32_p = ctypes.POINTER(ctypes.c_int32)
+c_void_p = ctypes.c_void_p
+
+# status codes (gsls_status_t)
+OK, ERR_ARG, ERR_CUDA, ERR_SINGULAR, ERR_ILL, ERR_CACHE, ERR_NONFINITE, ERR_TOO_LARGE, ERR_NO_DEVICE = range(9)
+
+
+class Dims(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("nu", ctypes.c_int32), ("nc", ctypes.c_int32),
+                ("nf", ctypes.c_int32), ("N", ctypes.c_int32), ("batch", ctypes.c_int32)]
+
+
+QP_FIELDS = ("A", "B", "b", "Q", "R", "S", "q", "r", "QN", "qN", "C", "D", "f", "CN", "fN", "dx0")
+
+
+class Qp(ctypes.Structure):
+    _fields_ = [(k, c_void_p) for k in QP_FIELDS]
+
+
+class AdmmSettings(ctypes.Structure):
+    _fields_ = [("rho0", ctypes.c_double), ("rho_min", ctypes.c_double), ("rho_max", ctypes.c_double),
+                ("sigma", ctypes.c_int32), ("tol_primal", ctypes.c_double), ("tol_dual", ctypes.c_double),
+                ("max_iter", ctypes.c_int32)]
+
+
+class AdmmState(ctypes.Structure):
+    _fields_ = [("z", c_void_p), ("lam", c_void_p), ("y", c_void_p), ("rho", c_void_p),
+                ("r_primal", c_void_p), ("r_dual", c_void_p), ("generation", c_void_p),
+                ("iteration", c_void_p)]
+
+
+class AdmmStats(ctypes.Structure):
+    _fields_ = [("iterations", c_void_p), ("converged", c_void_p), ("rho_changes", c_void_p),
+                ("cache_builds", c_void_p)]
+
+
+class Error(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_int32), ("instance", ctypes.c_int32), ("where", ctypes.c_int32),
+                ("aux", ctypes.c_int32), ("aux2", ctypes.c_int32), ("message", ctypes.c_char * 256)]
+
+
+_SIGS = {
+    "gsls_version": ([], ctypes.c_int),
+    "gsls_last_error": ([ctypes.POINTER(Error)], ctypes.c_int),
+    "gsls_ctx_create": ([ctypes.POINTER(Dims), ctypes.POINTER(c_void_p)], ctypes.c_int),
+    "gsls_ctx_destroy": ([c_void_p], ctypes.c_int),
+    "gsls_ctx_bytes": ([c_void_p], ctypes.c_int64),
+    "gsls_scan_plan": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_int32_p, c_int32_p, c_int32_p,
+                        c_int32_p, c_int32_p], ctypes.c_int),
+    "gsls_lqr_solve": ([c_void_p, ctypes.POINTER(Qp), ctypes.c_int32] + [c_void_p] * 6 + [c_void_p], ctypes.c_int),
+    "gsls_lqr_solve_cached": ([c_void_p, ctypes.POINTER(Qp), c_void_p, c_void_p, c_void_p, ctypes.c_int32]
+                              + [c_void_p] * 4 + [c_void_p], ctypes.c_int),
+    "gsls_admm_solve_qp": ([c_void_p, ctypes.POINTER(Qp), ctypes.POINTER(AdmmSettings),
+                            ctypes.POINTER(AdmmState), ctypes.POINTER(AdmmStats), c_void_p, c_void_p,
+                            c_void_p], ctypes.c_int),
+    "gsls_ctx_export_solution": ([c_void_p] * 6, ctypes.c_int),
+}
+
+# every symbol include/gsls.h declares (checked by the CPU test suite)
+EXPORTS = tuple(_SIGS)
+
+_lib = None
+
+
+def load(require_device: bool = True):
+    """Load libgsls.so (raises when missing; no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is not built; run __graft_entry__.build() "
+                               "(the GPU-SLS path has no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+    if require_device:
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("the GPU-SLS path needs a CUDA device (no CPU fallback)")
+    return _lib
+
+
+def last_error() -> Error:
+    e = Error()
+    load(False).gsls_last_error(ctypes.byref(e))
+    return e
+
+
+def check(rc: int, what: str = "gsls call"):
+    """Map a gsls_status_t to the reference's exception classes."""
+    if rc == OK:
+        return
+    from . import errors
+    e = last_error()
+    msg = e.message.decode(errors="replace") or what
+    if rc == ERR_ARG:
+        raise ValueError(msg)
+    if rc == ERR_SINGULAR:
+        raise errors.SingularStageError(msg)
+    if rc == ERR_ILL:
+        raise errors.IllConditionedCombineError(msg)
+    if rc == ERR_CACHE:
+        raise errors.CacheInvalidatedError(msg)
+    if rc == ERR_NONFINITE:
+        raise ArithmeticError(msg)
+    raise RuntimeError(f"{what}: {msg} (status {rc})")

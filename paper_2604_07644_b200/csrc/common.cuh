@@ -32,14 +32,15 @@ struct ErrSlot {
   int code;   // gsls_status_t
   int where;  // stage / op / position
   int aux;    // column j (SLS) or -1
-  int pad;
+  int label;  // GSLS_LABEL_*
 };
 
-__device__ inline void raise_err(ErrSlot* e, int code, int where, int aux = -1) {
+__device__ inline void raise_err(ErrSlot* e, int code, int where, int aux = -1, int label = 0) {
   if (e == nullptr) return;
   if (atomicCAS(&e->code, 0, code) == 0) {
     e->where = where;
     e->aux = aux;
+    e->label = label;
   }
 }
 

@@ -1,0 +1,91 @@
+// Host-side solver context: scan plans, device workspace and the LQR
+// factorization cache for one set of dimensions (gsls_ctx in include/gsls.h).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "plan.h"
+
+namespace gsls {
+
+constexpr size_t kReplaySmemMax = 220 * 1024;  // replay vectors live in smem up to this size
+
+// Device view of the cache, passed by value to kernels.
+struct DevLqr {
+  int n, m, c, nf, N, ldg, mtot;
+  // CVF plan (reverse scan over N+1 elements)
+  const int4* cvf_ops;
+  const int* cvf_out;
+  const int* cvf_loff;   // layer offsets (cvf_layers + 1)
+  int cvf_nslots, cvf_nops, cvf_layers;
+  // COT plan (forward scan over N elements)
+  const int4* cot_ops;
+  const int* cot_out;
+  const int* cot_loff;
+  int cot_nslots, cot_nops, cot_layers;
+  // scan values (matrices) per instance: [batch][slots][n*ldg]
+  float *Ps, *As, *Cs;   // CVF P, A, C
+  float* cvf_rec;        // [batch][cvf_nops][4][n*ldg]: Ups, Pr, Psi, Cl (column-major)
+  float* cotA;           // [batch][cot_nslots][n*ldg]
+  float* cot_rec;        // [batch][cot_nops][n*ldg]: A_later (column-major)
+  // per-stage cache, unpadded row-major: [batch][N][...]
+  float *Rhat, *Shat, *Rinv, *Gamma, *K;  // m*m, m*n, m*m, m*m, m*n
+  double* cvec;          // [batch][N][n]  P_{k+1} b_k
+  double* v0;            // [batch][n]     Abar_0 dx0
+  double* last_k;        // [batch][N][m]   feedforward of the last replay
+  double* last_p;        // [batch][N+1][n] cost-to-go gradients of the last replay
+  ErrSlot* err;          // [batch]
+};
+
+struct Ctx {
+  gsls_dims_t dims{};
+  int ldg = 0, mtot = 0;
+  ScanPlan cvf, cot;
+  std::vector<int> cvf_layer_off, cot_layer_off;  // host copies
+  int cvf_max_layer = 0, cot_max_layer = 0;
+  // device allocations
+  std::vector<void*> allocs;
+  int64_t bytes = 0;
+  DevLqr dev{};
+  int* d_inst_all = nullptr;   // 0..batch-1
+  int* d_inst_list = nullptr;  // scratch list (batch)
+  int32_t* d_status = nullptr; // [batch] per-instance ADMM exit status
+  double* d_scratch = nullptr; // global fallback for replay vectors
+  size_t scratch_floats = 0;   // per instance (doubles)
+  int generation = -1;         // cache stamp (single-generation API); -1 = none
+  std::vector<int> gen_host;   // per-instance stamp for the batched API
+  bool cache_valid = false;
+  void* sls = nullptr;         // SLS workspace (sls.cu), allocated on first use
+};
+
+// Matrix half of the CVF combine on an explicit slot space (lqr.cu); shared by
+// the LQR factorization (with aux record) and the SLS grid scan (without).
+struct CombineArgs {
+  int n;
+  const int4* ops;
+  int op_base;                 // global op index of ops[0] (record offset)
+  float *Ps, *As, *Cs;
+  long long inst_stride;       // floats between instances in Ps/As/Cs
+  float* rec;                  // nullptr: no record
+  long long rec_inst_stride;   // floats between instances in rec
+  const int* list;
+  ErrSlot* err;
+  float rel_tol;
+};
+int launch_combine(const CombineArgs& a, int nops, int count, cudaStream_t st);
+int combine_threads(int n);
+int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff);
+void sls_destroy(Ctx* c);
+
+void* dev_alloc(Ctx* c, size_t bytes);
+int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_list, int count,
+                cudaStream_t st);
+int check_errors(Ctx* c, cudaStream_t st, const char* what);
+
+// replay-kernel launch (admm.cu)
+struct ReplayArgs;
+size_t replay_smem_floats(const Ctx* c);
+
+}  // namespace gsls

@@ -1,0 +1,578 @@
+// LQR factorization ("cache build"): CVF leaves, CVF combine tree, gains,
+// COT combine tree.  Matrix work only — every vector (p, b, k, dx, du) is
+// produced by the replay kernel (admm.cu), so the full solve and the cached
+// solve run the same vector code and agree bitwise (lqr.py:419-454 contract).
+//
+// Reference map:
+//   k_leaf_init    _build_static / init_elements + ADMM augmentation
+//                  (lqr.py:297-335, admm.py:100-110)
+//   k_cvf_combine  _cvf_matrix_core + aux record (lqr.py:226-254)
+//   k_gains        Gamma, K, Abar, COT leaves (lqr.py:398-404, :349-356)
+//   k_cot_combine  cot_kernel + aux record (lqr.py:273-278)
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "ctx.h"
+#include "smallmat.cuh"
+
+namespace gsls {
+
+// ---------------------------------------------------------------------------
+// error plumbing shared by all translation units
+
+static std::mutex g_err_mu;
+static gsls_error_t g_err{};
+
+void set_last_error(const char* msg, const char* file, int line) {
+  std::lock_guard<std::mutex> g(g_err_mu);
+  g_err.code = GSLS_ERR_CUDA;
+  g_err.instance = -1;
+  snprintf(g_err.message, sizeof(g_err.message), "%s (%s:%d)", msg, file, line);
+}
+
+void set_error(int code, int inst, int where, int aux, int label, const char* msg) {
+  std::lock_guard<std::mutex> g(g_err_mu);
+  g_err.code = code;
+  g_err.instance = inst;
+  g_err.where = where;
+  g_err.aux = aux;
+  g_err.aux2 = label;
+  snprintf(g_err.message, sizeof(g_err.message), "%s", msg);
+}
+
+int get_last_error(gsls_error_t* out) {
+  std::lock_guard<std::mutex> g(g_err_mu);
+  *out = g_err;
+  return g_err.code;
+}
+
+void* dev_alloc(Ctx* c, size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  cudaMemset(p, 0, bytes);
+  c->allocs.push_back(p);
+  c->bytes += (int64_t)bytes;
+  return p;
+}
+
+static const char* label_text(int label) {
+  switch (label) {
+    case GSLS_LABEL_R: return "R";
+    case GSLS_LABEL_R_BPB: return "R + B'PB";
+    case GSLS_LABEL_QU: return "Qu";
+    case GSLS_LABEL_QU_BPB: return "Qu + B'PB";
+    default: return "matrix";
+  }
+}
+
+// Copies per-instance error slots to the host; raises the first one found.
+int check_errors(Ctx* c, cudaStream_t st, const char* what) {
+  const int B = c->dims.batch;
+  std::vector<ErrSlot> h(B);
+  GSLS_CUDA_CHECK(cudaMemcpyAsync(h.data(), c->dev.err, sizeof(ErrSlot) * B, cudaMemcpyDeviceToHost, st));
+  GSLS_CUDA_CHECK(cudaStreamSynchronize(st));
+  for (int i = 0; i < B; ++i) {
+    if (h[i].code == 0) continue;
+    char msg[256];
+    if (h[i].code == GSLS_ERR_SINGULAR_STAGE) {
+      if (h[i].aux >= 0)
+        snprintf(msg, sizeof msg, "singular %s block at (k=%d, j=%d)", label_text(h[i].label), h[i].where, h[i].aux);
+      else
+        snprintf(msg, sizeof msg, "singular %s at stage %d", label_text(h[i].label), h[i].where);
+    } else if (h[i].code == GSLS_ERR_ILL_CONDITIONED) {
+      snprintf(msg, sizeof msg, "ill-conditioned combine");
+    } else if (h[i].code == GSLS_ERR_NONFINITE) {
+      snprintf(msg, sizeof msg, "non-finite %s at stage %d",
+               h[i].label == GSLS_LABEL_NONFINITE_CON ? "constraints" : "dynamics", h[i].where);
+    } else {
+      snprintf(msg, sizeof msg, "%s failed", what);
+    }
+    set_error(h[i].code, i, h[i].where, h[i].aux, h[i].label, msg);
+    cudaMemsetAsync(c->dev.err, 0, sizeof(ErrSlot) * B, st);
+    return h[i].code;
+  }
+  return GSLS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+
+__device__ inline int inst_of(const int* list) { return list ? list[blockIdx.y] : (int)blockIdx.y; }
+
+// CVF leaves (Eq. 29) with penalty augmentation rho (0 for a plain LQR).
+__global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const double* rho_arr,
+                                                   const int* list) {
+  const int inst = inst_of(list);
+  const int k = blockIdx.x;
+  const int n = L.n, m = L.m, c = L.c, nf = L.nf, N = L.N, ldg = L.ldg;
+  const float rho = rho_arr ? (float)rho_arr[inst] : 0.f;
+  const size_t MS = (size_t)n * ldg;
+  const size_t sbase = ((size_t)inst * L.cvf_nslots + k) * MS;
+  float* Pd = L.Ps + sbase;
+  float* Ad = L.As + sbase;
+  float* Cd = L.Cs + sbase;
+  if (k == N) {
+    const float* QN = qp.QN + (size_t)inst * n * n;
+    const float* CN = qp.CN + (size_t)inst * nf * n;
+    for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
+      const int i = e / ldg, j = e - i * ldg;
+      float v = 0.f;
+      if (j < n) {
+        float s = 0.f;
+        for (int f = 0; f < nf; ++f) s = fmaf(CN[f * n + i], CN[f * n + j], s);
+        v = QN[i * n + j] + rho * s;
+      }
+      Pd[e] = v;
+      Ad[e] = 0.f;
+      Cd[e] = 0.f;
+    }
+    return;
+  }
+  extern __shared__ float sm[];
+  float* Cst = sm;                  // c x n
+  float* Dst = Cst + c * n;         // c x m
+  float* Bst = Dst + c * m;         // n x m
+  float* Sh = Bst + n * m;          // m x n
+  float* Rh = Sh + m * n;           // m x m
+  float* Ri = Rh + m * m;           // m x m
+  float* RS = Ri + m * m;           // m x n
+  float* BR = RS + m * n;           // n x m
+  float* wk = BR + n * m;           // spd work
+  const size_t st = (size_t)inst * N + k;
+  const float* Cg = qp.C + st * c * n;
+  const float* Dg = qp.D + st * c * m;
+  const float* Bg = qp.B + st * n * m;
+  for (int e = threadIdx.x; e < c * n; e += blockDim.x) Cst[e] = Cg[e];
+  for (int e = threadIdx.x; e < c * m; e += blockDim.x) Dst[e] = Dg[e];
+  for (int e = threadIdx.x; e < n * m; e += blockDim.x) Bst[e] = Bg[e];
+  __syncthreads();
+  const float* Rg = qp.R + st * m * m;
+  const float* Sg = qp.S ? qp.S + st * m * n : nullptr;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int i = e / m, j = e - i * m;
+    float s = 0.f;
+    for (int r = 0; r < c; ++r) s = fmaf(Dst[r * m + i], Dst[r * m + j], s);
+    Rh[e] = Rg[e] + rho * s;
+  }
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    float s = 0.f;
+    for (int r = 0; r < c; ++r) s = fmaf(Dst[r * m + i], Cst[r * n + j], s);
+    Sh[e] = (Sg ? Sg[e] : 0.f) + rho * s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    if (warp_spd_inverse(Rh, m, Ri, m, wk) && threadIdx.x == 0)
+      raise_err(L.err + inst, GSLS_ERR_SINGULAR_STAGE, k, -1, GSLS_LABEL_R);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+    const int l = e / n, j = e - l * n;
+    float s = 0.f;
+    for (int t = 0; t < m; ++t) s = fmaf(Ri[l * m + t], Sh[t * n + j], s);
+    RS[e] = s;
+  }
+  for (int e = threadIdx.x; e < n * m; e += blockDim.x) {
+    const int i = e / m, l = e - i * m;
+    float s = 0.f;
+    for (int t = 0; t < m; ++t) s = fmaf(Bst[i * m + t], Ri[t * m + l], s);
+    BR[e] = s;
+  }
+  __syncthreads();
+  const float* Qg = qp.Q + st * n * n;
+  const float* Ag = qp.A + st * n * n;
+  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
+    const int i = e / ldg, j = e - i * ldg;
+    float p = 0.f, a = 0.f, cc = 0.f;
+    if (j < n) {
+      float s = 0.f;
+      for (int r = 0; r < c; ++r) s = fmaf(Cst[r * n + i], Cst[r * n + j], s);
+      const float qh = Qg[i * n + j] + rho * s;
+      float sr = 0.f, br = 0.f, bb = 0.f;
+      for (int l = 0; l < m; ++l) {
+        sr = fmaf(Sh[l * n + i], RS[l * n + j], sr);
+        br = fmaf(Bst[i * m + l], RS[l * n + j], br);
+        bb = fmaf(BR[i * m + l], Bst[j * m + l], bb);
+      }
+      p = qh - sr;
+      a = Ag[i * n + j] - br;
+      cc = bb;
+    }
+    Pd[e] = p;
+    Ad[e] = a;
+    Cd[e] = cc;
+  }
+  float* Rhat = L.Rhat + st * m * m;
+  float* Shat = L.Shat + st * m * n;
+  float* Rinv = L.Rinv + st * m * m;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) { Rhat[e] = Rh[e]; Rinv[e] = Ri[e]; }
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) Shat[e] = Sh[e];
+}
+
+// Matrix half of the CVF combine (Eq. 28) for one op per CTA; optionally
+// records (Ups, Pr, Psi, Cl) column-major for the replay.
+__global__ void __launch_bounds__(512, 1) k_cvf_combine(CombineArgs a) {
+  const int inst = inst_of(a.list);
+  const int4 op = a.ops[blockIdx.x];
+  const int n = a.n, ldg = ldg_of(n), lds = lds_of(n);
+  const size_t MS = (size_t)n * ldg;
+  const size_t BS = (size_t)n * lds;
+  extern __shared__ float sm[];
+  float* b0 = sm;            // Pr^T -> Cl^T -> Ups^T
+  float* b1 = b0 + BS;       // Cl -> Minv
+  float* b2 = b1 + BS;       // Al
+  float* b3 = b2 + BS;       // Ar^T
+  float* b4 = b3 + BS;       // M1 -> Minv^T
+  float* b5 = b4 + BS;       // W1 -> Psi^T
+  float* b6 = b5 + BS;       // W2
+  float* gjbuf = b6 + BS;
+  const long long ib = (long long)inst * a.inst_stride;
+  const float* PE = a.Ps + ib + (size_t)op.y * MS;  // earlier (left)
+  const float* AE = a.As + ib + (size_t)op.y * MS;
+  const float* CE = a.Cs + ib + (size_t)op.y * MS;
+  const float* PL = a.Ps + ib + (size_t)op.z * MS;  // later (right)
+  const float* AL_ = a.As + ib + (size_t)op.z * MS;
+  const float* CL_ = a.Cs + ib + (size_t)op.z * MS;
+  float* PD = a.Ps + ib + (size_t)op.x * MS;
+  float* AD = a.As + ib + (size_t)op.x * MS;
+  float* CD = a.Cs + ib + (size_t)op.x * MS;
+  float* rec = a.rec ? a.rec + (long long)inst * a.rec_inst_stride + (size_t)(a.op_base + blockIdx.x) * 4 * MS
+                     : nullptr;
+
+  cta_load_t(b0, lds, PL, ldg, n);   // Pr^T
+  cta_load(b1, lds, CE, ldg, n, n);  // Cl
+  cta_load(b2, lds, AE, ldg, n, n);  // Al
+  cta_load_t(b3, lds, AL_, ldg, n);  // Ar^T
+  __syncthreads();
+  gemm_tn(n, b0, b1, lds, EpiSmem{b4, lds, true});    // M1 = I + Pr Cl
+  gemm_tn(n, b0, b2, lds, EpiSmem{b5, lds, false});   // W1 = Pr Al
+  if (rec) cta_store(rec + 1 * MS, b0, lds, n);        // Pr (column-major)
+  __syncthreads();
+  cta_transpose(b0, b1, lds, n);                        // Cl^T
+  __syncthreads();
+  gemm_tn(n, b0, b3, lds, EpiSmem{b6, lds, false});   // W2 = Cl Ar^T
+  if (rec) cta_store(rec + 3 * MS, b0, lds, n);        // Cl (column-major)
+  __syncthreads();
+  const bool ok = gj_inverse(b4, b1, lds, n, gjbuf, a.rel_tol);  // Minv = M1^{-1} -> b1
+  if (!ok && threadIdx.x == 0)
+    raise_err(a.err ? a.err + inst : nullptr, GSLS_ERR_ILL_CONDITIONED, a.op_base + blockIdx.x);
+  cta_transpose(b4, b1, lds, n);                        // Minv^T -> b4
+  gemm_tn(n, b1, b2, lds, EpiSmem{b0, lds, false});   // Ups^T = Minv^T Al
+  __syncthreads();
+  if (rec) cta_store(rec + 0 * MS, b0, lds, n);        // Ups (column-major)
+  gemm_tn(n, b0, b5, lds, EpiGlobal{PD, PE, ldg});    // P = Ups W1 + Pl
+  __syncthreads();
+  gemm_tn(n, b4, b3, lds, EpiSmem{b5, lds, false});   // Psi^T = Minv Ar^T
+  __syncthreads();
+  if (rec) cta_store(rec + 2 * MS, b5, lds, n);        // Psi (column-major)
+  gemm_tn(n, b5, b2, lds, EpiGlobal{AD, nullptr, ldg}); // A = Psi Al
+  gemm_tn(n, b5, b6, lds, EpiGlobal{CD, CL_, ldg});    // C = Psi W2 + Cr
+}
+
+size_t combine_smem_bytes(int n) {
+  return (7 * (size_t)n * lds_of(n) + 3 * ldg_of(n) + 2 * n + 8) * sizeof(float);
+}
+
+int combine_threads(int n) {
+  const int T = ldg_of(n) / 4;
+  int t = ((T * T + 31) / 32) * 32;
+  if (t < 128) t = 128;
+  if (t > 512) t = 512;
+  return t;
+}
+
+// Gains, closed loop and COT leaves per stage (lqr.py:398-404, :349-356).
+__global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const int* list) {
+  const int inst = inst_of(list);
+  const int k = blockIdx.x;
+  const int n = L.n, m = L.m, N = L.N, ldg = L.ldg;
+  const size_t MS = (size_t)n * ldg;
+  extern __shared__ float sm[];
+  float* Pn = sm;               // n x ldg
+  float* Bst = Pn + n * ldg;    // n x m
+  float* BtP = Bst + n * m;     // m x n
+  float* H = BtP + m * n;       // m x m
+  float* Gm = H + m * m;        // m x n
+  float* Ga = Gm + m * n;       // m x m
+  float* Ks = Ga + m * m;       // m x n
+  float* wk = Ks + m * n;
+  const size_t st = (size_t)inst * N + k;
+  const float* Pg = L.Ps + ((size_t)inst * L.cvf_nslots + L.cvf_out[k + 1]) * MS;
+  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) Pn[e] = Pg[e];
+  const float* Bg = qp.B + st * n * m;
+  for (int e = threadIdx.x; e < n * m; e += blockDim.x) Bst[e] = Bg[e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+    const int l = e / n, j = e - l * n;
+    float s = 0.f;
+    for (int i = 0; i < n; ++i) s = fmaf(Bst[i * m + l], Pn[i * ldg + j], s);
+    BtP[e] = s;
+  }
+  __syncthreads();
+  const float* Ag = qp.A + st * n * n;
+  const float* Rhat = L.Rhat + st * m * m;
+  const float* Shat = L.Shat + st * m * n;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int l = e / m, t = e - l * m;
+    float s = 0.f;
+    for (int j = 0; j < n; ++j) s = fmaf(BtP[l * n + j], Bst[j * m + t], s);
+    H[e] = Rhat[e] + s;
+  }
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+    const int l = e / n, j = e - l * n;
+    float s = 0.f;
+    for (int i = 0; i < n; ++i) s = fmaf(BtP[l * n + i], Ag[i * n + j], s);
+    Gm[e] = Shat[e] + s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    if (warp_spd_inverse(H, m, Ga, m, wk) && threadIdx.x == 0)
+      raise_err(L.err + inst, GSLS_ERR_SINGULAR_STAGE, k, -1, GSLS_LABEL_R_BPB);
+  }
+  __syncthreads();
+  float* Kg = L.K + st * m * n;
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+    const int l = e / n, j = e - l * n;
+    float s = 0.f;
+    for (int t = 0; t < m; ++t) s = fmaf(Ga[l * m + t], Gm[t * n + j], s);
+    Ks[e] = -s;
+    Kg[e] = -s;
+  }
+  float* Gg = L.Gamma + st * m * m;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) Gg[e] = Ga[e];
+  const double* bg = qp.b + st * n;
+  double* cv = L.cvec + st * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s = fma((double)Pn[i * ldg + j], bg[j], s);
+    cv[i] = s;
+  }
+  __syncthreads();
+  // closed loop Abar = A + B K -> COT leaf k (leaf 0 carries A = 0, lqr.py:354)
+  float* Ad = L.cotA + ((size_t)inst * L.cot_nslots + k) * MS;
+  float* Abar = Pn;  // reuse (Pn no longer needed)
+  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
+    const int i = e / ldg, j = e - i * ldg;
+    float v = 0.f;
+    if (j < n) {
+      float s = 0.f;
+      for (int l = 0; l < m; ++l) s = fmaf(Bst[i * m + l], Ks[l * n + j], s);
+      v = Ag[i * n + j] + s;
+    }
+    Abar[e] = v;
+    Ad[e] = (k == 0) ? 0.f : v;
+  }
+  if (k == 0) {
+    __syncthreads();
+    const double* dx0 = qp.dx0 + (size_t)inst * n;
+    double* v0 = L.v0 + (size_t)inst * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double s = 0.0;
+      for (int j = 0; j < n; ++j) s = fma((double)Abar[i * ldg + j], dx0[j], s);
+      v0[i] = s;
+    }
+  }
+}
+
+// COT combine: A = A_later A_earlier; records A_later column-major.
+__global__ void __launch_bounds__(512) k_cot_combine(DevLqr L, const int4* ops, int op_base, const int* list) {
+  const int inst = inst_of(list);
+  const int4 op = ops[blockIdx.x];
+  const int n = L.n, ldg = L.ldg, lds = lds_of(n);
+  const size_t MS = (size_t)n * ldg;
+  extern __shared__ float sm[];
+  float* Art = sm;
+  float* Ae = Art + (size_t)n * lds;
+  const float* base = L.cotA + (size_t)inst * L.cot_nslots * MS;
+  cta_load_t(Art, lds, base + (size_t)op.z * MS, ldg, n);
+  cta_load(Ae, lds, base + (size_t)op.y * MS, ldg, n, n);
+  __syncthreads();
+  float* rec = L.cot_rec + ((size_t)inst * L.cot_nops + op_base + blockIdx.x) * MS;
+  cta_store(rec, Art, lds, n);
+  gemm_tn(n, Art, Ae, lds, EpiGlobal{L.cotA + (size_t)inst * L.cot_nslots * MS + (size_t)op.x * MS, nullptr, ldg});
+}
+
+// ---------------------------------------------------------------------------
+// host driver
+
+static size_t leaf_smem_bytes(int n, int m, int c) {
+  return (size_t)(c * n + c * m + n * m + m * n + 2 * m * m + m * n + n * m + 2 * kMaxM * (kMaxM + 1) + 8 + m * m) *
+         sizeof(float);
+}
+static size_t gains_smem_bytes(int n, int m) {
+  return (size_t)(n * ldg_of(n) + n * m + m * n + m * m + m * n + m * m + m * n + 2 * kMaxM * (kMaxM + 1) + 8) *
+         sizeof(float);
+}
+
+static int set_smem(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    GSLS_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  }
+  return GSLS_OK;
+}
+
+int launch_combine(const CombineArgs& a, int nops, int count, cudaStream_t st) {
+  if (nops == 0 || count == 0) return GSLS_OK;
+  const size_t sb = combine_smem_bytes(a.n);
+  int rc = set_smem((const void*)k_cvf_combine, sb);
+  if (rc) return rc;
+  k_cvf_combine<<<dim3(nops, count), combine_threads(a.n), sb, st>>>(a);
+  GSLS_CUDA_CHECK(cudaGetLastError());
+  return GSLS_OK;
+}
+
+int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_list, int count, cudaStream_t st) {
+  const gsls_dims_t& d = c->dims;
+  DevLqr& L = c->dev;
+  if (count == 0) return GSLS_OK;
+  const int n = d.nx, N = d.N;
+  // leaves
+  {
+    const size_t sb = leaf_smem_bytes(n, d.nu, d.nc);
+    int rc = set_smem((const void*)k_leaf_init, sb);
+    if (rc) return rc;
+    k_leaf_init<<<dim3(N + 1, count), 256, sb, st>>>(L, *qp, d_rho, d_list);
+    GSLS_CUDA_CHECK(cudaGetLastError());
+  }
+  // CVF tree
+  const size_t MS = mat_elems(n);
+  for (int l = 0; l < c->cvf.layers; ++l) {
+    const int o0 = c->cvf_layer_off[l], o1 = c->cvf_layer_off[l + 1];
+    CombineArgs a{n, L.cvf_ops + o0, o0, L.Ps, L.As, L.Cs, (long long)L.cvf_nslots * (long long)MS,
+                  L.cvf_rec, (long long)L.cvf_nops * 4 * (long long)MS, d_list, L.err, 1e-10f};
+    int rc = launch_combine(a, o1 - o0, count, st);
+    if (rc) return rc;
+  }
+  if (N == 0) return GSLS_OK;
+  // gains / COT leaves
+  {
+    const size_t sb = gains_smem_bytes(n, d.nu);
+    int rc = set_smem((const void*)k_gains, sb);
+    if (rc) return rc;
+    k_gains<<<dim3(N, count), 256, sb, st>>>(L, *qp, d_list);
+    GSLS_CUDA_CHECK(cudaGetLastError());
+  }
+  // COT tree
+  {
+    const size_t sb = 2 * (size_t)n * lds_of(n) * sizeof(float);
+    int rc = set_smem((const void*)k_cot_combine, sb);
+    if (rc) return rc;
+    for (int l = 0; l < c->cot.layers; ++l) {
+      const int o0 = c->cot_layer_off[l], o1 = c->cot_layer_off[l + 1];
+      if (o1 == o0) continue;
+      k_cot_combine<<<dim3(o1 - o0, count), combine_threads(n), sb, st>>>(L, L.cot_ops + o0, o0, d_list);
+      GSLS_CUDA_CHECK(cudaGetLastError());
+    }
+  }
+  return GSLS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// context
+
+int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff) {
+  std::vector<int4> h(p.ops.size() ? p.ops.size() : 1);
+  for (size_t i = 0; i < p.ops.size(); ++i) h[i] = make_int4(p.ops[i].dst, p.ops[i].earlier, p.ops[i].later, 0);
+  int4* dops = (int4*)dev_alloc(c, h.size() * sizeof(int4));
+  int* dout = (int*)dev_alloc(c, (p.out.size() + 1) * sizeof(int));
+  int* dl = (int*)dev_alloc(c, (p.layer_off.size() + 1) * sizeof(int));
+  if (!dops || !dout || !dl) return GSLS_ERR_CUDA;
+  GSLS_CUDA_CHECK(cudaMemcpy(dops, h.data(), h.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  if (!p.out.empty()) GSLS_CUDA_CHECK(cudaMemcpy(dout, p.out.data(), p.out.size() * sizeof(int), cudaMemcpyHostToDevice));
+  if (!p.layer_off.empty())
+    GSLS_CUDA_CHECK(cudaMemcpy(dl, p.layer_off.data(), p.layer_off.size() * sizeof(int), cudaMemcpyHostToDevice));
+  *ops = dops;
+  *out = dout;
+  *loff = dl;
+  return GSLS_OK;
+}
+
+int ctx_create(const gsls_dims_t* dims, Ctx** out) {
+  const gsls_dims_t d = *dims;
+  if (d.nx < 1 || d.nu < 0 || d.nc < 0 || d.nf < 0 || d.N < 0 || d.batch < 1) {
+    set_error(GSLS_ERR_ARG, -1, 0, 0, 0, "invalid dimensions");
+    return GSLS_ERR_ARG;
+  }
+  if (d.nx > kMaxN || d.nu > kMaxM || (d.N > 0 && d.nu < 1)) {
+    set_error(GSLS_ERR_TOO_LARGE, -1, 0, 0, 0, "dimensions exceed compiled limits (nx<=80, 1<=nu<=24)");
+    return GSLS_ERR_TOO_LARGE;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    set_error(GSLS_ERR_NO_DEVICE, -1, 0, 0, 0, "no CUDA device");
+    return GSLS_ERR_NO_DEVICE;
+  }
+  Ctx* c = new Ctx();
+  c->dims = d;
+  c->ldg = ldg_of(d.nx);
+  c->mtot = d.N * d.nc + d.nf;
+  c->cvf = make_scan_plan(d.N + 1, true);
+  c->cot = d.N > 0 ? make_scan_plan(d.N, false) : ScanPlan{};
+  c->cvf_layer_off = c->cvf.layer_off;
+  c->cot_layer_off = c->cot.layer_off;
+  if (c->cot_layer_off.empty()) c->cot_layer_off.push_back(0);
+  for (int l = 0; l < c->cvf.layers; ++l)
+    c->cvf_max_layer = std::max(c->cvf_max_layer, c->cvf_layer_off[l + 1] - c->cvf_layer_off[l]);
+  for (int l = 0; l < c->cot.layers; ++l)
+    c->cot_max_layer = std::max(c->cot_max_layer, c->cot_layer_off[l + 1] - c->cot_layer_off[l]);
+
+  DevLqr& L = c->dev;
+  L.n = d.nx; L.m = d.nu; L.c = d.nc; L.nf = d.nf; L.N = d.N; L.ldg = c->ldg; L.mtot = c->mtot;
+  int rc = upload_plan(c, c->cvf, &L.cvf_ops, &L.cvf_out, &L.cvf_loff);
+  if (!rc && d.N > 0) rc = upload_plan(c, c->cot, &L.cot_ops, &L.cot_out, &L.cot_loff);
+  if (rc) { delete c; return rc; }
+  L.cvf_nslots = c->cvf.nslots;
+  L.cvf_nops = (int)c->cvf.ops.size();
+  L.cvf_layers = c->cvf.layers;
+  L.cot_nslots = c->cot.nslots;
+  L.cot_nops = (int)c->cot.ops.size();
+  L.cot_layers = c->cot.layers;
+  const size_t B = d.batch, MS = mat_elems(d.nx), n = d.nx, m = d.nu, N = d.N;
+  L.Ps = (float*)dev_alloc(c, B * L.cvf_nslots * MS * 4);
+  L.As = (float*)dev_alloc(c, B * L.cvf_nslots * MS * 4);
+  L.Cs = (float*)dev_alloc(c, B * L.cvf_nslots * MS * 4);
+  L.cvf_rec = (float*)dev_alloc(c, B * L.cvf_nops * 4 * MS * 4);
+  L.cotA = (float*)dev_alloc(c, B * L.cot_nslots * MS * 4);
+  L.cot_rec = (float*)dev_alloc(c, B * L.cot_nops * MS * 4);
+  L.Rhat = (float*)dev_alloc(c, B * N * m * m * 4);
+  L.Shat = (float*)dev_alloc(c, B * N * m * n * 4);
+  L.Rinv = (float*)dev_alloc(c, B * N * m * m * 4);
+  L.Gamma = (float*)dev_alloc(c, B * N * m * m * 4);
+  L.K = (float*)dev_alloc(c, B * N * m * n * 4);
+  L.cvec = (double*)dev_alloc(c, B * N * n * 8);
+  L.v0 = (double*)dev_alloc(c, B * n * 8);
+  L.last_k = (double*)dev_alloc(c, B * N * m * 8);
+  L.last_p = (double*)dev_alloc(c, B * (N + 1) * n * 8);
+  L.err = (ErrSlot*)dev_alloc(c, B * sizeof(ErrSlot));
+  c->d_inst_all = (int*)dev_alloc(c, B * sizeof(int));
+  c->d_inst_list = (int*)dev_alloc(c, B * sizeof(int));
+  c->d_status = (int32_t*)dev_alloc(c, B * sizeof(int32_t));
+  c->scratch_floats = replay_smem_floats(c);  // doubles
+  if (c->scratch_floats * 8 > kReplaySmemMax) c->d_scratch = (double*)dev_alloc(c, B * c->scratch_floats * 8);
+  bool fail = !L.Ps || !L.As || !L.Cs || !L.cvf_rec || !L.cotA || !L.cot_rec || !L.Rhat || !L.Shat || !L.Rinv ||
+              !L.Gamma || !L.K || !L.cvec || !L.v0 || !L.last_k || !L.last_p || !L.err || !c->d_inst_all || !c->d_inst_list || !c->d_status ||
+              (c->scratch_floats * 8 > kReplaySmemMax && !c->d_scratch);
+  if (fail) {
+    for (void* p : c->allocs) cudaFree(p);
+    delete c;
+    set_error(GSLS_ERR_CUDA, -1, 0, 0, 0, "device allocation failed");
+    return GSLS_ERR_CUDA;
+  }
+  std::vector<int> all(B);
+  for (size_t i = 0; i < B; ++i) all[i] = (int)i;
+  GSLS_CUDA_CHECK(cudaMemcpy(c->d_inst_all, all.data(), B * sizeof(int), cudaMemcpyHostToDevice));
+  c->gen_host.assign(B, -1);
+  *out = c;
+  return GSLS_OK;
+}
+
+void ctx_destroy(Ctx* c) {
+  if (!c) return;
+  if (c->sls) sls_destroy(c);
+  for (void* p : c->allocs) cudaFree(p);
+  delete c;
+}
+
+}  // namespace gsls

@@ -1,0 +1,266 @@
+// CTA-level dense kernels for n <= 80 matrices held in shared memory.
+//
+// * gemm_tn      C = At^T * B with At stored k-major (At[k][i]) and B row-major,
+//                4x4 register tiles, both operands read as float4 (the left
+//                operand is broadcast across a warp, the right one contiguous).
+// * gj_inverse   in-place Gauss-Jordan inverse with partial pivoting (argmax
+//                |a_ik|, first index on ties, as LAPACK i*amax) — replaces the
+//                reference's solve(M1^T, .) / solve(M2^T, .) pair, lqr.py:233-235.
+// * warp_spd_inverse  Cholesky + explicit inverse with the reference pivot /
+//                ridge rule (lqr.py:185-220) for m <= 24 blocks, one warp.
+#pragma once
+
+#include "common.cuh"
+
+namespace gsls {
+
+// ---- loads / stores between global (ld = ldg) and shared (ld = lds) ----------
+
+// dst[i][j] = src[i][j] for i < rows, j < cols; zero for cols <= j < ldg(cols)
+__device__ inline void cta_load(float* dst, int lds, const float* __restrict__ src, int lsrc, int rows,
+                                int cols) {
+  const int cp = ldg_of(cols);
+  for (int e = threadIdx.x; e < rows * cp; e += blockDim.x) {
+    const int i = e / cp, j = e - i * cp;
+    dst[i * lds + j] = (j < cols) ? src[(size_t)i * lsrc + j] : 0.f;
+  }
+}
+
+// dst[j][i] = src[i][j] (square n x n); padding columns of dst zeroed.
+__device__ inline void cta_load_t(float* dst, int lds, const float* __restrict__ src, int lsrc, int n) {
+  const int np = ldg_of(n);
+  for (int e = threadIdx.x; e < n * np; e += blockDim.x) {
+    const int i = e / np, j = e - i * np;  // i: src row, j: src col (coalesced read)
+    if (j < n) dst[j * lds + i] = src[(size_t)i * lsrc + j];
+    else dst[i * lds + j] = 0.f;  // row i, padding column j of dst
+  }
+}
+
+// smem -> smem transpose of the n x n block; padding columns of dst zeroed.
+__device__ inline void cta_transpose(float* dst, const float* src, int lds, int n) {
+  const int np = ldg_of(n);
+  for (int e = threadIdx.x; e < n * np; e += blockDim.x) {
+    const int i = e / np, j = e - i * np;
+    dst[i * lds + j] = (j < n) ? src[j * lds + i] : 0.f;
+  }
+}
+
+// smem (lds) -> global (ldg) copy of an n x ldg(n) block, float4 rows.
+__device__ inline void cta_store(float* __restrict__ dst, const float* src, int lds, int n) {
+  const int q = ldg_of(n) / 4;
+  for (int e = threadIdx.x; e < n * q; e += blockDim.x) {
+    const int i = e / q, j = (e - i * q) * 4;
+    *reinterpret_cast<float4*>(dst + (size_t)i * ldg_of(n) + j) = *reinterpret_cast<const float4*>(src + i * lds + j);
+  }
+}
+
+// ---- GEMM ---------------------------------------------------------------------
+
+// C[i][j] = sum_{k<n} At[k][i] * B[k][j] over the padded np x np output; the
+// epilogue is called once per tile row: epi(i, j0, float4) for i < n.
+template <class Epi>
+__device__ inline void gemm_tn(int n, const float* At, const float* B, int lds, Epi epi) {
+  const int T = ldg_of(n) >> 2;
+  const int tiles = T * T;
+  for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+    const int ti = t / T, tj = t - ti * T;
+    float acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+    const float* pa = At + 4 * ti;
+    const float* pb = B + 4 * tj;
+#pragma unroll 4
+    for (int k = 0; k < n; ++k) {
+      const float4 a = *reinterpret_cast<const float4*>(pa + k * lds);
+      const float4 b = *reinterpret_cast<const float4*>(pb + k * lds);
+      const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        acc[r][0] = fmaf(av[r], b.x, acc[r][0]);
+        acc[r][1] = fmaf(av[r], b.y, acc[r][1]);
+        acc[r][2] = fmaf(av[r], b.z, acc[r][2]);
+        acc[r][3] = fmaf(av[r], b.w, acc[r][3]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = 4 * ti + r;
+      if (i < n) epi(i, 4 * tj, make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]));
+    }
+  }
+}
+
+// epilogues
+struct EpiSmem {  // C (smem) = acc (+ I)
+  float* C;
+  int lds;
+  bool add_identity;
+  __device__ void operator()(int i, int j, float4 v) const {
+    if (add_identity && i >= j && i < j + 4) (&v.x)[i - j] += 1.f;
+    *reinterpret_cast<float4*>(C + i * lds + j) = v;
+  }
+};
+
+struct EpiGlobal {  // G (global, ld) = acc + add (global, may be null)
+  float* G;
+  const float* add;
+  int ld;
+  __device__ void operator()(int i, int j, float4 v) const {
+    if (add) {
+      const float4 a = *reinterpret_cast<const float4*>(add + (size_t)i * ld + j);
+      v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+    }
+    *reinterpret_cast<float4*>(G + (size_t)i * ld + j) = v;
+  }
+};
+
+// ---- Gauss-Jordan inverse -------------------------------------------------------
+
+// Scratch: buf needs 3*ldg(n) floats + 2*n ints (after the floats).
+// Returns (block-uniform) false when a pivot is zero / non-finite / below
+// rel_tol * max|a| (the ill-conditioned-combine rule, lqr.py:229-232).
+__device__ inline bool gj_inverse(float* a, float* out, int lds, int n, float* buf, float rel_tol) {
+  const int np = ldg_of(n);
+  float* rbuf = buf;
+  float* fbuf = buf + np;
+  float* misc = buf + 2 * np;           // misc[0]: max|a|, misc[1]: fail flag
+  int* perm = reinterpret_cast<int*>(buf + 3 * np);
+  int* src = perm + n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+
+  // max |a| for the relative pivot threshold
+  if (warp == 0) {
+    float mx = 0.f;
+    for (int e = lane; e < n * n; e += 32) mx = fmaxf(mx, fabsf(a[(e / n) * lds + e % n]));
+    mx = warp_max(mx);
+    if (lane == 0) { misc[0] = mx; misc[1] = 0.f; }
+  }
+  __syncthreads();
+  const float thresh = rel_tol * misc[0];
+
+  for (int k = 0; k < n; ++k) {
+    if (warp == 0) {
+      float best = -1.f;
+      int bi = n;
+      for (int i = k + lane; i < n; i += 32) {
+        const float v = fabsf(a[i * lds + k]);
+        if (v > best) { best = v; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      const int p = bi;
+      if (p != k) {
+        for (int j = lane; j < n; j += 32) {
+          const float t = a[k * lds + j];
+          a[k * lds + j] = a[p * lds + j];
+          a[p * lds + j] = t;
+        }
+      }
+      __syncwarp();
+      const float piv = a[k * lds + k];
+      if (lane == 0) {
+        perm[k] = p;
+        if (!(fabsf(piv) > thresh) || !isfinite(piv)) misc[1] = 1.f;
+      }
+      const float inv = 1.f / piv;
+      for (int j = lane; j < n; j += 32) rbuf[j] = (j == k) ? inv : a[k * lds + j] * inv;
+      for (int i = lane; i < n; i += 32) fbuf[i] = (i == k) ? 0.f : a[i * lds + k];
+    }
+    __syncthreads();
+    for (int i = warp; i < n; i += nw) {
+      const float f = fbuf[i];
+      for (int j = lane; j < n; j += 32) {
+        if (i == k) a[i * lds + j] = rbuf[j];
+        else if (j == k) a[i * lds + j] = -f * rbuf[k];
+        else a[i * lds + j] = fmaf(-f, rbuf[j], a[i * lds + j]);
+      }
+    }
+    __syncthreads();
+  }
+  // undo the row interchanges as a column permutation (applied last-to-first)
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < n; ++j) src[j] = j;
+    for (int k = n - 1; k >= 0; --k) {
+      const int p = perm[k];
+      const int t = src[k];
+      src[k] = src[p];
+      src[p] = t;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * np; e += blockDim.x) {
+    const int i = e / np, j = e - i * np;
+    out[i * lds + j] = (j < n) ? a[i * lds + src[j]] : 0.f;
+  }
+  __syncthreads();
+  return misc[1] == 0.f;
+}
+
+// ---- SPD inverse (one warp, m <= 24) ---------------------------------------------
+
+// M (ld = ldm) is read; inv (ld = ldm) is written.  work: 2 * 24 * 25 floats.
+// Returns 0 ok, 1 singular (after the ridge retry).  Pivot rule of lqr.py:185-220:
+// Cholesky; min pivot^2 < 1e-10 or failure -> retry with ridge 1e-9 (no pivot
+// test) -> failure is SingularStageError.
+__device__ inline int warp_spd_inverse(const float* M, int ldm, float* inv, int m, float* work) {
+  const int lane = threadIdx.x & 31;
+  const int ld = kMaxM + 1;
+  float* L = work;
+  float* X = work + kMaxM * ld;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const float ridge = attempt ? 1e-9f : 0.f;
+    for (int e = lane; e < m * m; e += 32) {
+      const int i = e / m, j = e % m;
+      L[i * ld + j] = M[i * ldm + j] + ((i == j) ? ridge : 0.f);
+    }
+    __syncwarp();
+    bool ok = true, small = false;
+    for (int j = 0; j < m; ++j) {
+      const float d = L[j * ld + j];
+      if (!(d > 0.f) || !isfinite(d)) { ok = false; break; }
+      const float piv = sqrtf(d);
+      if (piv * piv < 1e-10f) small = true;
+      __syncwarp();
+      if (lane == j) L[j * ld + j] = piv;
+      if (lane > j && lane < m) L[lane * ld + j] /= piv;
+      __syncwarp();
+      if (lane > j && lane < m) {
+        const float lij = L[lane * ld + j];
+        for (int l = j + 1; l <= lane; ++l) L[lane * ld + l] = fmaf(-lij, L[l * ld + j], L[lane * ld + l]);
+      }
+      __syncwarp();
+    }
+    if (!ok || (attempt == 0 && small)) {
+      if (attempt == 1) return 1;
+      continue;
+    }
+    // X = L^{-1}: lane j solves L x = e_j
+    if (lane < m) {
+      const int j = lane;
+      for (int i = 0; i < m; ++i) {
+        float s = (i == j) ? 1.f : 0.f;
+        for (int k = j; k < i; ++k) s = fmaf(-L[i * ld + k], X[k * ld + j], s);
+        X[i * ld + j] = (i < j) ? 0.f : s / L[i * ld + i];
+      }
+    }
+    __syncwarp();
+    // inv = X^T X
+    for (int e = lane; e < m * m; e += 32) {
+      const int i = e / m, j = e % m;
+      float s = 0.f;
+      for (int k = max(i, j); k < m; ++k) s = fmaf(X[k * ld + i], X[k * ld + j], s);
+      inv[i * ldm + j] = s;
+    }
+    __syncwarp();
+    return 0;
+  }
+  return 1;
+}
+
+}  // namespace gsls
