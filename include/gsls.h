@@ -115,6 +115,10 @@ int gsls_version(void);
 int gsls_last_error(gsls_error_t* out);
 int gsls_ctx_create(const gsls_dims_t* dims, gsls_ctx** out);
 int gsls_ctx_destroy(gsls_ctx* ctx);
+/* Synchronizes the stream and reports the first per-instance error recorded
+ * by earlier kernels (singular blocks, ill-conditioned combines, non-finite
+ * model output), clearing the record. */
+int gsls_ctx_check(gsls_ctx* ctx, void* stream);
 /* bytes of device memory held by the context */
 int64_t gsls_ctx_bytes(const gsls_ctx* ctx);
 
@@ -160,6 +164,13 @@ int gsls_ctx_export_solution(gsls_ctx* ctx, float* K, double* k, float* P, doubl
  * Phi^u, tau); cells with k = N carry the terminal ones (Qx_term, tau_term via
  * column j).  Phi^x is defined on every cell. */
 int gsls_sls_ncell(int32_t N);
+/* Host-side inspection of the merged column schedules: cvf = 1 the reverse
+ * CVF grid scan (leaves at cell(k, j) for k in [j+1, N]), cvf = 0 the forward
+ * product scan (leaf of position p at cell(p+1, j)).  ops as gsls_scan_plan;
+ * out_cell[cell(k, j)] = slot holding the column-j output of position k
+ * (CVF) / of position k-1 (product).  Sizes only when max_ops is too small. */
+int gsls_sls_plan(int32_t N, int32_t cvf, int32_t max_ops, int32_t* ops, int32_t* layer_off, int32_t* out_cell,
+                  int32_t* n_ops, int32_t* n_layers, int32_t* n_slots);
 /* sls.assemble_costs (sls.py:176-200): [C D]' diag(tau) [C D] + blkdiag(Qbar, Rbar)
  * per cell, CN' diag(tau_term) CN + QbarN on terminal cells.  tau (B,ncell,nc)
  * float64 or NULL (= unweighted, sls.py:189); tau_term (B,N,nf) or NULL.
@@ -169,21 +180,70 @@ int gsls_sls_assemble(gsls_ctx* ctx, const gsls_qp_t* qp, const double* tau, con
                       const float* Qbar, const float* Rbar, const float* QbarN, int32_t weights_per_instance,
                       void* stream);
 /* Explicit SlsCosts (sls.py:129-143) in cell layout: Qx (B,ncell,nx,nx) (terminal
- * cells hold Qx_term), Qu (B,ncell,nu,nu), Qux (B,ncell,nu,nx), float32. */
-int gsls_sls_set_costs(gsls_ctx* ctx, const float* Qx, const float* Qu, const float* Qux, void* stream);
+ * cells hold Qx_term), Qu (B,ncell,nu,nu), Qux (B,ncell,nu,nx), float64. */
+int gsls_sls_set_costs(gsls_ctx* ctx, const double* Qx, const double* Qu, const double* Qux, void* stream);
+/* Reads back the costs held by ctx in the gsls_sls_set_costs layout; any may be NULL. */
+int gsls_sls_export_costs(gsls_ctx* ctx, double* Qx, double* Qu, double* Qux, void* stream);
 /* sls.synthesize (sls.py:227-318) on the costs held by ctx; A, B from qp,
  * E (B,N,nx,nx) float32.  The response stays on the device. */
 int gsls_sls_synthesize(gsls_ctx* ctx, const gsls_qp_t* qp, const float* E, void* stream);
-/* sls.tighten (sls.py:329-341): h (B,N,nc), hf (B,nf), float64. */
-int gsls_sls_tighten(gsls_ctx* ctx, double* h, double* hf, void* stream);
-/* sls.compute_duals (sls.py:150-173): lam_stage (B,N,nc) lam_term (B,nf) ->
- * tau (B,ncell,nc), tau_term (B,N,nf) [beta, beta_term same shapes, may be
- * NULL], float64.  use_response = 0 reproduces response=None (beta = 0). */
-int gsls_sls_duals(gsls_ctx* ctx, const double* lam_stage, const double* lam_term, double eps, int32_t use_response,
-                   double* tau, double* tau_term, double* beta, double* beta_term, void* stream);
+/* sls.tighten (sls.py:329-341) of the response held by ctx with C, D, CN
+ * from qp: h (B,N,nc), hf (B,nf), float64. */
+int gsls_sls_tighten(gsls_ctx* ctx, const gsls_qp_t* qp, double* h, double* hf, void* stream);
+/* sls.compute_duals (sls.py:150-173): lam is the stacked multiplier
+ * (B, N*nc+nf) (AdmmState.lam, admm.py:82-88) -> tau (B,ncell,nc),
+ * tau_term (B,N,nf) [beta, beta_term same shapes, may be NULL], float64;
+ * C, D, CN from qp.  use_response = 0 reproduces response=None (beta = 0);
+ * reuse_rownorms = 1 skips recomputing the row norms of the last
+ * gsls_sls_tighten (same C, D, CN). */
+int gsls_sls_duals(gsls_ctx* ctx, const gsls_qp_t* qp, const double* lam, double eps, int32_t use_response,
+                   int32_t reuse_rownorms, double* tau, double* tau_term, double* beta, double* beta_term,
+                   void* stream);
+/* Loads an SlsResponse built elsewhere: Phi_x (B,ncell,nx,nx), Phi_u (B,ncell,nu,nx). */
+int gsls_sls_import_response(gsls_ctx* ctx, const float* phix, const float* phiu, void* stream);
 /* SlsResponse export (sls.py:51-92): Phi_x (B,ncell,nx,nx), Phi_u and gains
  * (B,ncell,nu,nx) (zero on terminal cells), float32; any may be NULL. */
 int gsls_sls_export(gsls_ctx* ctx, float* phix, float* phiu, float* gains, void* stream);
+
+/* ---- SQP linearization (sqp.py:105-147) ----------------------------------- */
+enum { GSLS_MODEL_DUBINS = 1, GSLS_MODEL_PLANAR_QUAD = 2, GSLS_MODEL_PENDULUM = 3,
+       GSLS_MODEL_QUAD12 = 4, GSLS_MODEL_SYNTHETIC = 5 };
+
+typedef struct {
+  int32_t model_id;             /* GSLS_MODEL_*                                        */
+  const double* params;         /* model parameters + constraint block (device)        */
+  int32_t cons_offset;          /* index of the constraint block in params:
+                                   n_obs, u_min[nu], u_max[nu], (cx, cy, r) per obstacle */
+  const double *x, *u;          /* linearization trajectory (B,N+1,nx), (B,N,nu)       */
+  const double *h, *hf;         /* tightenings (B,N,nc), (B,nf) or NULL                */
+  const double* xbar0;          /* measured state (B,nx) or NULL (dx0 = 0)              */
+  const double *Qw, *Rw, *QNw;  /* tracking weights (nx,nx) (nu,nu) (nx,nx)             */
+  const double *xref, *uref;    /* reference (N+1,nx), (N,nu)                           */
+  const double* E_const;        /* constant disturbance map (nx,nx) or NULL             */
+  int32_t write_weights;        /* 1: also write Q, R, S (= 0), QN and E                */
+} gsls_linearize_args_t;
+
+/* sqp.linearize: writes A, B, b, C, D, f (= -g - h), q, r, CN, fN, qN, dx0 of
+ * `out` (device buffers of the gsls_qp_t layout; the pointers are written
+ * through), and Q, R, S, QN, E (B,N,nx,nx) when write_weights is set.
+ * Non-finite dynamics raise GSLS_ERR_NONFINITE naming the stage. */
+int gsls_linearize(gsls_ctx* ctx, const gsls_linearize_args_t* args, const gsls_qp_t* out, float* E, void* stream);
+
+/* Trajectory terms of the SQP loop (sqp.py:150-187) for the trajectory in
+ * args (x, u, h, hf, xbar0; weights/reference for the tracking cost):
+ * out (B,8) float64 = {tracking cost J, max|defect|, sum|defect|,
+ * max(g + h) (unclamped), sum max(g + h, 0), sum|x0 - xbar0|, max|x0 - xbar0|, n_obs}. */
+int gsls_traj_eval(gsls_ctx* ctx, const gsls_linearize_args_t* args, double* out, void* stream);
+
+/* f -= h, fN -= hf in place (the tightened re-linearization, sqp.py:136/:140). */
+int gsls_apply_tightening(gsls_ctx* ctx, double* f, double* fN, const double* h, const double* hf, void* stream);
+/* RTI update (sqp.py:293-301, :40-43): plan = prev + (dx, du); warm start =
+ * plan shifted with the last stage duplicated; u0 = plan.u[0]; cost (B) =
+ * tracking cost of the plan (models.py:85-93) or NULL.  All float64. */
+int gsls_rti_apply(gsls_ctx* ctx, const double* prev_x, const double* prev_u, const double* dx, const double* du,
+                   double* plan_x, double* plan_u, double* warm_x, double* warm_u, double* u0, const double* Qw,
+                   const double* Rw, const double* QNw, const double* xref, const double* uref, double* cost,
+                   void* stream);
 
 #ifdef __cplusplus
 }

@@ -49,6 +49,13 @@ class AdmmStats(ctypes.Structure):
                 ("cache_builds", c_void_p)]
 
 
+class LinArgs(ctypes.Structure):
+    _fields_ = [("model_id", ctypes.c_int32), ("params", c_void_p), ("cons_offset", ctypes.c_int32),
+                ("x", c_void_p), ("u", c_void_p), ("h", c_void_p), ("hf", c_void_p), ("xbar0", c_void_p),
+                ("Qw", c_void_p), ("Rw", c_void_p), ("QNw", c_void_p), ("xref", c_void_p), ("uref", c_void_p),
+                ("E_const", c_void_p), ("write_weights", ctypes.c_int32)]
+
+
 class Error(ctypes.Structure):
     _fields_ = [("code", ctypes.c_int32), ("instance", ctypes.c_int32), ("where", ctypes.c_int32),
                 ("aux", ctypes.c_int32), ("aux2", ctypes.c_int32), ("message", ctypes.c_char * 256)]
@@ -60,6 +67,7 @@ _SIGS = {
     "gsls_ctx_create": ([ctypes.POINTER(Dims), ctypes.POINTER(c_void_p)], ctypes.c_int),
     "gsls_ctx_destroy": ([c_void_p], ctypes.c_int),
     "gsls_ctx_bytes": ([c_void_p], ctypes.c_int64),
+    "gsls_ctx_check": ([c_void_p, c_void_p], ctypes.c_int),
     "gsls_scan_plan": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_int32_p, c_int32_p, c_int32_p,
                         c_int32_p, c_int32_p], ctypes.c_int),
     "gsls_lqr_solve": ([c_void_p, ctypes.POINTER(Qp), ctypes.c_int32] + [c_void_p] * 6 + [c_void_p], ctypes.c_int),
@@ -69,6 +77,21 @@ _SIGS = {
                             ctypes.POINTER(AdmmState), ctypes.POINTER(AdmmStats), c_void_p, c_void_p,
                             c_void_p], ctypes.c_int),
     "gsls_ctx_export_solution": ([c_void_p] * 6, ctypes.c_int),
+    "gsls_sls_ncell": ([ctypes.c_int32], ctypes.c_int),
+    "gsls_sls_plan": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_int32] + [c_int32_p] * 6, ctypes.c_int),
+    "gsls_sls_assemble": ([c_void_p, ctypes.POINTER(Qp)] + [c_void_p] * 5 + [ctypes.c_int32, c_void_p], ctypes.c_int),
+    "gsls_sls_set_costs": ([c_void_p] * 5, ctypes.c_int),
+    "gsls_sls_export_costs": ([c_void_p] * 5, ctypes.c_int),
+    "gsls_sls_synthesize": ([c_void_p, ctypes.POINTER(Qp), c_void_p, c_void_p], ctypes.c_int),
+    "gsls_sls_tighten": ([c_void_p, ctypes.POINTER(Qp), c_void_p, c_void_p, c_void_p], ctypes.c_int),
+    "gsls_sls_duals": ([c_void_p, ctypes.POINTER(Qp), c_void_p, ctypes.c_double, ctypes.c_int32, ctypes.c_int32]
+                       + [c_void_p] * 5, ctypes.c_int),
+    "gsls_sls_import_response": ([c_void_p] * 4, ctypes.c_int),
+    "gsls_sls_export": ([c_void_p] * 5, ctypes.c_int),
+    "gsls_linearize": ([c_void_p, ctypes.POINTER(LinArgs), ctypes.POINTER(Qp), c_void_p, c_void_p], ctypes.c_int),
+    "gsls_traj_eval": ([c_void_p, ctypes.POINTER(LinArgs), c_void_p, c_void_p], ctypes.c_int),
+    "gsls_apply_tightening": ([c_void_p] * 6, ctypes.c_int),
+    "gsls_rti_apply": ([c_void_p] * 17, ctypes.c_int),
 }
 
 # every symbol include/gsls.h declares (checked by the CPU test suite)

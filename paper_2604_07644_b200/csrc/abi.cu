@@ -11,6 +11,7 @@ namespace gsls {
 int ctx_create(const gsls_dims_t* dims, Ctx** out);
 void ctx_destroy(Ctx* c);
 int get_last_error(gsls_error_t* out);
+int check_errors(Ctx* c, cudaStream_t st, const char* what);
 void set_error(int code, int inst, int where, int aux, int label, const char* msg);
 int lqr_solve(Ctx* c, const gsls_qp_t* qp, int generation, double* dx, double* du, float* K, double* k, float* P,
               double* p, cudaStream_t st);
@@ -21,11 +22,21 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
 int ctx_export(Ctx* c, float* K, double* k, float* P, double* p, cudaStream_t st);
 int sls_assemble(Ctx* c, const gsls_qp_t* qp, const double* tau, const double* tau_term, const float* Qbar,
                  const float* Rbar, const float* QbarN, int weights_per_instance, cudaStream_t st);
-int sls_set_costs(Ctx* c, const float* Qx, const float* Qu, const float* Qux, cudaStream_t st);
+int sls_set_costs(Ctx* c, const double* Qx, const double* Qu, const double* Qux, cudaStream_t st);
 int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st, bool check);
-int sls_tighten(Ctx* c, double* h, double* hf, cudaStream_t st);
-int sls_duals(Ctx* c, const double* lam_s, const double* lam_t, double eps, int use_response, double* tau,
-              double* tau_term, double* beta, double* beta_term, cudaStream_t st);
+int sls_tighten(Ctx* c, const gsls_qp_t* qp, double* h, double* hf, cudaStream_t st);
+int sls_duals(Ctx* c, const gsls_qp_t* qp, const double* lam, double eps, int use_response, int reuse_rownorms,
+              double* tau, double* tau_term, double* beta, double* beta_term, cudaStream_t st);
+int sls_import(Ctx* c, const float* phix, const float* phiu, cudaStream_t st);
+int sls_export_costs(Ctx* c, double* Qx, double* Qu, double* Qux, cudaStream_t st);
+int sls_plan(int N, int cvf, int max_ops, int* ops, int* layer_off, int* out, int* n_ops, int* n_layers,
+             int* n_slots);
+int linearize(Ctx* c, const gsls_linearize_args_t* in, gsls_qp_t* out_qp, float* E, cudaStream_t st);
+int traj_eval(Ctx* c, const gsls_linearize_args_t* in, double* out, cudaStream_t st);
+int apply_tightening(Ctx* c, double* f, double* fN, const double* h, const double* hf, cudaStream_t st);
+int rti_apply(Ctx* c, const double* px, const double* pu, const double* dx, const double* du, double* plan_x,
+              double* plan_u, double* warm_x, double* warm_u, double* u0, const double* Qw, const double* Rw,
+              const double* QNw, const double* xref, const double* uref, double* cost, cudaStream_t st);
 int sls_export(Ctx* c, float* phix, float* phiu, float* gains, cudaStream_t st);
 }  // namespace gsls
 
@@ -73,6 +84,11 @@ int gsls_ctx_destroy(gsls_ctx* ctx) {
 }
 
 int64_t gsls_ctx_bytes(const gsls_ctx* ctx) { return ctx ? ctx->impl->bytes : 0; }
+
+int gsls_ctx_check(gsls_ctx* ctx, void* stream) {
+  if (!ctx) return fail_null("ctx");
+  return check_errors(ctx->impl, (cudaStream_t)stream, "check");
+}
 
 int gsls_scan_plan(int32_t length, int32_t reverse, int32_t max_ops, int32_t* ops, int32_t* layer_off,
                    int32_t* out_slot, int32_t* n_ops, int32_t* n_layers) {
@@ -125,6 +141,12 @@ int gsls_ctx_export_solution(gsls_ctx* ctx, float* K, double* k, float* P, doubl
 
 int gsls_sls_ncell(int32_t N) { return N * (N + 1) / 2; }
 
+int gsls_sls_plan(int32_t N, int32_t cvf, int32_t max_ops, int32_t* ops, int32_t* layer_off, int32_t* out_cell,
+                  int32_t* n_ops, int32_t* n_layers, int32_t* n_slots) {
+  if (N < 1 || !n_ops || !n_layers || !n_slots) return fail_null("argument");
+  return sls_plan(N, cvf, max_ops, ops, layer_off, out_cell, n_ops, n_layers, n_slots);
+}
+
 int gsls_sls_assemble(gsls_ctx* ctx, const gsls_qp_t* qp, const double* tau, const double* tau_term,
                       const float* Qbar, const float* Rbar, const float* QbarN, int32_t weights_per_instance,
                       void* stream) {
@@ -136,9 +158,14 @@ int gsls_sls_assemble(gsls_ctx* ctx, const gsls_qp_t* qp, const double* tau, con
   return sls_assemble(ctx->impl, qp, tau, tau_term, Qbar, Rbar, QbarN, weights_per_instance, (cudaStream_t)stream);
 }
 
-int gsls_sls_set_costs(gsls_ctx* ctx, const float* Qx, const float* Qu, const float* Qux, void* stream) {
+int gsls_sls_set_costs(gsls_ctx* ctx, const double* Qx, const double* Qu, const double* Qux, void* stream) {
   if (!ctx || !Qx || !Qu || !Qux) return fail_null("argument");
   return sls_set_costs(ctx->impl, Qx, Qu, Qux, (cudaStream_t)stream);
+}
+
+int gsls_sls_export_costs(gsls_ctx* ctx, double* Qx, double* Qu, double* Qux, void* stream) {
+  if (!ctx) return fail_null("ctx");
+  return sls_export_costs(ctx->impl, Qx, Qu, Qux, (cudaStream_t)stream);
 }
 
 int gsls_sls_synthesize(gsls_ctx* ctx, const gsls_qp_t* qp, const float* E, void* stream) {
@@ -146,21 +173,61 @@ int gsls_sls_synthesize(gsls_ctx* ctx, const gsls_qp_t* qp, const float* E, void
   return sls_synthesize(ctx->impl, qp, E, (cudaStream_t)stream, true);
 }
 
-int gsls_sls_tighten(gsls_ctx* ctx, double* h, double* hf, void* stream) {
-  if (!ctx || !h) return fail_null("argument");
-  return sls_tighten(ctx->impl, h, hf, (cudaStream_t)stream);
+int gsls_sls_tighten(gsls_ctx* ctx, const gsls_qp_t* qp, double* h, double* hf, void* stream) {
+  if (!ctx || !qp || !h) return fail_null("argument");
+  return sls_tighten(ctx->impl, qp, h, hf, (cudaStream_t)stream);
 }
 
-int gsls_sls_duals(gsls_ctx* ctx, const double* lam_stage, const double* lam_term, double eps, int32_t use_response,
-                   double* tau, double* tau_term, double* beta, double* beta_term, void* stream) {
-  if (!ctx || !lam_stage || !tau || !tau_term) return fail_null("argument");
-  return sls_duals(ctx->impl, lam_stage, lam_term, eps, use_response, tau, tau_term, beta, beta_term,
+int gsls_sls_duals(gsls_ctx* ctx, const gsls_qp_t* qp, const double* lam, double eps, int32_t use_response,
+                   int32_t reuse_rownorms, double* tau, double* tau_term, double* beta, double* beta_term,
+                   void* stream) {
+  if (!ctx || !qp || !lam || !tau || !tau_term) return fail_null("argument");
+  return sls_duals(ctx->impl, qp, lam, eps, use_response, reuse_rownorms, tau, tau_term, beta, beta_term,
                    (cudaStream_t)stream);
+}
+
+int gsls_sls_import_response(gsls_ctx* ctx, const float* phix, const float* phiu, void* stream) {
+  if (!ctx || !phix || !phiu) return fail_null("argument");
+  return sls_import(ctx->impl, phix, phiu, (cudaStream_t)stream);
 }
 
 int gsls_sls_export(gsls_ctx* ctx, float* phix, float* phiu, float* gains, void* stream) {
   if (!ctx) return fail_null("ctx");
   return sls_export(ctx->impl, phix, phiu, gains, (cudaStream_t)stream);
+}
+
+int gsls_linearize(gsls_ctx* ctx, const gsls_linearize_args_t* args, const gsls_qp_t* out, float* E, void* stream) {
+  if (!ctx || !args || !out || !args->params || !args->x || !args->u || !args->Qw || !args->Rw || !args->QNw ||
+      !args->xref || !args->uref)
+    return fail_null("argument");
+  gsls_qp_t o = *out;
+  int rc = linearize(ctx->impl, args, &o, E, (cudaStream_t)stream);
+  if (rc == GSLS_ERR_ARG) set_error(rc, -1, 0, 0, 0, "model / dimension mismatch");
+  if (rc == GSLS_ERR_TOO_LARGE) set_error(rc, -1, 0, 0, 0, "model too large");
+  return rc;
+}
+
+int gsls_traj_eval(gsls_ctx* ctx, const gsls_linearize_args_t* args, double* out, void* stream) {
+  if (!ctx || !args || !out || !args->params || !args->x || !args->u || !args->Qw || !args->Rw || !args->QNw ||
+      !args->xref || !args->uref)
+    return fail_null("argument");
+  return traj_eval(ctx->impl, args, out, (cudaStream_t)stream);
+}
+
+int gsls_apply_tightening(gsls_ctx* ctx, double* f, double* fN, const double* h, const double* hf, void* stream) {
+  if (!ctx || (!f && ctx->impl->dims.nc > 0) || (!h && ctx->impl->dims.nc > 0)) return fail_null("argument");
+  return apply_tightening(ctx->impl, f, fN, h, hf, (cudaStream_t)stream);
+}
+
+int gsls_rti_apply(gsls_ctx* ctx, const double* prev_x, const double* prev_u, const double* dx, const double* du,
+                   double* plan_x, double* plan_u, double* warm_x, double* warm_u, double* u0, const double* Qw,
+                   const double* Rw, const double* QNw, const double* xref, const double* uref, double* cost,
+                   void* stream) {
+  if (!ctx || !prev_x || !prev_u || !dx || !du || !plan_x || !plan_u || !warm_x || !warm_u || !u0)
+    return fail_null("argument");
+  if (cost && (!Qw || !Rw || !QNw || !xref || !uref)) return fail_null("cost weights");
+  return rti_apply(ctx->impl, prev_x, prev_u, dx, du, plan_x, plan_u, warm_x, warm_u, u0, Qw, Rw, QNw, xref, uref,
+                   cost, (cudaStream_t)stream);
 }
 
 }  // extern "C"

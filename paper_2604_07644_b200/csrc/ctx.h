@@ -31,7 +31,9 @@ struct DevLqr {
   float* cotA;           // [batch][cot_nslots][n*ldg]
   float* cot_rec;        // [batch][cot_nops][n*ldg]: A_later (column-major)
   // per-stage cache, unpadded row-major: [batch][N][...]
-  float *Rhat, *Shat, *Rinv, *Gamma, *K;  // m*m, m*n, m*m, m*m, m*n
+  double* Rhat;          // [batch][N][m*m] augmented R (float64)
+  double* Shat64;        // [batch][N][m*n] augmented S (float64, for the gains)
+  float *Shat, *Rinv, *Gamma, *K;  // m*n, m*m, m*m, m*n (float32, replay operands)
   double* cvec;          // [batch][N][n]  P_{k+1} b_k
   double* v0;            // [batch][n]     Abar_0 dx0
   double* last_k;        // [batch][N][m]   feedforward of the last replay

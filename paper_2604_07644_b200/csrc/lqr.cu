@@ -102,12 +102,14 @@ int check_errors(Ctx* c, cudaStream_t st, const char* what) {
 __device__ inline int inst_of(const int* list) { return list ? list[blockIdx.y] : (int)blockIdx.y; }
 
 // CVF leaves (Eq. 29) with penalty augmentation rho (0 for a plain LQR).
+// Computed in float64: the Schur complement Q^ - S^' R^-1 S^ cancels O(rho)
+// terms; only the result is rounded to the float32 scan storage.
 __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const double* rho_arr,
                                                    const int* list) {
   const int inst = inst_of(list);
   const int k = blockIdx.x;
   const int n = L.n, m = L.m, c = L.c, nf = L.nf, N = L.N, ldg = L.ldg;
-  const float rho = rho_arr ? (float)rho_arr[inst] : 0.f;
+  const double rho = rho_arr ? rho_arr[inst] : 0.0;
   const size_t MS = (size_t)n * ldg;
   const size_t sbase = ((size_t)inst * L.cvf_nslots + k) * MS;
   float* Pd = L.Ps + sbase;
@@ -118,28 +120,28 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
     const float* CN = qp.CN + (size_t)inst * nf * n;
     for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
       const int i = e / ldg, j = e - i * ldg;
-      float v = 0.f;
+      double v = 0.0;
       if (j < n) {
-        float s = 0.f;
-        for (int f = 0; f < nf; ++f) s = fmaf(CN[f * n + i], CN[f * n + j], s);
-        v = QN[i * n + j] + rho * s;
+        double s = 0.0;
+        for (int f = 0; f < nf; ++f) s = fma((double)CN[f * n + i], (double)CN[f * n + j], s);
+        v = (double)QN[i * n + j] + rho * s;
       }
-      Pd[e] = v;
+      Pd[e] = (float)v;
       Ad[e] = 0.f;
       Cd[e] = 0.f;
     }
     return;
   }
-  extern __shared__ float sm[];
-  float* Cst = sm;                  // c x n
-  float* Dst = Cst + c * n;         // c x m
-  float* Bst = Dst + c * m;         // n x m
-  float* Sh = Bst + n * m;          // m x n
-  float* Rh = Sh + m * n;           // m x m
-  float* Ri = Rh + m * m;           // m x m
-  float* RS = Ri + m * m;           // m x n
-  float* BR = RS + m * n;           // n x m
-  float* wk = BR + n * m;           // spd work
+  extern __shared__ double smd[];
+  double* Cst = smd;                 // c x n
+  double* Dst = Cst + c * n;         // c x m
+  double* Bst = Dst + c * m;         // n x m
+  double* Sh = Bst + n * m;          // m x n
+  double* Rh = Sh + m * n;           // m x m
+  double* Ri = Rh + m * m;           // m x m
+  double* RS = Ri + m * m;           // m x n
+  double* BR = RS + m * n;           // n x m
+  double* wk = BR + n * m;           // spd work
   const size_t st = (size_t)inst * N + k;
   const float* Cg = qp.C + st * c * n;
   const float* Dg = qp.D + st * c * m;
@@ -152,15 +154,15 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   const float* Sg = qp.S ? qp.S + st * m * n : nullptr;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
     const int i = e / m, j = e - i * m;
-    float s = 0.f;
-    for (int r = 0; r < c; ++r) s = fmaf(Dst[r * m + i], Dst[r * m + j], s);
-    Rh[e] = Rg[e] + rho * s;
+    double s = 0.0;
+    for (int r = 0; r < c; ++r) s = fma(Dst[r * m + i], Dst[r * m + j], s);
+    Rh[e] = (double)Rg[e] + rho * s;
   }
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     const int i = e / n, j = e - i * n;
-    float s = 0.f;
-    for (int r = 0; r < c; ++r) s = fmaf(Dst[r * m + i], Cst[r * n + j], s);
-    Sh[e] = (Sg ? Sg[e] : 0.f) + rho * s;
+    double s = 0.0;
+    for (int r = 0; r < c; ++r) s = fma(Dst[r * m + i], Cst[r * n + j], s);
+    Sh[e] = (Sg ? (double)Sg[e] : 0.0) + rho * s;
   }
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -170,14 +172,14 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   __syncthreads();
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     const int l = e / n, j = e - l * n;
-    float s = 0.f;
-    for (int t = 0; t < m; ++t) s = fmaf(Ri[l * m + t], Sh[t * n + j], s);
+    double s = 0.0;
+    for (int t = 0; t < m; ++t) s = fma(Ri[l * m + t], Sh[t * n + j], s);
     RS[e] = s;
   }
   for (int e = threadIdx.x; e < n * m; e += blockDim.x) {
     const int i = e / m, l = e - i * m;
-    float s = 0.f;
-    for (int t = 0; t < m; ++t) s = fmaf(Bst[i * m + t], Ri[t * m + l], s);
+    double s = 0.0;
+    for (int t = 0; t < m; ++t) s = fma(Bst[i * m + t], Ri[t * m + l], s);
     BR[e] = s;
   }
   __syncthreads();
@@ -185,30 +187,32 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   const float* Ag = qp.A + st * n * n;
   for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
     const int i = e / ldg, j = e - i * ldg;
-    float p = 0.f, a = 0.f, cc = 0.f;
+    double p = 0.0, a = 0.0, cc = 0.0;
     if (j < n) {
-      float s = 0.f;
-      for (int r = 0; r < c; ++r) s = fmaf(Cst[r * n + i], Cst[r * n + j], s);
-      const float qh = Qg[i * n + j] + rho * s;
-      float sr = 0.f, br = 0.f, bb = 0.f;
+      double s = 0.0;
+      for (int r = 0; r < c; ++r) s = fma(Cst[r * n + i], Cst[r * n + j], s);
+      const double qh = (double)Qg[i * n + j] + rho * s;
+      double sr = 0.0, br = 0.0, bb = 0.0;
       for (int l = 0; l < m; ++l) {
-        sr = fmaf(Sh[l * n + i], RS[l * n + j], sr);
-        br = fmaf(Bst[i * m + l], RS[l * n + j], br);
-        bb = fmaf(BR[i * m + l], Bst[j * m + l], bb);
+        sr = fma(Sh[l * n + i], RS[l * n + j], sr);
+        br = fma(Bst[i * m + l], RS[l * n + j], br);
+        bb = fma(BR[i * m + l], Bst[j * m + l], bb);
       }
       p = qh - sr;
-      a = Ag[i * n + j] - br;
+      a = (double)Ag[i * n + j] - br;
       cc = bb;
     }
-    Pd[e] = p;
-    Ad[e] = a;
-    Cd[e] = cc;
+    Pd[e] = (float)p;
+    Ad[e] = (float)a;
+    Cd[e] = (float)cc;
   }
-  float* Rhat = L.Rhat + st * m * m;
+  double* Rhat = L.Rhat + st * m * m;
   float* Shat = L.Shat + st * m * n;
   float* Rinv = L.Rinv + st * m * m;
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) { Rhat[e] = Rh[e]; Rinv[e] = Ri[e]; }
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) Shat[e] = Sh[e];
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) { Rhat[e] = Rh[e]; Rinv[e] = (float)Ri[e]; }
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) Shat[e] = (float)Sh[e];
+  double* Shd = L.Shat64 + st * m * n;
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) Shd[e] = Sh[e];
 }
 
 // Matrix half of the CVF combine (Eq. 28) for one op per CTA; optionally
@@ -283,47 +287,46 @@ int combine_threads(int n) {
   return t;
 }
 
-// Gains, closed loop and COT leaves per stage (lqr.py:398-404, :349-356).
+// Gains, closed loop and COT leaves per stage (lqr.py:398-404, :349-356), in float64.
 __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const int* list) {
   const int inst = inst_of(list);
   const int k = blockIdx.x;
   const int n = L.n, m = L.m, N = L.N, ldg = L.ldg;
   const size_t MS = (size_t)n * ldg;
-  extern __shared__ float sm[];
-  float* Pn = sm;               // n x ldg
-  float* Bst = Pn + n * ldg;    // n x m
-  float* BtP = Bst + n * m;     // m x n
-  float* H = BtP + m * n;       // m x m
-  float* Gm = H + m * m;        // m x n
-  float* Ga = Gm + m * n;       // m x m
-  float* Ks = Ga + m * m;       // m x n
-  float* wk = Ks + m * n;
+  extern __shared__ double smd[];
+  double* Bst = smd;             // n x m
+  double* BtP = Bst + n * m;     // m x n
+  double* H = BtP + m * n;       // m x m
+  double* Gm = H + m * m;        // m x n
+  double* Ga = Gm + m * n;       // m x m
+  double* Ks = Ga + m * m;       // m x n
+  double* wk = Ks + m * n;
+  float* Abar = reinterpret_cast<float*>(wk + 2 * kMaxM * (kMaxM + 1) + 8);  // n x ldg (float)
   const size_t st = (size_t)inst * N + k;
-  const float* Pg = L.Ps + ((size_t)inst * L.cvf_nslots + L.cvf_out[k + 1]) * MS;
-  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) Pn[e] = Pg[e];
+  const float* Pn = L.Ps + ((size_t)inst * L.cvf_nslots + L.cvf_out[k + 1]) * MS;
   const float* Bg = qp.B + st * n * m;
   for (int e = threadIdx.x; e < n * m; e += blockDim.x) Bst[e] = Bg[e];
   __syncthreads();
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     const int l = e / n, j = e - l * n;
-    float s = 0.f;
-    for (int i = 0; i < n; ++i) s = fmaf(Bst[i * m + l], Pn[i * ldg + j], s);
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s = fma(Bst[i * m + l], (double)Pn[i * ldg + j], s);
     BtP[e] = s;
   }
   __syncthreads();
   const float* Ag = qp.A + st * n * n;
-  const float* Rhat = L.Rhat + st * m * m;
-  const float* Shat = L.Shat + st * m * n;
+  const double* Rhat = L.Rhat + st * m * m;
+  const double* Shat = L.Shat64 + st * m * n;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
     const int l = e / m, t = e - l * m;
-    float s = 0.f;
-    for (int j = 0; j < n; ++j) s = fmaf(BtP[l * n + j], Bst[j * m + t], s);
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s = fma(BtP[l * n + j], Bst[j * m + t], s);
     H[e] = Rhat[e] + s;
   }
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     const int l = e / n, j = e - l * n;
-    float s = 0.f;
-    for (int i = 0; i < n; ++i) s = fmaf(BtP[l * n + i], Ag[i * n + j], s);
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s = fma(BtP[l * n + i], (double)Ag[i * n + j], s);
     Gm[e] = Shat[e] + s;
   }
   __syncthreads();
@@ -335,13 +338,13 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const int
   float* Kg = L.K + st * m * n;
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     const int l = e / n, j = e - l * n;
-    float s = 0.f;
-    for (int t = 0; t < m; ++t) s = fmaf(Ga[l * m + t], Gm[t * n + j], s);
+    double s = 0.0;
+    for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Gm[t * n + j], s);
     Ks[e] = -s;
-    Kg[e] = -s;
+    Kg[e] = (float)(-s);
   }
   float* Gg = L.Gamma + st * m * m;
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) Gg[e] = Ga[e];
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) Gg[e] = (float)Ga[e];
   const double* bg = qp.b + st * n;
   double* cv = L.cvec + st * n;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -352,17 +355,16 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const int
   __syncthreads();
   // closed loop Abar = A + B K -> COT leaf k (leaf 0 carries A = 0, lqr.py:354)
   float* Ad = L.cotA + ((size_t)inst * L.cot_nslots + k) * MS;
-  float* Abar = Pn;  // reuse (Pn no longer needed)
   for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
     const int i = e / ldg, j = e - i * ldg;
-    float v = 0.f;
+    double v = 0.0;
     if (j < n) {
-      float s = 0.f;
-      for (int l = 0; l < m; ++l) s = fmaf(Bst[i * m + l], Ks[l * n + j], s);
-      v = Ag[i * n + j] + s;
+      double s = 0.0;
+      for (int l = 0; l < m; ++l) s = fma(Bst[i * m + l], Ks[l * n + j], s);
+      v = (double)Ag[i * n + j] + s;
     }
-    Abar[e] = v;
-    Ad[e] = (k == 0) ? 0.f : v;
+    Abar[e] = (float)v;
+    Ad[e] = (k == 0) ? 0.f : (float)v;
   }
   if (k == 0) {
     __syncthreads();
@@ -398,12 +400,12 @@ __global__ void __launch_bounds__(512) k_cot_combine(DevLqr L, const int4* ops, 
 // host driver
 
 static size_t leaf_smem_bytes(int n, int m, int c) {
-  return (size_t)(c * n + c * m + n * m + m * n + 2 * m * m + m * n + n * m + 2 * kMaxM * (kMaxM + 1) + 8 + m * m) *
-         sizeof(float);
+  return (size_t)(c * n + c * m + n * m + m * n + 2 * m * m + m * n + n * m + 2 * kMaxM * (kMaxM + 1) + 8) *
+         sizeof(double);
 }
 static size_t gains_smem_bytes(int n, int m) {
-  return (size_t)(n * ldg_of(n) + n * m + m * n + m * m + m * n + m * m + m * n + 2 * kMaxM * (kMaxM + 1) + 8) *
-         sizeof(float);
+  return (size_t)(n * m + m * n + m * m + m * n + m * m + m * n + 2 * kMaxM * (kMaxM + 1) + 8) * sizeof(double) +
+         (size_t)n * ldg_of(n) * sizeof(float);
 }
 
 static int set_smem(const void* fn, size_t bytes) {
@@ -536,8 +538,9 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
   L.cvf_rec = (float*)dev_alloc(c, B * L.cvf_nops * 4 * MS * 4);
   L.cotA = (float*)dev_alloc(c, B * L.cot_nslots * MS * 4);
   L.cot_rec = (float*)dev_alloc(c, B * L.cot_nops * MS * 4);
-  L.Rhat = (float*)dev_alloc(c, B * N * m * m * 4);
+  L.Rhat = (double*)dev_alloc(c, B * N * m * m * 8);
   L.Shat = (float*)dev_alloc(c, B * N * m * n * 4);
+  L.Shat64 = (double*)dev_alloc(c, B * N * m * n * 8);
   L.Rinv = (float*)dev_alloc(c, B * N * m * m * 4);
   L.Gamma = (float*)dev_alloc(c, B * N * m * m * 4);
   L.K = (float*)dev_alloc(c, B * N * m * n * 4);
@@ -551,7 +554,7 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
   c->d_status = (int32_t*)dev_alloc(c, B * sizeof(int32_t));
   c->scratch_floats = replay_smem_floats(c);  // doubles
   if (c->scratch_floats * 8 > kReplaySmemMax) c->d_scratch = (double*)dev_alloc(c, B * c->scratch_floats * 8);
-  bool fail = !L.Ps || !L.As || !L.Cs || !L.cvf_rec || !L.cotA || !L.cot_rec || !L.Rhat || !L.Shat || !L.Rinv ||
+  bool fail = !L.Ps || !L.As || !L.Cs || !L.cvf_rec || !L.cotA || !L.cot_rec || !L.Rhat || !L.Shat || !L.Shat64 || !L.Rinv ||
               !L.Gamma || !L.K || !L.cvec || !L.v0 || !L.last_k || !L.last_p || !L.err || !c->d_inst_all || !c->d_inst_list || !c->d_status ||
               (c->scratch_floats * 8 > kReplaySmemMax && !c->d_scratch);
   if (fail) {

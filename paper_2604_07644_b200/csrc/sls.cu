@@ -77,7 +77,8 @@ struct DevSls {
   const int* mp_loff;
   int mp_nslots, mp_nops, mp_layers;
   float *Ps, *As, *Cs, *Ms;
-  float *Qx, *Qu, *Qux, *Kc, *Phiu;
+  double *Qx, *Qu, *Qux;  // cost blocks (float64: the leaf Schur complement cancels O(tau) terms)
+  float *Kc, *Phiu;
   double* rn;
   ErrSlot* err;
   int have_response;
@@ -126,9 +127,9 @@ static int sls_init(Ctx* c) {
   S.As = (float*)dev_alloc(c, B * S.cvf_nslots * MS * 4);
   S.Cs = (float*)dev_alloc(c, B * S.cvf_nslots * MS * 4);
   S.Ms = (float*)dev_alloc(c, B * S.mp_nslots * MS * 4);
-  S.Qx = (float*)dev_alloc(c, B * S.ncell * MS * 4);
-  S.Qu = (float*)dev_alloc(c, B * S.ncell * m * m * 4);
-  S.Qux = (float*)dev_alloc(c, B * S.ncell * m * n * 4);
+  S.Qx = (double*)dev_alloc(c, B * S.ncell * n * n * 8);
+  S.Qu = (double*)dev_alloc(c, B * S.ncell * m * m * 8);
+  S.Qux = (double*)dev_alloc(c, B * S.ncell * m * n * 8);
   S.Kc = (float*)dev_alloc(c, B * S.ncell * m * n * 4);
   S.Phiu = (float*)dev_alloc(c, B * S.ncell * m * n * 4);
   S.rn = (double*)dev_alloc(c, B * S.ncell * S.cmax * 8);
@@ -146,70 +147,62 @@ static int sls_init(Ctx* c) {
 
 // [C D]' diag(tau) [C D] + blkdiag(Qbar, Rbar) per cell; terminal cells (k = N)
 // get CN' diag(tau_N) CN + QbarN.  Weights are per instance (stride wst, 0 = shared).
+// float64 throughout; Qx is stored unpadded n x n.
 __global__ void __launch_bounds__(256) k_sls_assemble(DevSls S, gsls_qp_t qp, const double* tau,
                                                       const double* tau_term, const float* Qbar, const float* Rbar,
                                                       const float* QbarN, long long wst) {
   const int cell = blockIdx.x, inst = blockIdx.y;
   const int2 kj = S.cell_kj[cell];
   const int k = kj.x, j = kj.y;
-  const int n = S.n, m = S.m, c = S.c, nf = S.nf, N = S.N, ldg = S.ldg;
-  const size_t MS = (size_t)n * ldg;
-  float* Qx = S.Qx + ((size_t)inst * S.ncell + cell) * MS;
-  extern __shared__ float sm[];
-  float* t = sm;  // c or nf
+  const int n = S.n, m = S.m, c = S.c, nf = S.nf, N = S.N;
+  const size_t cb = (size_t)inst * S.ncell + cell;
+  double* Qx = S.Qx + cb * n * n;
+  extern __shared__ double smd[];
+  double* t = smd;  // c or nf
   if (k == N) {
     const float* CN = qp.CN + (size_t)inst * nf * n;
     const float* QbN = QbarN + (size_t)inst * wst * n * n;
-    for (int f = threadIdx.x; f < nf; f += blockDim.x)
-      t[f] = tau_term ? (float)tau_term[((size_t)inst * N + j) * nf + f] : 0.f;
+    for (int f = threadIdx.x; f < nf; f += blockDim.x) t[f] = tau_term ? tau_term[((size_t)inst * N + j) * nf + f] : 0.0;
     __syncthreads();
-    for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
-      const int i = e / ldg, jj = e - i * ldg;
-      float v = 0.f;
-      if (jj < n) {
-        float s = 0.f;
-        for (int f = 0; f < nf; ++f) s = fmaf(CN[f * n + i] * t[f], CN[f * n + jj], s);
-        v = s + QbN[i * n + jj];
-      }
-      Qx[e] = v;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e / n, jj = e - i * n;
+      double s = 0.0;
+      for (int f = 0; f < nf; ++f) s = fma((double)CN[f * n + i] * t[f], (double)CN[f * n + jj], s);
+      Qx[e] = s + (double)QbN[e];
     }
     return;
   }
   const size_t st = (size_t)inst * N + k;
   const float* Ck = qp.C + st * c * n;
   const float* Dk = qp.D + st * c * m;
-  for (int r = threadIdx.x; r < c; r += blockDim.x)
-    t[r] = tau ? (float)tau[((size_t)inst * S.ncell + cell) * c + r] : 0.f;
+  for (int r = threadIdx.x; r < c; r += blockDim.x) t[r] = tau ? tau[cb * c + r] : 0.0;
   __syncthreads();
   const float* Qb = Qbar + (size_t)inst * wst * n * n;
   const float* Rb = Rbar + (size_t)inst * wst * m * m;
-  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
-    const int i = e / ldg, jj = e - i * ldg;
-    float v = 0.f;
-    if (jj < n) {
-      float s = 0.f;
-      for (int r = 0; r < c; ++r) s = fmaf(Ck[r * n + i] * t[r], Ck[r * n + jj], s);
-      v = s + Qb[i * n + jj];
-    }
-    Qx[e] = v;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, jj = e - i * n;
+    double s = 0.0;
+    for (int r = 0; r < c; ++r) s = fma((double)Ck[r * n + i] * t[r], (double)Ck[r * n + jj], s);
+    Qx[e] = s + (double)Qb[e];
   }
-  float* Qu = S.Qu + ((size_t)inst * S.ncell + cell) * m * m;
+  double* Qu = S.Qu + cb * m * m;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
     const int a = e / m, b = e - a * m;
-    float s = 0.f;
-    for (int r = 0; r < c; ++r) s = fmaf(Dk[r * m + a] * t[r], Dk[r * m + b], s);
-    Qu[e] = s + Rb[e];
+    double s = 0.0;
+    for (int r = 0; r < c; ++r) s = fma((double)Dk[r * m + a] * t[r], (double)Dk[r * m + b], s);
+    Qu[e] = s + (double)Rb[e];
   }
-  float* Qux = S.Qux + ((size_t)inst * S.ncell + cell) * m * n;
+  double* Qux = S.Qux + cb * m * n;
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     const int a = e / n, i = e - a * n;
-    float s = 0.f;
-    for (int r = 0; r < c; ++r) s = fmaf(Dk[r * m + a] * t[r], Ck[r * n + i], s);
+    double s = 0.0;
+    for (int r = 0; r < c; ++r) s = fma((double)Dk[r * m + a] * t[r], (double)Ck[r * n + i], s);
     Qux[e] = s;
   }
 }
 
-// Grid leaves: Qu^-1, P = Qx - Qux' Qu^-1 Qux, A = A_k - B_k Qu^-1 Qux, C = B_k Qu^-1 B_k'.
+// Grid leaves (float64 algebra, float32 result): Qu^-1, P = Qx - Qux' Qu^-1 Qux,
+// A = A_k - B_k Qu^-1 Qux, C = B_k Qu^-1 B_k'.
 __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   const int cell = blockIdx.x, inst = blockIdx.y;
   const int2 kj = S.cell_kj[cell];
@@ -220,20 +213,25 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   float* Pd = S.Ps + ((size_t)inst * S.cvf_nslots + slot) * MS;
   float* Ad = S.As + ((size_t)inst * S.cvf_nslots + slot) * MS;
   float* Cd = S.Cs + ((size_t)inst * S.cvf_nslots + slot) * MS;
-  const float* Qx = S.Qx + ((size_t)inst * S.ncell + cell) * MS;
+  const size_t cb = (size_t)inst * S.ncell + cell;
+  const double* Qx = S.Qx + cb * n * n;
   if (k == N) {  // terminal element (Qx_term, 0, 0)
-    for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) { Pd[e] = Qx[e]; Ad[e] = 0.f; Cd[e] = 0.f; }
+    for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
+      const int i = e / ldg, jj = e - i * ldg;
+      Pd[e] = (jj < n) ? (float)Qx[i * n + jj] : 0.f;
+      Ad[e] = 0.f;
+      Cd[e] = 0.f;
+    }
     return;
   }
-  extern __shared__ float sm[];
-  float* Qu = sm;             // m x m
-  float* Qi = Qu + m * m;     // m x m
-  float* Qux = Qi + m * m;    // m x n
-  float* QQ = Qux + m * n;    // m x n
-  float* Bk = QQ + m * n;     // n x m
-  float* BQ = Bk + n * m;     // n x m
-  float* wk = BQ + n * m;
-  const size_t cb = (size_t)inst * S.ncell + cell;
+  extern __shared__ double smd[];
+  double* Qu = smd;            // m x m
+  double* Qi = Qu + m * m;     // m x m
+  double* Qux = Qi + m * m;    // m x n
+  double* QQ = Qux + m * n;    // m x n
+  double* Bk = QQ + m * n;     // n x m
+  double* BQ = Bk + n * m;     // n x m
+  double* wk = BQ + n * m;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) Qu[e] = S.Qu[cb * m * m + e];
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) Qux[e] = S.Qux[cb * m * n + e];
   const size_t st = (size_t)inst * N + k;
@@ -246,40 +244,41 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   __syncthreads();
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     const int a = e / n, i = e - a * n;
-    float s = 0.f;
-    for (int b = 0; b < m; ++b) s = fmaf(Qi[a * m + b], Qux[b * n + i], s);
+    double s = 0.0;
+    for (int b = 0; b < m; ++b) s = fma(Qi[a * m + b], Qux[b * n + i], s);
     QQ[e] = s;
   }
   for (int e = threadIdx.x; e < n * m; e += blockDim.x) {
     const int i = e / m, a = e - i * m;
-    float s = 0.f;
-    for (int b = 0; b < m; ++b) s = fmaf(Bk[i * m + b], Qi[b * m + a], s);
+    double s = 0.0;
+    for (int b = 0; b < m; ++b) s = fma(Bk[i * m + b], Qi[b * m + a], s);
     BQ[e] = s;
   }
   __syncthreads();
   const float* Ak = qp.A + st * n * n;
   for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
     const int i = e / ldg, jj = e - i * ldg;
-    float p = 0.f, a = 0.f, cc = 0.f;
+    double p = 0.0, a = 0.0, cc = 0.0;
     if (jj < n) {
-      float s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
       for (int l = 0; l < m; ++l) {
-        s1 = fmaf(Qux[l * n + i], QQ[l * n + jj], s1);
-        s2 = fmaf(Bk[i * m + l], QQ[l * n + jj], s2);
-        s3 = fmaf(BQ[i * m + l], Bk[jj * m + l], s3);
+        s1 = fma(Qux[l * n + i], QQ[l * n + jj], s1);
+        s2 = fma(Bk[i * m + l], QQ[l * n + jj], s2);
+        s3 = fma(BQ[i * m + l], Bk[jj * m + l], s3);
       }
-      p = Qx[i * ldg + jj] - s1;
-      a = Ak[i * n + jj] - s2;
+      p = Qx[i * n + jj] - s1;
+      a = (double)Ak[i * n + jj] - s2;
       cc = s3;
     }
-    Pd[e] = p;
-    Ad[e] = a;
-    Cd[e] = cc;
+    Pd[e] = (float)p;
+    Ad[e] = (float)a;
+    Cd[e] = (float)cc;
   }
 }
 
 // Gains on cell (k, j), k <= N-1, from P+ = P(k+1, j); closed loop -> product
-// leaf of position k.  Cell (N, j) writes E_j into the leaf of position j.
+// leaf of position k (float64 algebra).  Cell (N, j) writes E_j into the leaf
+// of position j.
 __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const float* E) {
   const int cell = blockIdx.x, inst = blockIdx.y;
   const int2 kj = S.cell_kj[cell];
@@ -296,41 +295,39 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
     }
     return;
   }
-  extern __shared__ float sm[];
-  float* Pn = sm;               // n x ldg
-  float* Bst = Pn + n * ldg;    // n x m
-  float* BtP = Bst + n * m;     // m x n
-  float* H = BtP + m * n;       // m x m
-  float* Gm = H + m * m;        // m x n
-  float* Ga = Gm + m * m;       // m x m
-  float* Ks = Ga + m * m;       // m x n
-  float* wk = Ks + m * n;
-  const float* Pg = S.Ps + ((size_t)inst * S.cvf_nslots + S.cvf_out[cell_of(N, k + 1, j)]) * MS;
-  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) Pn[e] = Pg[e];
+  extern __shared__ double smd[];
+  double* Bst = smd;             // n x m
+  double* BtP = Bst + n * m;     // m x n
+  double* H = BtP + m * n;       // m x m
+  double* Gm = H + m * m;        // m x n
+  double* Ga = Gm + m * n;       // m x m
+  double* Ks = Ga + m * m;       // m x n
+  double* wk = Ks + m * n;
+  const float* Pn = S.Ps + ((size_t)inst * S.cvf_nslots + S.cvf_out[cell_of(N, k + 1, j)]) * MS;
   const size_t st = (size_t)inst * N + k;
   for (int e = threadIdx.x; e < n * m; e += blockDim.x) Bst[e] = qp.B[st * n * m + e];
   __syncthreads();
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     const int l = e / n, jj = e - l * n;
-    float s = 0.f;
-    for (int i = 0; i < n; ++i) s = fmaf(Bst[i * m + l], Pn[i * ldg + jj], s);
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s = fma(Bst[i * m + l], (double)Pn[i * ldg + jj], s);
     BtP[e] = s;
   }
   __syncthreads();
   const float* Ak = qp.A + st * n * n;
   const size_t cb = (size_t)inst * S.ncell + cell;
-  const float* Qu = S.Qu + cb * m * m;
-  const float* Qux = S.Qux + cb * m * n;
+  const double* Qu = S.Qu + cb * m * m;
+  const double* Qux = S.Qux + cb * m * n;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
     const int l = e / m, t = e - l * m;
-    float s = 0.f;
-    for (int i = 0; i < n; ++i) s = fmaf(BtP[l * n + i], Bst[i * m + t], s);
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s = fma(BtP[l * n + i], Bst[i * m + t], s);
     H[e] = Qu[e] + s;
   }
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     const int l = e / n, jj = e - l * n;
-    float s = 0.f;
-    for (int i = 0; i < n; ++i) s = fmaf(BtP[l * n + i], Ak[i * n + jj], s);
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s = fma(BtP[l * n + i], (double)Ak[i * n + jj], s);
     Gm[e] = Qux[e] + s;
   }
   __syncthreads();
@@ -342,22 +339,22 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   float* Kg = S.Kc + cb * m * n;
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     const int l = e / n, jj = e - l * n;
-    float s = 0.f;
-    for (int t = 0; t < m; ++t) s = fmaf(Ga[l * m + t], Gm[t * n + jj], s);
+    double s = 0.0;
+    for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Gm[t * n + jj], s);
     Ks[e] = -s;
-    Kg[e] = -s;
+    Kg[e] = (float)(-s);
   }
   __syncthreads();
   float* Ml = Mbase + (size_t)cell_of(N, k + 1, j) * MS;  // product leaf of position k
   for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
     const int i = e / ldg, jj = e - i * ldg;
-    float v = 0.f;
+    double v = 0.0;
     if (jj < n) {
-      float s = 0.f;
-      for (int l = 0; l < m; ++l) s = fmaf(Bst[i * m + l], Ks[l * n + jj], s);
-      v = Ak[i * n + jj] + s;
+      double s = 0.0;
+      for (int l = 0; l < m; ++l) s = fma(Bst[i * m + l], Ks[l * n + jj], s);
+      v = (double)Ak[i * n + jj] + s;
     }
-    Ml[e] = v;
+    Ml[e] = (float)v;
   }
 }
 
@@ -377,20 +374,44 @@ __global__ void __launch_bounds__(512) k_matprod(float* Ms, long long inst_strid
   gemm_tn(n, Lt, Er, lds, EpiGlobal{base + (size_t)op.x * MS, nullptr, ldg});
 }
 
-// Phi^u = K Phi^x and the constraint-row norms of C Phi^x + D Phi^u (terminal: CN Phi^x).
-__global__ void __launch_bounds__(256) k_sls_phi(DevSls S, gsls_qp_t qp) {
+// Phi^u_{k,j} = K_{k,j} Phi^x_{k,j} (sls.py:310-318).
+__global__ void __launch_bounds__(256) k_sls_phiu(DevSls S) {
   const int cell = blockIdx.x, inst = blockIdx.y;
-  const int2 kj = S.cell_kj[cell];
-  const int k = kj.x;
+  const int k = S.cell_kj[cell].x;
+  if (k >= S.N) return;
+  const int n = S.n, m = S.m, ldg = S.ldg;
+  const size_t MS = (size_t)n * ldg;
+  extern __shared__ float sm[];
+  float* Px = sm;
+  const float* Pg = S.Ms + ((size_t)inst * S.mp_nslots + S.mp_out[cell]) * MS;
+  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) Px[e] = Pg[e];
+  __syncthreads();
+  const size_t cb = (size_t)inst * S.ncell + cell;
+  const float* Kg = S.Kc + cb * m * n;
+  float* Pug = S.Phiu + cb * m * n;
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+    const int a = e / n, i = e - a * n;
+    float s = 0.f;
+    for (int l = 0; l < n; ++l) s = fmaf(Kg[a * n + l], Px[l * ldg + i], s);
+    Pug[e] = s;
+  }
+}
+
+// Row norms of C_k Phi^x + D_k Phi^u (terminal cells: CN Phi^x), sls.py:146-147, :167, :336, :340.
+__global__ void __launch_bounds__(256) k_sls_rownorm(DevSls S, gsls_qp_t qp) {
+  const int cell = blockIdx.x, inst = blockIdx.y;
+  const int k = S.cell_kj[cell].x;
   const int n = S.n, m = S.m, c = S.c, nf = S.nf, N = S.N, ldg = S.ldg;
   const size_t MS = (size_t)n * ldg;
   extern __shared__ float sm[];
   float* Px = sm;            // n x ldg
   float* Pu = Px + n * ldg;  // m x n
   const float* Pg = S.Ms + ((size_t)inst * S.mp_nslots + S.mp_out[cell]) * MS;
-  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) Px[e] = Pg[e];
-  __syncthreads();
   const size_t cb = (size_t)inst * S.ncell + cell;
+  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) Px[e] = Pg[e];
+  if (k < N)
+    for (int e = threadIdx.x; e < m * n; e += blockDim.x) Pu[e] = S.Phiu[cb * m * n + e];
+  __syncthreads();
   double* rn = S.rn + cb * S.cmax;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   if (k == N) {
@@ -407,16 +428,6 @@ __global__ void __launch_bounds__(256) k_sls_phi(DevSls S, gsls_qp_t qp) {
     }
     return;
   }
-  const float* Kg = S.Kc + cb * m * n;
-  float* Pug = S.Phiu + cb * m * n;
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
-    const int a = e / n, i = e - a * n;
-    float s = 0.f;
-    for (int l = 0; l < n; ++l) s = fmaf(Kg[a * n + l], Px[l * ldg + i], s);
-    Pu[e] = s;
-    Pug[e] = s;
-  }
-  __syncthreads();
   const size_t st = (size_t)inst * N + k;
   const float* Ck = qp.C + st * c * n;
   const float* Dk = qp.D + st * c * m;
@@ -432,6 +443,19 @@ __global__ void __launch_bounds__(256) k_sls_phi(DevSls S, gsls_qp_t qp) {
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     if (lane == 0) rn[r] = sqrt(ss);
   }
+}
+
+// Response import (cell layout, unpadded) for responses built elsewhere.
+__global__ void k_sls_import(DevSls S, const float* phix, const float* phiu) {
+  const int cell = blockIdx.x, inst = blockIdx.y;
+  const int n = S.n, m = S.m, ldg = S.ldg;
+  const size_t cb = (size_t)inst * S.ncell + cell;
+  float* dst = S.Ms + ((size_t)inst * S.mp_nslots + S.mp_out[cell]) * n * ldg;
+  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
+    const int i = e / ldg, j = e - i * ldg;
+    dst[e] = (j < n) ? phix[cb * n * n + i * n + j] : 0.f;
+  }
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) S.Phiu[cb * m * n + e] = phiu[cb * m * n + e];
 }
 
 // h_k = sum_{j<k} rownorm(k, j) (k >= 1; h_0 = 0); hf = sum_j rownorm(N, j).
@@ -453,10 +477,13 @@ __global__ void k_sls_tighten(DevSls S, double* h, double* hf) {
 }
 
 // tau = max(lam, 0) / sqrt(beta + eps), beta = rownorm^2 (0 without a response).
-__global__ void k_sls_duals(DevSls S, const double* lam_s, const double* lam_t, double eps, double* tau,
-                            double* tau_term, double* beta, double* beta_term) {
+// lam is the stacked ADMM multiplier (B, N*nc + nf) (admm.py:82-88).
+__global__ void k_sls_duals(DevSls S, const double* lam, double eps, double* tau, double* tau_term, double* beta,
+                            double* beta_term) {
   const int inst = blockIdx.x;
   const int c = S.c, nf = S.nf, N = S.N;
+  const double* lam_s = lam + (size_t)inst * (N * c + nf);
+  const double* lam_t = lam_s + (size_t)N * c;
   const double* rn = S.rn + (size_t)inst * S.ncell * S.cmax;
   for (int e = threadIdx.x; e < S.ncell * c; e += blockDim.x) {
     const int cell = e / c, r = e - cell * c;
@@ -464,7 +491,7 @@ __global__ void k_sls_duals(DevSls S, const double* lam_s, const double* lam_t, 
     if (kj.x >= N) continue;
     const double v = S.have_response ? rn[(size_t)cell * S.cmax + r] : 0.0;
     const double b = v * v;
-    const double l = fmax(lam_s[((size_t)inst * N + kj.x) * c + r], 0.0);
+    const double l = fmax(lam_s[(size_t)kj.x * c + r], 0.0);
     const size_t o = ((size_t)inst * S.ncell + cell) * c + r;
     tau[o] = l / sqrt(b + eps);
     if (beta) beta[o] = b;
@@ -473,7 +500,7 @@ __global__ void k_sls_duals(DevSls S, const double* lam_s, const double* lam_t, 
     const int j = e / nf, f = e - j * nf;
     const double v = S.have_response ? rn[(size_t)cell_of(N, N, j) * S.cmax + f] : 0.0;
     const double b = v * v;
-    const double l = fmax(lam_t[(size_t)inst * nf + f], 0.0);
+    const double l = fmax(lam_t[f], 0.0);
     tau_term[(size_t)inst * N * nf + e] = l / sqrt(b + eps);
     if (beta_term) beta_term[(size_t)inst * N * nf + e] = b;
   }
@@ -508,7 +535,7 @@ int sls_assemble(Ctx* c, const gsls_qp_t* qp, const double* tau, const double* t
   int rc = sls_init(c);
   if (rc) return rc;
   DevSls& S = sls_of(c)->dev;
-  const size_t sb = (size_t)S.cmax * sizeof(float) + 16;
+  const size_t sb = (size_t)S.cmax * sizeof(double) + 16;
   k_sls_assemble<<<dim3(S.ncell, c->dims.batch), 256, sb, st>>>(S, *qp, tau, tau_term, Qbar, Rbar, QbarN,
                                                                   weights_per_instance ? 1 : 0);
   GSLS_CUDA_CHECK(cudaGetLastError());
@@ -517,19 +544,16 @@ int sls_assemble(Ctx* c, const gsls_qp_t* qp, const double* tau, const double* t
 
 // Explicit costs (cell layout, unpadded): Qx (B,ncell,n,n) with Qx_term on k = N
 // cells, Qu (B,ncell,m,m), Qux (B,ncell,m,n).
-__global__ void k_sls_set_costs(DevSls S, const float* Qx, const float* Qu, const float* Qux) {
+__global__ void k_sls_set_costs(DevSls S, const double* Qx, const double* Qu, const double* Qux) {
   const int cell = blockIdx.x, inst = blockIdx.y;
-  const int n = S.n, m = S.m, ldg = S.ldg;
+  const int n = S.n, m = S.m;
   const size_t cb = (size_t)inst * S.ncell + cell;
-  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
-    const int i = e / ldg, j = e - i * ldg;
-    S.Qx[cb * n * ldg + e] = (j < n) ? Qx[cb * n * n + i * n + j] : 0.f;
-  }
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) S.Qx[cb * n * n + e] = Qx[cb * n * n + e];
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) S.Qu[cb * m * m + e] = Qu[cb * m * m + e];
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) S.Qux[cb * m * n + e] = Qux[cb * m * n + e];
 }
 
-int sls_set_costs(Ctx* c, const float* Qx, const float* Qu, const float* Qux, cudaStream_t st) {
+int sls_set_costs(Ctx* c, const double* Qx, const double* Qu, const double* Qux, cudaStream_t st) {
   int rc = sls_init(c);
   if (rc) return rc;
   DevSls& S = sls_of(c)->dev;
@@ -547,7 +571,7 @@ int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st,
   const size_t MS = mat_elems(n);
   const size_t wk = 2 * kMaxM * (kMaxM + 1) + 8;
   {
-    const size_t sb = (2 * m * m + 2 * m * n + 2 * n * m + wk) * sizeof(float);
+    const size_t sb = (2 * m * m + 2 * m * n + 2 * n * m + wk) * sizeof(double);
     if ((rc = smem_attr((const void*)k_sls_leaf, sb))) return rc;
     k_sls_leaf<<<dim3(S.ncell, B), 256, sb, st>>>(S, *qp);
     GSLS_CUDA_CHECK(cudaGetLastError());
@@ -559,7 +583,7 @@ int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st,
     if ((rc = launch_combine(a, o1 - o0, B, st))) return rc;
   }
   {
-    const size_t sb = ((size_t)n * ldg + n * m + 3 * m * n + 2 * m * m + wk) * sizeof(float);
+    const size_t sb = ((size_t)n * m + 3 * m * n + 2 * m * m + wk) * sizeof(double);
     if ((rc = smem_attr((const void*)k_sls_gains, sb))) return rc;
     k_sls_gains<<<dim3(S.ncell, B), 256, sb, st>>>(S, *qp, E);
     GSLS_CUDA_CHECK(cudaGetLastError());
@@ -576,33 +600,56 @@ int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st,
     }
   }
   {
-    const size_t sb = ((size_t)n * ldg + m * n) * sizeof(float);
-    if ((rc = smem_attr((const void*)k_sls_phi, sb))) return rc;
-    k_sls_phi<<<dim3(S.ncell, B), 256, sb, st>>>(S, *qp);
+    const size_t sb = (size_t)n * ldg * sizeof(float);
+    if ((rc = smem_attr((const void*)k_sls_phiu, sb))) return rc;
+    k_sls_phiu<<<dim3(S.ncell, B), 256, sb, st>>>(S);
     GSLS_CUDA_CHECK(cudaGetLastError());
   }
   S.have_response = 1;
   return check ? check_errors(c, st, "sls.synthesize") : GSLS_OK;
 }
 
-int sls_tighten(Ctx* c, double* h, double* hf, cudaStream_t st) {
+static int sls_rownorms(Ctx* c, const gsls_qp_t* qp, cudaStream_t st) {
+  DevSls& S = sls_of(c)->dev;
+  const size_t sb = ((size_t)S.n * S.ldg + S.m * S.n) * sizeof(float);
+  int rc = smem_attr((const void*)k_sls_rownorm, sb);
+  if (rc) return rc;
+  k_sls_rownorm<<<dim3(S.ncell, c->dims.batch), 256, sb, st>>>(S, *qp);
+  GSLS_CUDA_CHECK(cudaGetLastError());
+  return GSLS_OK;
+}
+
+int sls_import(Ctx* c, const float* phix, const float* phiu, cudaStream_t st) {
+  int rc = sls_init(c);
+  if (rc) return rc;
+  DevSls& S = sls_of(c)->dev;
+  k_sls_import<<<dim3(S.ncell, c->dims.batch), 256, 0, st>>>(S, phix, phiu);
+  GSLS_CUDA_CHECK(cudaGetLastError());
+  S.have_response = 1;
+  return GSLS_OK;
+}
+
+int sls_tighten(Ctx* c, const gsls_qp_t* qp, double* h, double* hf, cudaStream_t st) {
   SlsState* s = sls_of(c);
   if (!s || !s->dev.have_response) {
     set_error(GSLS_ERR_ARG, -1, 0, 0, 0, "no SLS response in context");
     return GSLS_ERR_ARG;
   }
+  int rc = sls_rownorms(c, qp, st);
+  if (rc) return rc;
   k_sls_tighten<<<c->dims.batch, 256, 0, st>>>(s->dev, h, hf);
   GSLS_CUDA_CHECK(cudaGetLastError());
   return GSLS_OK;
 }
 
-int sls_duals(Ctx* c, const double* lam_s, const double* lam_t, double eps, int use_response, double* tau,
-              double* tau_term, double* beta, double* beta_term, cudaStream_t st) {
+int sls_duals(Ctx* c, const gsls_qp_t* qp, const double* lam, double eps, int use_response, int reuse_rownorms,
+              double* tau, double* tau_term, double* beta, double* beta_term, cudaStream_t st) {
   int rc = sls_init(c);
   if (rc) return rc;
   DevSls S = sls_of(c)->dev;
   S.have_response = use_response && S.have_response;
-  k_sls_duals<<<c->dims.batch, 256, 0, st>>>(S, lam_s, lam_t, eps, tau, tau_term, beta, beta_term);
+  if (S.have_response && !reuse_rownorms && (rc = sls_rownorms(c, qp, st))) return rc;
+  k_sls_duals<<<c->dims.batch, 256, 0, st>>>(S, lam, eps, tau, tau_term, beta, beta_term);
   GSLS_CUDA_CHECK(cudaGetLastError());
   return GSLS_OK;
 }
@@ -618,6 +665,44 @@ int sls_export(Ctx* c, float* phix, float* phiu, float* gains, cudaStream_t st) 
   return GSLS_OK;
 }
 
+__global__ void k_sls_export_costs(DevSls S, double* Qx, double* Qu, double* Qux) {
+  const int cell = blockIdx.x, inst = blockIdx.y;
+  const int n = S.n, m = S.m;
+  const size_t cb = (size_t)inst * S.ncell + cell;
+  if (Qx)
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) Qx[cb * n * n + e] = S.Qx[cb * n * n + e];
+  if (Qu)
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) Qu[cb * m * m + e] = S.Qu[cb * m * m + e];
+  if (Qux)
+    for (int e = threadIdx.x; e < m * n; e += blockDim.x) Qux[cb * m * n + e] = S.Qux[cb * m * n + e];
+}
+
+int sls_export_costs(Ctx* c, double* Qx, double* Qu, double* Qux, cudaStream_t st) {
+  int rc = sls_init(c);
+  if (rc) return rc;
+  DevSls& S = sls_of(c)->dev;
+  k_sls_export_costs<<<dim3(S.ncell, c->dims.batch), 256, 0, st>>>(S, Qx, Qu, Qux);
+  GSLS_CUDA_CHECK(cudaGetLastError());
+  return GSLS_OK;
+}
+
 int sls_ncell(int N) { return N * (N + 1) / 2; }
+
+int sls_plan(int N, int cvf, int max_ops, int* ops, int* layer_off, int* out, int* n_ops, int* n_layers,
+             int* n_slots) {
+  ScanPlan p = merge_columns(N, cvf != 0);
+  *n_ops = (int)p.ops.size();
+  *n_layers = p.layers;
+  *n_slots = p.nslots;
+  if ((int)p.ops.size() > max_ops) return GSLS_OK;
+  for (size_t i = 0; i < p.ops.size(); ++i) {
+    ops[3 * i] = p.ops[i].dst;
+    ops[3 * i + 1] = p.ops[i].earlier;
+    ops[3 * i + 2] = p.ops[i].later;
+  }
+  for (int l = 0; l <= p.layers; ++l) layer_off[l] = p.layer_off[l];
+  for (size_t i = 0; i < p.out.size(); ++i) out[i] = p.out[i];
+  return GSLS_OK;
+}
 
 }  // namespace gsls

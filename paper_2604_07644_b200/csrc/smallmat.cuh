@@ -204,35 +204,36 @@ __device__ inline bool gj_inverse(float* a, float* out, int lds, int n, float* b
 
 // ---- SPD inverse (one warp, m <= 24) ---------------------------------------------
 
-// M (ld = ldm) is read; inv (ld = ldm) is written.  work: 2 * 24 * 25 floats.
+// M (ld = ldm) is read; inv (ld = ldm) is written.  work: 2 * 24 * 25 elements.
 // Returns 0 ok, 1 singular (after the ridge retry).  Pivot rule of lqr.py:185-220:
 // Cholesky; min pivot^2 < 1e-10 or failure -> retry with ridge 1e-9 (no pivot
 // test) -> failure is SingularStageError.
-__device__ inline int warp_spd_inverse(const float* M, int ldm, float* inv, int m, float* work) {
+template <class T>
+__device__ inline int warp_spd_inverse(const T* M, int ldm, T* inv, int m, T* work) {
   const int lane = threadIdx.x & 31;
   const int ld = kMaxM + 1;
-  float* L = work;
-  float* X = work + kMaxM * ld;
+  T* L = work;
+  T* X = work + kMaxM * ld;
   for (int attempt = 0; attempt < 2; ++attempt) {
-    const float ridge = attempt ? 1e-9f : 0.f;
+    const T ridge = attempt ? T(1e-9) : T(0);
     for (int e = lane; e < m * m; e += 32) {
       const int i = e / m, j = e % m;
-      L[i * ld + j] = M[i * ldm + j] + ((i == j) ? ridge : 0.f);
+      L[i * ld + j] = M[i * ldm + j] + ((i == j) ? ridge : T(0));
     }
     __syncwarp();
     bool ok = true, small = false;
     for (int j = 0; j < m; ++j) {
-      const float d = L[j * ld + j];
-      if (!(d > 0.f) || !isfinite(d)) { ok = false; break; }
-      const float piv = sqrtf(d);
-      if (piv * piv < 1e-10f) small = true;
+      const T d = L[j * ld + j];
+      if (!(d > T(0)) || !isfinite((double)d)) { ok = false; break; }
+      const T piv = sqrt(d);
+      if ((double)piv * (double)piv < 1e-10) small = true;
       __syncwarp();
       if (lane == j) L[j * ld + j] = piv;
       if (lane > j && lane < m) L[lane * ld + j] /= piv;
       __syncwarp();
       if (lane > j && lane < m) {
-        const float lij = L[lane * ld + j];
-        for (int l = j + 1; l <= lane; ++l) L[lane * ld + l] = fmaf(-lij, L[l * ld + j], L[lane * ld + l]);
+        const T lij = L[lane * ld + j];
+        for (int l = j + 1; l <= lane; ++l) L[lane * ld + l] = fma(-lij, L[l * ld + j], L[lane * ld + l]);
       }
       __syncwarp();
     }
@@ -240,21 +241,19 @@ __device__ inline int warp_spd_inverse(const float* M, int ldm, float* inv, int 
       if (attempt == 1) return 1;
       continue;
     }
-    // X = L^{-1}: lane j solves L x = e_j
-    if (lane < m) {
+    if (lane < m) {  // X = L^{-1}: lane j solves L x = e_j
       const int j = lane;
       for (int i = 0; i < m; ++i) {
-        float s = (i == j) ? 1.f : 0.f;
-        for (int k = j; k < i; ++k) s = fmaf(-L[i * ld + k], X[k * ld + j], s);
-        X[i * ld + j] = (i < j) ? 0.f : s / L[i * ld + i];
+        T s = (i == j) ? T(1) : T(0);
+        for (int k = j; k < i; ++k) s = fma(-L[i * ld + k], X[k * ld + j], s);
+        X[i * ld + j] = (i < j) ? T(0) : s / L[i * ld + i];
       }
     }
     __syncwarp();
-    // inv = X^T X
-    for (int e = lane; e < m * m; e += 32) {
+    for (int e = lane; e < m * m; e += 32) {  // inv = X^T X
       const int i = e / m, j = e % m;
-      float s = 0.f;
-      for (int k = max(i, j); k < m; ++k) s = fmaf(X[k * ld + i], X[k * ld + j], s);
+      T s = T(0);
+      for (int k = max(i, j); k < m; ++k) s = fma(X[k * ld + i], X[k * ld + j], s);
       inv[i * ldm + j] = s;
     }
     __syncwarp();

@@ -1,0 +1,199 @@
+"""Batched, device-resident MPC steps: the hot path of the metric.
+
+``RtiEngine`` runs B independent instances of one plant through
+``sls.rti_robust_step`` (sls.py:500-525) — or the nominal ``sqp.rti_step``
+(sqp.py:272-302) when ``robust=False`` — entirely on one GPU:
+
+    linearize (csrc/models.cu)
+    -> assemble_costs -> synthesize -> tighten (csrc/sls.cu)
+    -> f -= h (tightened re-linearization)
+    -> ADMM QP with cached factorizations (csrc/lqr.cu, csrc/admm.cu)
+    -> compute_duals (tau for the next step) -> plan / warm start / u0
+
+Every buffer is allocated once per engine; a step issues only kernel
+launches plus the ADMM driver's per-rebuild status read.  The drop-in
+functions in ``sls`` / ``sqp`` wrap an engine with batch 1.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .admm import AdmmSettings, DeviceAdmmState, DeviceAdmmStats
+from .device import Context, DeviceQp, field_dtype, stream_ptr, to_dev
+
+F32, F64 = torch.float32, torch.float64
+
+
+def _p(t):
+    return t.data_ptr() if (t is not None and t.numel()) else None
+
+
+class DeviceModel:
+    """Device twin of a plant: parameters, weights and reference uploaded once."""
+
+    def __init__(self, model, N: int):
+        spec = model.device_spec()
+        if spec is None:
+            raise TypeError(f"{type(model).__name__} has no device twin (device_spec() is None)")
+        mid, mparams, cparams = spec
+        self.model = model
+        self.model_id = int(mid)
+        self.params = to_dev(np.concatenate([np.asarray(mparams, float), np.asarray(cparams, float)]), F64)
+        self.cons_offset = len(mparams)
+        self.nx, self.nu, self.nc, self.nf, self.N = model.nx, model.nu, model.nc, model.nf, N
+        Q, R, QN = model.cost_weights()
+        xref, uref = model.reference(N)
+        self.Qw, self.Rw, self.QNw = (to_dev(np.asarray(a, float), F64) for a in (Q, R, QN))
+        self.xref, self.uref = to_dev(xref, F64), to_dev(uref, F64)
+        self.E = to_dev(np.asarray(model.disturbance(np.zeros(self.nx)), float), F64)
+
+
+def alloc_qp(B, n, m, c, nf, N, device=None) -> DeviceQp:
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    shapes = {"A": (B, N, n, n), "B": (B, N, n, m), "b": (B, N, n), "Q": (B, N, n, n), "R": (B, N, m, m),
+              "S": (B, N, m, n), "q": (B, N, n), "r": (B, N, m), "QN": (B, n, n), "qN": (B, n),
+              "C": (B, N, c, n), "D": (B, N, c, m), "f": (B, N, c), "CN": (B, nf, n), "fN": (B, nf),
+              "dx0": (B, n)}
+    return DeviceQp(**{k: torch.zeros(s, dtype=field_dtype(k), device=dev) for k, s in shapes.items()})
+
+
+def linearize_into(ctx: Context, dm: DeviceModel, qp: DeviceQp, x, u, h=None, hf=None, xbar0=None, E=None,
+                   write_weights: bool = True):
+    """sqp.linearize (sqp.py:105-147) of a batch of trajectories into ``qp`` (device)."""
+    a = nat.LinArgs()
+    a.model_id = dm.model_id
+    a.params = dm.params.data_ptr()
+    a.cons_offset = dm.cons_offset
+    a.x, a.u = x.data_ptr(), u.data_ptr()
+    a.h, a.hf = _p(h), _p(hf)
+    a.xbar0 = _p(xbar0)
+    a.Qw, a.Rw, a.QNw = dm.Qw.data_ptr(), dm.Rw.data_ptr(), dm.QNw.data_ptr()
+    a.xref, a.uref = dm.xref.data_ptr(), dm.uref.data_ptr()
+    a.E_const = dm.E.data_ptr()
+    a.write_weights = int(write_weights)
+    s = qp.cstruct()
+    nat.check(ctx.lib.gsls_linearize(ctx.handle, ctypes.byref(a), ctypes.byref(s), _p(E), stream_ptr()),
+              "linearize")
+
+
+class RtiEngine:
+    """B instances of one plant, one robust (or nominal) RTI step per call."""
+
+    def __init__(self, model, N: int, batch: int, settings, robust: bool = True):
+        """``settings`` is an ``sls.RobustSettings`` (robust) or ``sqp.SqpSettings`` (nominal)."""
+        nat.load()
+        self.model = model
+        self.robust = robust
+        self.settings = settings
+        sqp_set = settings.sqp if robust else settings
+        self.admm_settings: AdmmSettings = sqp_set.admm
+        n, m, c, nf = model.nx, model.nu, model.nc, model.nf
+        self.dims = (n, m, c, nf, N)
+        self.B = batch
+        self.ctx = Context(n, m, c, nf, N, batch)
+        self.dm = DeviceModel(model, N)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.qp = alloc_qp(batch, n, m, c, nf, N, dev)
+        self.mtot = N * c + nf
+        self.ncell = N * (N + 1) // 2
+        self.E = torch.zeros(batch, N, n, n, dtype=F32, device=dev)
+        self.h = torch.zeros(batch, N, c, dtype=F64, device=dev)
+        self.hf = torch.zeros(batch, nf, dtype=F64, device=dev)
+        self.tau = torch.zeros(batch, self.ncell, c, dtype=F64, device=dev)
+        self.tau_term = torch.zeros(batch, N, nf, dtype=F64, device=dev)
+        self.beta = torch.zeros_like(self.tau)
+        self.beta_term = torch.zeros_like(self.tau_term)
+        self.tau_valid = False
+        if robust:
+            w = settings.weights
+            if w is None:
+                s = settings.weight_scale
+                Qb, Rb, QbN = s * np.eye(n), s * np.eye(m), s * np.eye(n)
+            else:
+                Qb, Rb, QbN = w.Qbar, w.Rbar, w.QbarN
+            self.Qbar, self.Rbar, self.QbarN = (to_dev(np.asarray(a, float), F32) for a in (Qb, Rb, QbN))
+        self.state = DeviceAdmmState(batch, self.mtot, self.admm_settings.rho0, dev)
+        self.stats = DeviceAdmmStats(batch, dev)
+        d = lambda *s: torch.zeros(s, dtype=F64, device=dev)  # noqa: E731
+        self.dx, self.du = d(batch, N + 1, n), d(batch, N, m)
+        self.plan_x, self.plan_u = d(batch, N + 1, n), d(batch, N, m)
+        self.warm_x, self.warm_u = d(batch, N + 1, n), d(batch, N, m)
+        self.u0 = d(batch, m)
+        self.cost = d(batch)
+        self._weights_written = False
+        self.launches_per_step = 0
+
+    # -- pieces ------------------------------------------------------------------
+    def _reset_admm(self, warm: DeviceAdmmState | None = None):
+        st = self.state
+        if warm is None:
+            st.z.zero_(); st.lam.zero_(); st.y.zero_()
+            st.rho.fill_(float(self.admm_settings.rho0))
+            st.generation.zero_(); st.iteration.zero_()
+            st.r_primal.fill_(np.inf); st.r_dual.fill_(np.inf)
+
+    def step(self, xbar0: torch.Tensor, prev_x: torch.Tensor, prev_u: torch.Tensor, tau=None, tau_term=None,
+             use_tau: bool | None = None, E: torch.Tensor | None = None, warm_admm: bool = False):
+        """One step for every instance.  Inputs are float64 CUDA tensors
+        (B,n), (B,N+1,n), (B,N,m); ``tau``/``tau_term`` (cell layout) override the
+        engine-held duals; ``use_tau=False`` forces the unweighted synthesis."""
+        ctx, lib, qp, S = self.ctx, self.ctx.lib, self.qp, stream_ptr()
+        qs = qp.cstruct()
+        linearize_into(ctx, self.dm, qp, prev_x, prev_u, xbar0=xbar0, E=self.E,
+                       write_weights=not self._weights_written)
+        self._weights_written = True
+        if E is not None:
+            self.E.copy_(E)
+        if self.robust:
+            if tau is not None:
+                self.tau.copy_(tau)
+                self.tau_term.copy_(tau_term)
+                self.tau_valid = True
+            if use_tau is None:
+                use_tau = self.tau_valid
+            nat.check(lib.gsls_sls_assemble(ctx.handle, ctypes.byref(qs), _p(self.tau) if use_tau else None,
+                                            _p(self.tau_term) if use_tau else None, self.Qbar.data_ptr(),
+                                            self.Rbar.data_ptr(), self.QbarN.data_ptr(), 0, S), "assemble_costs")
+            nat.check(lib.gsls_sls_synthesize(ctx.handle, ctypes.byref(qs), self.E.data_ptr(), S), "synthesize")
+            nat.check(lib.gsls_sls_tighten(ctx.handle, ctypes.byref(qs), _p(self.h), _p(self.hf), S), "tighten")
+            nat.check(lib.gsls_apply_tightening(ctx.handle, _p(qp.f), _p(qp.fN), _p(self.h), _p(self.hf), S),
+                      "apply_tightening")
+        if not warm_admm:
+            self._reset_admm()
+        sa, ss, st = self.state.cstruct(), self.stats.cstruct(), self.admm_settings.cstruct()
+        nat.check(lib.gsls_admm_solve_qp(ctx.handle, ctypes.byref(qs), ctypes.byref(st), ctypes.byref(sa),
+                                         ctypes.byref(ss), self.dx.data_ptr(), _p(self.du), S), "admm.solve_qp")
+        if self.robust:
+            eps = float(self.settings.eps)
+            nat.check(lib.gsls_sls_duals(ctx.handle, ctypes.byref(qs), self.state.lam.data_ptr(), eps, 1, 1,
+                                         _p(self.tau), _p(self.tau_term), _p(self.beta), _p(self.beta_term), S),
+                      "compute_duals")
+            self.tau_valid = True
+        nat.check(lib.gsls_rti_apply(ctx.handle, prev_x.data_ptr(), prev_u.data_ptr(), self.dx.data_ptr(),
+                                     self.du.data_ptr(), self.plan_x.data_ptr(), self.plan_u.data_ptr(),
+                                     self.warm_x.data_ptr(), self.warm_u.data_ptr(), self.u0.data_ptr(),
+                                     self.dm.Qw.data_ptr(), self.dm.Rw.data_ptr(), self.dm.QNw.data_ptr(),
+                                     self.dm.xref.data_ptr(), self.dm.uref.data_ptr(), self.cost.data_ptr(), S),
+                  "rti_apply")
+        return self
+
+    # -- views ---------------------------------------------------------------------
+    def lam_split(self):
+        n, m, c, nf, N = self.dims
+        return self.state.lam[:, : N * c].reshape(self.B, N, c), self.state.lam[:, N * c:]
+
+    def export_response(self):
+        """(phix (B,ncell,n,n), phiu, gains (B,ncell,m,n)) float32 device tensors."""
+        n, m, c, nf, N = self.dims
+        dev = self.qp.QN.device
+        phix = torch.empty(self.B, self.ncell, n, n, dtype=F32, device=dev)
+        phiu = torch.empty(self.B, self.ncell, m, n, dtype=F32, device=dev)
+        gains = torch.empty_like(phiu)
+        nat.check(self.ctx.lib.gsls_sls_export(self.ctx.handle, phix.data_ptr(), phiu.data_ptr(),
+                                               gains.data_ptr(), stream_ptr()), "sls export")
+        return phix, phiu, gains

@@ -129,7 +129,10 @@ class Model(abc.ABC):
 
     # -- device twin ---------------------------------------------------------
     def device_spec(self):
-        """(model_id, float64 parameter vector) for csrc/models.cu, or None."""
+        """(model_id, model parameters, constraint block) for csrc/models.cu, or None.
+
+        The constraint block is ``[n_obs, u_min (nu), u_max (nu), (cx, cy, r) * n_obs]``.
+        """
         return None
 
 
@@ -212,7 +215,7 @@ class DubinsCar(_BoxObstacleModel):
         return np.tile(np.asarray(self.goal, float), (N + 1, 1)), np.zeros((N, 1))
 
     def device_spec(self):
-        return DEV_DUBINS, np.concatenate([[self.v, self.dt], self._constraint_params()])
+        return DEV_DUBINS, np.array([self.v, self.dt], float), self._constraint_params()
 
 
 @dataclass(frozen=True)
@@ -262,8 +265,7 @@ class PlanarQuadrotor(_BoxObstacleModel):
                 np.full((N, 2), self.hover_thrust()))
 
     def device_spec(self):
-        return DEV_PLANAR_QUAD, np.concatenate([[self.m, self.L, self.J, self.dt],
-                                                self._constraint_params()])
+        return DEV_PLANAR_QUAD, np.array([self.m, self.L, self.J, self.dt], float), self._constraint_params()
 
 
 @dataclass(frozen=True)
@@ -364,8 +366,8 @@ class NLinkPendulum(_BoxObstacleModel):
 
     def device_spec(self):
         n = self.n_links
-        return DEV_PENDULUM, np.concatenate([[n, self.dt], self._kappa.ravel(), self._inertia,
-                                             self._glever, self._constraint_params()])
+        return (DEV_PENDULUM, np.concatenate([[n, self.dt], self._kappa.ravel(), self._inertia, self._glever]),
+                self._constraint_params())
 
 
 @dataclass(frozen=True)
@@ -441,8 +443,8 @@ class Quadrotor12(_BoxObstacleModel):
                 np.full((N, 4), self.hover_thrust()))
 
     def device_spec(self):
-        return DEV_QUAD12, np.concatenate([[self.mass, self.arm, *self.inertia, self.kappa, self.dt],
-                                           self._constraint_params()])
+        return (DEV_QUAD12, np.array([self.mass, self.arm, *self.inertia, self.kappa, self.dt], float),
+                self._constraint_params())
 
 
 class SyntheticLegged(_BoxObstacleModel):
@@ -517,9 +519,8 @@ class SyntheticLegged(_BoxObstacleModel):
         return np.tile(self._goal, (N + 1, 1)), np.zeros((N, self.nu))
 
     def device_spec(self):
-        return DEV_SYNTH, np.concatenate([[self.dt, self.coupling], self.A0.ravel(),
-                                          self.B0.ravel(), self.W.ravel(),
-                                          self._constraint_params()])
+        return (DEV_SYNTH, np.concatenate([[self.dt, self.coupling], self.A0.ravel(), self.B0.ravel(),
+                                           self.W.ravel()]), self._constraint_params())
 
 
 def quadruped61(seed: int = 0, **kw) -> SyntheticLegged:
