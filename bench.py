@@ -1,0 +1,432 @@
+#!/usr/bin/env python
+"""Benchmark: robust MPC steps (QP + SLS) on B200, BASELINE.json's metric.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--batch B]
+
+Our arm (default): BASELINE cfg-D — one robust RTI step (sls.rti_robust_step:
+linearize, SLS synthesis + tube tightening, tightened ADMM QP, duals) per
+scenario for a batch of 1024 perturbed 61D-quadruped scenarios per GPU
+(weak scaling; ranks gather u0 with NCCL after every step).  ``value`` is
+whole-job solves/s timed with CUDA events; ``e2e`` is the same through the
+public API with inputs copied from pinned host memory and u0/plan read
+back every step.  Single-instance step latency p50/p90 at 61D and 75D is
+reported alongside.  ``cpu_baseline`` times the CPU oracle (a float64
+restatement of the reference, ``oracle/``) on the box's host cores.
+
+Reference arm (--impl reference): the CPU oracle port of the reference
+algorithm on the same workload, all host cores (one single-threaded solve
+per core), rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MPC step latency ms p50 (QP+SLS) at 61D/75D; batched solves/sec at 1-8 GPUs"
+UNIT = "solves/s"
+
+
+# --------------------------------------------------------------------------- helpers
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def W(L):
+    return 2 * (L - 1)
+
+
+def flops_cvf(n):
+    return 50.0 / 3.0 * n ** 3          # 16 2/3 n^3 per CVF combine (matrix part)
+
+
+def bytes_replay_iter(n, m, c, nf, N):
+    """SURVEY §8d B_iter: algorithmic bytes of one cached ADMM iteration (fp32 convention)."""
+    return 4 * (4 * n * n * W(N + 1) + n * n * W(N) + N * (n * n + 2 * m * m + 3 * n * m + 2 * c * (n + m) + 5 * n
+                                                          + 3 * m + 5 * c) + 2 * nf * n)
+
+
+# --------------------------------------------------------------------------- CPU arms
+
+def _oracle_worker(args):
+    tag, idx = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    sys.path.insert(0, ROOT)
+    from paper_2604_07644_b200 import scenarios
+    import oracle
+    wl = scenarios.rti_workload(tag)
+    m = wl.model
+    rs = oracle_settings(m)
+    tau = oracle.sls.Duals.zero(wl.N, m.nc, m.nf, rs.eps)
+    tau.tau = wl.tau
+    tau.tau_term = wl.tau_term
+    x = wl.scenario_states(idx, 1)[0]
+    t = time.perf_counter()
+    r = oracle.sls.rti_robust_step(m, x, oracle.sqp.Trajectory(wl.prev_x, wl.prev_u, m.dt), tau, rs)
+    return time.perf_counter() - t, r.stats.admm_iterations
+
+
+def oracle_settings(model):
+    import oracle
+    from paper_2604_07644_b200 import scenarios as S
+    return oracle.sls.RobustSettings(
+        sqp=oracle.sqp.Settings(admm=oracle.admm.Settings(**S.ADMM), **S.SQP), eps=S.EPS,
+        weights=oracle.sls.Weights(np.eye(model.nx), S.RBAR * np.eye(model.nu), np.eye(model.nx)))
+
+
+def cpu_round(pool, tag, first, count):
+    t = time.perf_counter()
+    res = pool.map(_oracle_worker, [(tag, first + i) for i in range(count)])
+    return time.perf_counter() - t, res
+
+
+def _worker_init():
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OMP_NUM_THREADS"] = "1"
+
+
+def make_pool(cores):
+    import multiprocessing as mp
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"   # inherited by the spawned workers before numpy loads
+    ctx = mp.get_context("spawn")
+    pool = ctx.Pool(cores, initializer=_worker_init)
+    os.environ.pop("OPENBLAS_NUM_THREADS", None)
+    return pool
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    pool = make_pool(cores)
+    try:
+        for w in range(args.warmup):
+            cpu_round(pool, "q61", w * cores, cores)
+        t_tot, n_tot = 0.0, 0
+        per = []
+        for k in range(args.steps):
+            dt, res = cpu_round(pool, "q61", (args.warmup + k) * cores, cores)
+            t_tot += dt
+            n_tot += len(res)
+            per.extend(r[0] for r in res)
+    finally:
+        pool.close()
+    value = n_tot / t_tot
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_tot / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": workload_config(args.batch, world),
+           "latency_ms_p50": {"q61": 1e3 * statistics.median(per)},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                            "sample": f"{args.steps} rounds x {cores} q61 scenarios, one oracle rti_robust_step each "
+                                      "(single-threaded numpy per core, multiprocessing pool)"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+
+def workload_config(batch, world):
+    return {"workload": "cfg-D: 61D/12u synthetic quadruped, one robust RTI step (linearize + SLS synthesis/"
+                        "tightening + tightened ADMM QP + duals) per scenario, N=25, nc=26, nf=2",
+            "batch_per_gpu": batch, "N": 25, "nx": 61, "nu": 12, "parallelism": f"dp{world} (independent scenarios; "
+            "NCCL all_gather of u0 per step)", "l2": "inputs larger than L2 (per-step SLS/LQR workspace >> 126 MB)",
+            "timing": "CUDA events on the launching stream, max over ranks"}
+
+
+def latency(tag, steps=30, warmup=5):
+    """Single-instance robust RTI step latency (device events) and through the drop-in API."""
+    import torch
+    from paper_2604_07644_b200 import scenarios, sls, sqp
+    from paper_2604_07644_b200.engine import RtiEngine
+    from paper_2604_07644_b200.sls import ragged_to_cells
+    wl = scenarios.rti_workload(tag)
+    m = wl.model
+    rs = scenarios.our_settings()(m)
+    eng = RtiEngine(m, wl.N, 1, rs)
+    d = lambda a: torch.as_tensor(np.asarray(a), dtype=torch.float64, device="cuda").contiguous()  # noqa: E731
+    xb, px, pu = d(wl.xbar0[None]), d(wl.prev_x[None]), d(wl.prev_u[None])
+    tc, tt = d(ragged_to_cells(wl.tau, wl.N, (m.nc,))[None]), d(wl.tau_term[None])
+    times = []
+    for i in range(warmup + steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        eng.step(xb, px, pu, tau=tc, tau_term=tt)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= warmup:
+            times.append(e0.elapsed_time(e1))
+    its = int(eng.stats.iterations[0])
+    # end to end through the public drop-in API (numpy in, numpy out)
+    tau = sls.SlsDuals.zero(wl.N, m.nc, m.nf, rs.eps)
+    tau.tau, tau.tau_term = wl.tau, wl.tau_term
+    prev = sqp.Trajectory(wl.prev_x, wl.prev_u, m.dt)
+    e2e = []
+    for i in range(warmup + steps // 2):
+        t = time.perf_counter()
+        sls.rti_robust_step(m, wl.xbar0, prev, tau, rs).u0
+        torch.cuda.synchronize()
+        if i >= warmup:
+            e2e.append(1e3 * (time.perf_counter() - t))
+    del eng
+    return {"p50": statistics.median(times), "p90": float(np.percentile(times, 90)), "admm_iterations": its,
+            "e2e_p50": statistics.median(e2e)}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2604_07644_b200 import _native as nat, scenarios
+    from paper_2604_07644_b200.engine import RtiEngine
+    from paper_2604_07644_b200.sls import ragged_to_cells
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = nat.load()
+    peaks = measured_peaks()
+
+    lat = {}
+    if rank == 0 and not args.no_latency:
+        for tag in ("q61", "h75"):
+            lat[tag] = latency(tag)
+
+    wl = scenarios.rti_workload("q61")
+    m = wl.model
+    B = args.batch
+    n, mu, c, nf, N = m.nx, m.nu, m.nc, m.nf, wl.N
+    rs = scenarios.our_settings()(m)
+    eng = RtiEngine(m, N, B, rs)
+    d = lambda a: torch.as_tensor(np.asarray(a), dtype=torch.float64, device="cuda").contiguous()  # noqa: E731
+    xs = wl.scenario_states(rank * B, B)
+    host = {"xbar0": xs, "prev_x": np.broadcast_to(wl.prev_x, (B,) + wl.prev_x.shape).copy(),
+            "prev_u": np.broadcast_to(wl.prev_u, (B,) + wl.prev_u.shape).copy(),
+            "tau": np.broadcast_to(ragged_to_cells(wl.tau, N, (c,)), (B, N * (N + 1) // 2, c)).copy(),
+            "tau_term": np.broadcast_to(wl.tau_term, (B, N, nf)).copy()}
+    dev = {k: d(v) for k, v in host.items()}
+    gathered = torch.empty(world * B, mu, dtype=torch.float64, device="cuda")
+
+    def step(inp):
+        eng.step(inp["xbar0"], inp["prev_x"], inp["prev_u"], tau=inp["tau"], tau_term=inp["tau_term"])
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, eng.u0)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step(dev)
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- timed: device-resident inputs ------------------------------------------
+    lib.gsls_prof_enable(1)
+    lib.gsls_prof_read(None, None, None, 0)
+    its = []
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            step(dev)
+            its.append(eng.stats.iterations.clone())
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+    lib.gsls_prof_enable(0)
+    ms = e0.elapsed_time(e1)
+    nfam = len(nat.PROF_FAMILIES)
+    pm, pu_, pl = np.zeros(nfam), np.zeros(nfam), np.zeros(nfam, np.int64)
+    lib.gsls_prof_read(pm.ctypes.data, pu_.ctypes.data, pl.ctypes.data, nfam)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t)
+    value = world * B * args.steps / (ms_max / 1e3)
+    its_all = torch.stack(its).double()
+
+    # ---- timed: end to end through the API with host buffers ---------------------
+    pinned = {k: torch.as_tensor(v).pin_memory() for k, v in host.items()}
+    out_u0 = torch.empty(B, mu, dtype=torch.float64).pin_memory()
+    out_plan = torch.empty(B, N + 1, n, dtype=torch.float64).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in pinned.values())
+    d2h = out_u0.numel() * 8 + out_plan.numel() * 8
+    torch.cuda.synchronize()
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record()
+    for _ in range(args.steps):
+        inp = {k: t.to("cuda", non_blocking=True) for k, t in pinned.items()}
+        step(inp)
+        out_u0.copy_(eng.u0, non_blocking=True)
+        out_plan.copy_(eng.plan_x, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    e3.record()
+    torch.cuda.synchronize()
+    barrier()
+    ms_e = torch.tensor([e2.elapsed_time(e3)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_e, op=dist.ReduceOp.MAX)
+    e2e_value = world * B * args.steps / (float(ms_e) / 1e3)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel family ------------------------------------
+    fam = dict(zip(nat.PROF_FAMILIES, zip(pm, pu_, pl)))
+    clk = clocks.summary()
+    sm_max = clk["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    phases = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[2] / args.steps} for k, v in fam.items()
+              if v[2]}
+    total_iters = float(its_all.sum())
+    rl = {}
+    for k in ("sls_cvf", "cvf_lqr"):
+        t_ms, units, nl = fam[k]
+        if nl:
+            ach = units * flops_cvf(n) / (t_ms / 1e3) / 1e12
+            rl[k] = {"bound": "fp32-simt", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
+                     "frac": ach / fp32_peak, "traffic": None}
+    t_ms, units, nl = fam["replay"]
+    if nl:
+        ach = total_iters * bytes_replay_iter(n, mu, c, nf, N) / (t_ms / 1e3) / 1e9
+        rl["replay"] = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                        "traffic": None}
+    dom = max(fam, key=lambda k: fam[k][0])
+    roof = dict(rl.get(dom, {}), kernel=dom,
+                peak_source=("derived: 148 SMs x 128 FP32 FMA/clk x 2 x max SM clock (no FP32-SIMT figure in "
+                             "MEASURED_PEAKS.json)") if dom in ("sls_cvf", "cvf_lqr") else
+                "MEASURED_PEAKS.json hbm_gbs",
+                work=("units = combines per launch x batch; 16 2/3 n^3 flop per combine (SURVEY §8d)"
+                      if dom in ("sls_cvf", "cvf_lqr") else "B_iter x ADMM iterations (SURVEY §8d)"))
+
+    # ---- CPU baseline (rank 0, N=1 only) -----------------------------------------
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        pool = make_pool(cores)
+        try:
+            dt, res = cpu_round(pool, "q61", 0, cores)
+        finally:
+            pool.close()
+        cpu = {"value": len(res) / dt, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{cores} q61 scenarios, one oracle rti_robust_step each (single-threaded numpy per core)"}
+
+    launches = int(pl.sum())
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32 factorizations / f64 vectors", "data": "synthetic",
+           "config": workload_config(B, world),
+           "latency_ms_p50": {k: v["p50"] for k, v in lat.items()},
+           "latency_ms_p90": {k: v["p90"] for k, v in lat.items()},
+           "latency_e2e_ms_p50": {k: v["e2e_p50"] for k, v in lat.items()},
+           "latency_admm_iterations": {k: v["admm_iterations"] for k, v in lat.items()},
+           "admm_iterations_mean": total_iters / its_all.numel(),
+           "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+           "gpu_launches": launches, "roofline": roof, "roofline_by_kernel": rl, "phases": phases,
+           "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
+           "cpu_baseline": cpu}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=1024)
+    ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

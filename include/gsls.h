@@ -245,6 +245,17 @@ int gsls_rti_apply(gsls_ctx* ctx, const double* prev_x, const double* prev_u, co
                    const double* Rw, const double* QNw, const double* xref, const double* uref, double* cost,
                    void* stream);
 
+/* ---- profiling (bench.py roofline evidence) -----------------------------
+ * When enabled, every kernel launch records a CUDA event pair on its stream.
+ * gsls_prof_read synchronizes and returns, per kernel family (order:
+ * leaf, cvf_lqr, gains, cot, replay, sls_assemble, sls_leaf, sls_cvf,
+ * sls_gains, sls_matprod, sls_phiu, sls_rownorm, sls_small, linearize,
+ * rti_misc): accumulated ms, work units (combines for scan families,
+ * instances for the replay) and launch counts, then resets.  Returns the
+ * number of families. */
+int gsls_prof_enable(int32_t on);
+int gsls_prof_read(double* ms, double* units, int64_t* launches, int32_t max_ids);
+
 #ifdef __cplusplus
 }
 #endif

@@ -91,8 +91,13 @@ _SIGS = {
     "gsls_linearize": ([c_void_p, ctypes.POINTER(LinArgs), ctypes.POINTER(Qp), c_void_p, c_void_p], ctypes.c_int),
     "gsls_traj_eval": ([c_void_p, ctypes.POINTER(LinArgs), c_void_p, c_void_p], ctypes.c_int),
     "gsls_apply_tightening": ([c_void_p] * 6, ctypes.c_int),
+    "gsls_prof_enable": ([ctypes.c_int32], ctypes.c_int),
+    "gsls_prof_read": ([c_void_p, c_void_p, c_void_p, ctypes.c_int32], ctypes.c_int),
     "gsls_rti_apply": ([c_void_p] * 17, ctypes.c_int),
 }
+
+PROF_FAMILIES = ("leaf", "cvf_lqr", "gains", "cot", "replay", "sls_assemble", "sls_leaf", "sls_cvf", "sls_gains",
+                 "sls_matprod", "sls_phiu", "sls_rownorm", "sls_small", "linearize", "rti_misc")
 
 # every symbol include/gsls.h declares (checked by the CPU test suite)
 EXPORTS = tuple(_SIGS)

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "ctx.h"
+#include "prof.h"
 
 namespace gsls {
 
@@ -407,6 +408,7 @@ static int launch_replay(Ctx* c, ReplayArgs& a, int count, cudaStream_t st) {
     if (sb > 48 * 1024)
       GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
   }
+  ProfScope ps(P_REPLAY, st, (double)count);
   k_replay<<<dim3(1, count), 512, sb, st>>>(a);
   GSLS_CUDA_CHECK(cudaGetLastError());
   return GSLS_OK;

@@ -27,8 +27,10 @@ struct DevLqr {
   int cot_nslots, cot_nops, cot_layers;
   // scan values (matrices) per instance: [batch][slots][n*ldg]
   float *Ps, *As, *Cs;   // CVF P, A, C
+  float* ATs;            // CVF A transposed (both orientations kept; see k_cvf_combine)
   float* cvf_rec;        // [batch][cvf_nops][4][n*ldg]: Ups, Pr, Psi, Cl (column-major)
   float* cotA;           // [batch][cot_nslots][n*ldg]
+  float* cotAT;          // transposed
   float* cot_rec;        // [batch][cot_nops][n*ldg]: A_later (column-major)
   // per-stage cache, unpadded row-major: [batch][N][...]
   double* Rhat;          // [batch][N][m*m] augmented R (float64)
@@ -68,8 +70,8 @@ struct CombineArgs {
   int n;
   const int4* ops;
   int op_base;                 // global op index of ops[0] (record offset)
-  float *Ps, *As, *Cs;
-  long long inst_stride;       // floats between instances in Ps/As/Cs
+  float *Ps, *As, *Cs, *ATs;
+  long long inst_stride;       // floats between instances in Ps/As/Cs/ATs
   float* rec;                  // nullptr: no record
   long long rec_inst_stride;   // floats between instances in rec
   const int* list;
@@ -78,6 +80,7 @@ struct CombineArgs {
 };
 int launch_combine(const CombineArgs& a, int nops, int count, cudaStream_t st);
 int combine_threads(int n);
+int matmul_threads(int n);
 int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff);
 void sls_destroy(Ctx* c);
 

@@ -14,7 +14,9 @@
 #include <mutex>
 
 #include "ctx.h"
+#include "prof.h"
 #include "smallmat.cuh"
+#include "gj.cuh"
 
 namespace gsls {
 
@@ -114,6 +116,7 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   const size_t sbase = ((size_t)inst * L.cvf_nslots + k) * MS;
   float* Pd = L.Ps + sbase;
   float* Ad = L.As + sbase;
+  float* ATd = L.ATs + sbase;
   float* Cd = L.Cs + sbase;
   if (k == N) {
     const float* QN = qp.QN + (size_t)inst * n * n;
@@ -128,6 +131,7 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
       }
       Pd[e] = (float)v;
       Ad[e] = 0.f;
+      ATd[e] = 0.f;
       Cd[e] = 0.f;
     }
     return;
@@ -204,6 +208,7 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
     }
     Pd[e] = (float)p;
     Ad[e] = (float)a;
+    if (j < n) ATd[j * ldg + i] = (float)a;
     Cd[e] = (float)cc;
   }
   double* Rhat = L.Rhat + st * m * m;
@@ -216,70 +221,81 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
 }
 
 // Matrix half of the CVF combine (Eq. 28) for one op per CTA; optionally
-// records (Ups, Pr, Psi, Cl) column-major for the replay.
-__global__ void __launch_bounds__(512, 1) k_cvf_combine(CombineArgs a) {
+// records (Ups, Pr, Psi, Cl) column-major for the replay.  Shared with the SLS
+// grid scan (no record).
+//
+// P and C are symmetric in exact arithmetic (value-function Hessians and
+// controllability Gramians, lqr.py:236-238), so Pr and Cl serve as their own
+// transposes; A is kept in both orientations (As, ATs) so every operand
+// arrives by a plain cp.async copy.  Six n x lds smem buffers:
+//   b0 Pr -> W2 | b1 Cl -> Minv -> V | b2 M1 -> Minv^T | b3 Al | b4 Ar^T | b5 W1 -> Psi^T
+template <int NP>
+__global__ void __launch_bounds__(NP == 64 ? 256 : 416, NP == 64 ? 2 : 1) k_cvf_combine(CombineArgs a) {
   const int inst = inst_of(a.list);
   const int4 op = a.ops[blockIdx.x];
   const int n = a.n, ldg = ldg_of(n), lds = lds_of(n);
   const size_t MS = (size_t)n * ldg;
   const size_t BS = (size_t)n * lds;
   extern __shared__ float sm[];
-  float* b0 = sm;            // Pr^T -> Cl^T -> Ups^T
-  float* b1 = b0 + BS;       // Cl -> Minv
-  float* b2 = b1 + BS;       // Al
-  float* b3 = b2 + BS;       // Ar^T
-  float* b4 = b3 + BS;       // M1 -> Minv^T
-  float* b5 = b4 + BS;       // W1 -> Psi^T
-  float* b6 = b5 + BS;       // W2
-  float* gjbuf = b6 + BS;
+  float* b0 = sm;
+  float* b1 = b0 + BS;
+  float* b2 = b1 + BS;
+  float* b3 = b2 + BS;
+  float* b4 = b3 + BS;
+  float* b5 = b4 + BS;
+  float* gjbuf = b5 + BS;
   const long long ib = (long long)inst * a.inst_stride;
-  const float* PE = a.Ps + ib + (size_t)op.y * MS;  // earlier (left)
-  const float* AE = a.As + ib + (size_t)op.y * MS;
-  const float* CE = a.Cs + ib + (size_t)op.y * MS;
-  const float* PL = a.Ps + ib + (size_t)op.z * MS;  // later (right)
-  const float* AL_ = a.As + ib + (size_t)op.z * MS;
-  const float* CL_ = a.Cs + ib + (size_t)op.z * MS;
-  float* PD = a.Ps + ib + (size_t)op.x * MS;
-  float* AD = a.As + ib + (size_t)op.x * MS;
-  float* CD = a.Cs + ib + (size_t)op.x * MS;
+  const size_t oe = (size_t)op.y * MS, ol = (size_t)op.z * MS, od = (size_t)op.x * MS;
   float* rec = a.rec ? a.rec + (long long)inst * a.rec_inst_stride + (size_t)(a.op_base + blockIdx.x) * 4 * MS
                      : nullptr;
 
-  cta_load_t(b0, lds, PL, ldg, n);   // Pr^T
-  cta_load(b1, lds, CE, ldg, n, n);  // Cl
-  cta_load(b2, lds, AE, ldg, n, n);  // Al
-  cta_load_t(b3, lds, AL_, ldg, n);  // Ar^T
+  cta_load_async(b0, lds, a.Ps + ib + ol, n);   // Pr (= Pr^T)
+  cta_load_async(b1, lds, a.Cs + ib + oe, n);   // Cl (= Cl^T)
+  cp_async_commit();
+  cta_load_async(b3, lds, a.As + ib + oe, n);   // Al
+  cta_load_async(b4, lds, a.ATs + ib + ol, n);  // Ar^T
+  cp_async_commit();
+  cp_async_wait<1>();
   __syncthreads();
-  gemm_tn(n, b0, b1, lds, EpiSmem{b4, lds, true});    // M1 = I + Pr Cl
-  gemm_tn(n, b0, b2, lds, EpiSmem{b5, lds, false});   // W1 = Pr Al
-  if (rec) cta_store(rec + 1 * MS, b0, lds, n);        // Pr (column-major)
+  gemm_tn(n, b0, b1, lds, EpiSmem{b2, lds, n, true});   // M1 = I + Pr Cl
+  if (rec) {
+    cta_store(rec + 1 * MS, b0, lds, n);                 // Pr record
+    cta_store(rec + 3 * MS, b1, lds, n);                 // Cl record
+  }
+  cp_async_wait<0>();
   __syncthreads();
-  cta_transpose(b0, b1, lds, n);                        // Cl^T
+  gemm_tn(n, b0, b3, lds, EpiSmem{b5, lds, n, false});  // W1 = Pr Al
   __syncthreads();
-  gemm_tn(n, b0, b3, lds, EpiSmem{b6, lds, false});   // W2 = Cl Ar^T
-  if (rec) cta_store(rec + 3 * MS, b0, lds, n);        // Cl (column-major)
+  gemm_tn(n, b1, b4, lds, EpiSmem{b0, lds, n, false});  // W2 = Cl Ar^T (over Pr)
   __syncthreads();
-  const bool ok = gj_inverse(b4, b1, lds, n, gjbuf, a.rel_tol);  // Minv = M1^{-1} -> b1
+  // Minv = M1^{-1} -> b1 (row-major, over Cl), Minv^T -> b2 (over M1, read first)
+  const bool ok = gj_inverse_rows<NP>(b2, b1, b2, lds, n, gjbuf, a.rel_tol);
   if (!ok && threadIdx.x == 0)
     raise_err(a.err ? a.err + inst : nullptr, GSLS_ERR_ILL_CONDITIONED, a.op_base + blockIdx.x);
-  cta_transpose(b4, b1, lds, n);                        // Minv^T -> b4
-  gemm_tn(n, b1, b2, lds, EpiSmem{b0, lds, false});   // Ups^T = Minv^T Al
+  if (rec) {
+    gemm_tn(n, b1, b3, lds, EpiGlobal{rec, nullptr, ldg, n, nullptr});  // Ups^T = Minv^T Al -> record
+    __syncthreads();
+  }
+  gemm_tn(n, b2, b5, lds, EpiSmem{b1, lds, n, false});  // V = Minv W1 (over Minv)
   __syncthreads();
-  if (rec) cta_store(rec + 0 * MS, b0, lds, n);        // Ups (column-major)
-  gemm_tn(n, b0, b5, lds, EpiGlobal{PD, PE, ldg});    // P = Ups W1 + Pl
+  gemm_tn(n, b3, b1, lds, EpiGlobal{a.Ps + ib + od, a.Ps + ib + oe, ldg, n, nullptr});  // P = Al^T V + Pl
+  gemm_tn(n, b2, b4, lds, EpiSmem{b5, lds, n, false});  // Psi^T = Minv Ar^T (over W1)
   __syncthreads();
-  gemm_tn(n, b4, b3, lds, EpiSmem{b5, lds, false});   // Psi^T = Minv Ar^T
-  __syncthreads();
-  if (rec) cta_store(rec + 2 * MS, b5, lds, n);        // Psi (column-major)
-  gemm_tn(n, b5, b2, lds, EpiGlobal{AD, nullptr, ldg}); // A = Psi Al
-  gemm_tn(n, b5, b6, lds, EpiGlobal{CD, CL_, ldg});    // C = Psi W2 + Cr
+  if (rec) cta_store(rec + 2 * MS, b5, lds, n);          // Psi record
+  gemm_tn(n, b5, b3, lds, EpiGlobal{a.As + ib + od, nullptr, ldg, n, a.ATs + ib + od});  // A = Psi Al (+ A^T)
+  gemm_tn(n, b5, b0, lds, EpiGlobal{a.Cs + ib + od, a.Cs + ib + ol, ldg, n, nullptr});   // C = Psi W2 + Cr
 }
 
 size_t combine_smem_bytes(int n) {
-  return (7 * (size_t)n * lds_of(n) + 3 * ldg_of(n) + 2 * n + 8) * sizeof(float);
+  return (6 * (size_t)n * lds_of(n) + gj_scratch_words(n <= 64 ? 64 : 80)) * sizeof(float);
 }
 
-int combine_threads(int n) {
+int combine_threads(int n) {  // k_cvf_combine needs >= 4*NP threads for the inverse
+  if (n <= 64) return 256;
+  return 416;
+}
+
+int matmul_threads(int n) {
   const int T = ldg_of(n) / 4;
   int t = ((T * T + 31) / 32) * 32;
   if (t < 128) t = 128;
@@ -355,6 +371,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const int
   __syncthreads();
   // closed loop Abar = A + B K -> COT leaf k (leaf 0 carries A = 0, lqr.py:354)
   float* Ad = L.cotA + ((size_t)inst * L.cot_nslots + k) * MS;
+  float* ATd = L.cotAT + ((size_t)inst * L.cot_nslots + k) * MS;
   for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
     const int i = e / ldg, j = e - i * ldg;
     double v = 0.0;
@@ -365,6 +382,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const int
     }
     Abar[e] = (float)v;
     Ad[e] = (k == 0) ? 0.f : (float)v;
+    if (j < n) ATd[j * ldg + i] = (k == 0) ? 0.f : (float)v;
   }
   if (k == 0) {
     __syncthreads();
@@ -378,7 +396,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const int
   }
 }
 
-// COT combine: A = A_later A_earlier; records A_later column-major.
+// COT combine: A = A_later A_earlier (+ transpose); records A_later column-major.
 __global__ void __launch_bounds__(512) k_cot_combine(DevLqr L, const int4* ops, int op_base, const int* list) {
   const int inst = inst_of(list);
   const int4 op = ops[blockIdx.x];
@@ -387,13 +405,15 @@ __global__ void __launch_bounds__(512) k_cot_combine(DevLqr L, const int4* ops, 
   extern __shared__ float sm[];
   float* Art = sm;
   float* Ae = Art + (size_t)n * lds;
-  const float* base = L.cotA + (size_t)inst * L.cot_nslots * MS;
-  cta_load_t(Art, lds, base + (size_t)op.z * MS, ldg, n);
-  cta_load(Ae, lds, base + (size_t)op.y * MS, ldg, n, n);
+  const size_t ib = (size_t)inst * L.cot_nslots * MS;
+  cta_load_async(Art, lds, L.cotAT + ib + (size_t)op.z * MS, n);
+  cta_load_async(Ae, lds, L.cotA + ib + (size_t)op.y * MS, n);
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   float* rec = L.cot_rec + ((size_t)inst * L.cot_nops + op_base + blockIdx.x) * MS;
   cta_store(rec, Art, lds, n);
-  gemm_tn(n, Art, Ae, lds, EpiGlobal{L.cotA + (size_t)inst * L.cot_nslots * MS + (size_t)op.x * MS, nullptr, ldg});
+  gemm_tn(n, Art, Ae, lds, EpiGlobal{L.cotA + ib + (size_t)op.x * MS, nullptr, ldg, n, L.cotAT + ib + (size_t)op.x * MS});
 }
 
 // ---------------------------------------------------------------------------
@@ -418,9 +438,15 @@ static int set_smem(const void* fn, size_t bytes) {
 int launch_combine(const CombineArgs& a, int nops, int count, cudaStream_t st) {
   if (nops == 0 || count == 0) return GSLS_OK;
   const size_t sb = combine_smem_bytes(a.n);
-  int rc = set_smem((const void*)k_cvf_combine, sb);
-  if (rc) return rc;
-  k_cvf_combine<<<dim3(nops, count), combine_threads(a.n), sb, st>>>(a);
+  if (a.n <= 64) {
+    int rc = set_smem((const void*)k_cvf_combine<64>, sb);
+    if (rc) return rc;
+    k_cvf_combine<64><<<dim3(nops, count), combine_threads(a.n), sb, st>>>(a);
+  } else {
+    int rc = set_smem((const void*)k_cvf_combine<80>, sb);
+    if (rc) return rc;
+    k_cvf_combine<80><<<dim3(nops, count), combine_threads(a.n), sb, st>>>(a);
+  }
   GSLS_CUDA_CHECK(cudaGetLastError());
   return GSLS_OK;
 }
@@ -435,6 +461,7 @@ int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_l
     const size_t sb = leaf_smem_bytes(n, d.nu, d.nc);
     int rc = set_smem((const void*)k_leaf_init, sb);
     if (rc) return rc;
+    ProfScope ps(P_LEAF, st, (double)(N + 1) * count);
     k_leaf_init<<<dim3(N + 1, count), 256, sb, st>>>(L, *qp, d_rho, d_list);
     GSLS_CUDA_CHECK(cudaGetLastError());
   }
@@ -442,8 +469,10 @@ int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_l
   const size_t MS = mat_elems(n);
   for (int l = 0; l < c->cvf.layers; ++l) {
     const int o0 = c->cvf_layer_off[l], o1 = c->cvf_layer_off[l + 1];
-    CombineArgs a{n, L.cvf_ops + o0, o0, L.Ps, L.As, L.Cs, (long long)L.cvf_nslots * (long long)MS,
+    CombineArgs a{n, L.cvf_ops + o0, o0, L.Ps, L.As, L.Cs, L.ATs, (long long)L.cvf_nslots * (long long)MS,
                   L.cvf_rec, (long long)L.cvf_nops * 4 * (long long)MS, d_list, L.err, 1e-10f};
+    if (o1 == o0) continue;
+    ProfScope ps(P_CVF_LQR, st, (double)(o1 - o0) * count);
     int rc = launch_combine(a, o1 - o0, count, st);
     if (rc) return rc;
   }
@@ -453,6 +482,7 @@ int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_l
     const size_t sb = gains_smem_bytes(n, d.nu);
     int rc = set_smem((const void*)k_gains, sb);
     if (rc) return rc;
+    ProfScope ps(P_GAINS, st, (double)N * count);
     k_gains<<<dim3(N, count), 256, sb, st>>>(L, *qp, d_list);
     GSLS_CUDA_CHECK(cudaGetLastError());
   }
@@ -464,7 +494,8 @@ int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_l
     for (int l = 0; l < c->cot.layers; ++l) {
       const int o0 = c->cot_layer_off[l], o1 = c->cot_layer_off[l + 1];
       if (o1 == o0) continue;
-      k_cot_combine<<<dim3(o1 - o0, count), combine_threads(n), sb, st>>>(L, L.cot_ops + o0, o0, d_list);
+      ProfScope ps(P_COT, st, (double)(o1 - o0) * count);
+      k_cot_combine<<<dim3(o1 - o0, count), matmul_threads(n), sb, st>>>(L, L.cot_ops + o0, o0, d_list);
       GSLS_CUDA_CHECK(cudaGetLastError());
     }
   }
@@ -535,8 +566,10 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
   L.Ps = (float*)dev_alloc(c, B * L.cvf_nslots * MS * 4);
   L.As = (float*)dev_alloc(c, B * L.cvf_nslots * MS * 4);
   L.Cs = (float*)dev_alloc(c, B * L.cvf_nslots * MS * 4);
+  L.ATs = (float*)dev_alloc(c, B * L.cvf_nslots * MS * 4);
   L.cvf_rec = (float*)dev_alloc(c, B * L.cvf_nops * 4 * MS * 4);
   L.cotA = (float*)dev_alloc(c, B * L.cot_nslots * MS * 4);
+  L.cotAT = (float*)dev_alloc(c, B * L.cot_nslots * MS * 4);
   L.cot_rec = (float*)dev_alloc(c, B * L.cot_nops * MS * 4);
   L.Rhat = (double*)dev_alloc(c, B * N * m * m * 8);
   L.Shat = (float*)dev_alloc(c, B * N * m * n * 4);
@@ -554,7 +587,7 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
   c->d_status = (int32_t*)dev_alloc(c, B * sizeof(int32_t));
   c->scratch_floats = replay_smem_floats(c);  // doubles
   if (c->scratch_floats * 8 > kReplaySmemMax) c->d_scratch = (double*)dev_alloc(c, B * c->scratch_floats * 8);
-  bool fail = !L.Ps || !L.As || !L.Cs || !L.cvf_rec || !L.cotA || !L.cot_rec || !L.Rhat || !L.Shat || !L.Shat64 || !L.Rinv ||
+  bool fail = !L.Ps || !L.As || !L.Cs || !L.ATs || !L.cotAT || !L.cvf_rec || !L.cotA || !L.cot_rec || !L.Rhat || !L.Shat || !L.Shat64 || !L.Rinv ||
               !L.Gamma || !L.K || !L.cvec || !L.v0 || !L.last_k || !L.last_p || !L.err || !c->d_inst_all || !c->d_inst_list || !c->d_status ||
               (c->scratch_floats * 8 > kReplaySmemMax && !c->d_scratch);
   if (fail) {

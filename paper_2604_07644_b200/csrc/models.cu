@@ -12,6 +12,7 @@
 #include <cmath>
 
 #include "ctx.h"
+#include "prof.h"
 
 namespace gsls {
 
@@ -335,6 +336,7 @@ int linearize(Ctx* c, const gsls_linearize_args_t* in, gsls_qp_t* out_qp, float*
   a.f = (double*)out_qp->f; a.fN = (double*)out_qp->fN; a.dx0 = (double*)out_qp->dx0;
   a.err = c->dev.err;
   a.n = d.nx; a.m = d.nu; a.c = d.nc; a.nf = d.nf; a.N = d.N;
+  ProfScope ps(P_LINEARIZE, st, (double)(d.N + 1) * d.batch);
   k_linearize<<<dim3(d.N + 1, d.batch), 128, 0, st>>>(a);
   GSLS_CUDA_CHECK(cudaGetLastError());
   return GSLS_OK;
@@ -360,6 +362,7 @@ int apply_tightening(Ctx* c, double* f, double* fN, const double* h, const doubl
   const long long ns = (long long)d.batch * d.N * d.nc, nt = (long long)d.batch * d.nf;
   if (ns + nt == 0) return GSLS_OK;
   const int blocks = (int)std::min<long long>((ns + nt + 255) / 256, 148 * 8);
+  ProfScope ps(P_RTI_MISC, st, (double)d.batch);
   k_apply_tightening<<<blocks, 256, 0, st>>>(f, fN, h, hf, ns, nt);
   GSLS_CUDA_CHECK(cudaGetLastError());
   return GSLS_OK;
@@ -421,6 +424,7 @@ int rti_apply(Ctx* c, const double* px, const double* pu, const double* dx, cons
               double* plan_u, double* warm_x, double* warm_u, double* u0, const double* Qw, const double* Rw,
               const double* QNw, const double* xref, const double* uref, double* cost, cudaStream_t st) {
   const gsls_dims_t& d = c->dims;
+  ProfScope ps(P_RTI_MISC, st, (double)d.batch);
   k_rti_apply<<<d.batch, 256, 0, st>>>(d.nx, d.nu, d.N, px, pu, dx, du, plan_x, plan_u, warm_x, warm_u, u0, Qw, Rw,
                                        QNw, xref, uref, cost);
   GSLS_CUDA_CHECK(cudaGetLastError());

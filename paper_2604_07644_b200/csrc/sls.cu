@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "ctx.h"
+#include "prof.h"
 #include "smallmat.cuh"
 
 namespace gsls {
@@ -76,7 +77,7 @@ struct DevSls {
   const int* mp_out;
   const int* mp_loff;
   int mp_nslots, mp_nops, mp_layers;
-  float *Ps, *As, *Cs, *Ms;
+  float *Ps, *As, *Cs, *ATs, *Ms, *MsT;
   double *Qx, *Qu, *Qux;  // cost blocks (float64: the leaf Schur complement cancels O(tau) terms)
   float *Kc, *Phiu;
   double* rn;
@@ -126,7 +127,9 @@ static int sls_init(Ctx* c) {
   S.Ps = (float*)dev_alloc(c, B * S.cvf_nslots * MS * 4);
   S.As = (float*)dev_alloc(c, B * S.cvf_nslots * MS * 4);
   S.Cs = (float*)dev_alloc(c, B * S.cvf_nslots * MS * 4);
+  S.ATs = (float*)dev_alloc(c, B * S.cvf_nslots * MS * 4);
   S.Ms = (float*)dev_alloc(c, B * S.mp_nslots * MS * 4);
+  S.MsT = (float*)dev_alloc(c, B * S.mp_nslots * MS * 4);
   S.Qx = (double*)dev_alloc(c, B * S.ncell * n * n * 8);
   S.Qu = (double*)dev_alloc(c, B * S.ncell * m * m * 8);
   S.Qux = (double*)dev_alloc(c, B * S.ncell * m * n * 8);
@@ -134,7 +137,7 @@ static int sls_init(Ctx* c) {
   S.Phiu = (float*)dev_alloc(c, B * S.ncell * m * n * 4);
   S.rn = (double*)dev_alloc(c, B * S.ncell * S.cmax * 8);
   S.err = c->dev.err;
-  if (!S.Ps || !S.As || !S.Cs || !S.Ms || !S.Qx || !S.Qu || !S.Qux || !S.Kc || !S.Phiu || !S.rn) {
+  if (!S.Ps || !S.As || !S.Cs || !S.ATs || !S.Ms || !S.MsT || !S.Qx || !S.Qu || !S.Qux || !S.Kc || !S.Phiu || !S.rn) {
     set_error(GSLS_ERR_CUDA, -1, 0, 0, 0, "SLS workspace allocation failed");
     return GSLS_ERR_CUDA;
   }
@@ -212,6 +215,7 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   const int slot = cell;  // leaves occupy slots [0, ncell)
   float* Pd = S.Ps + ((size_t)inst * S.cvf_nslots + slot) * MS;
   float* Ad = S.As + ((size_t)inst * S.cvf_nslots + slot) * MS;
+  float* ATd = S.ATs + ((size_t)inst * S.cvf_nslots + slot) * MS;
   float* Cd = S.Cs + ((size_t)inst * S.cvf_nslots + slot) * MS;
   const size_t cb = (size_t)inst * S.ncell + cell;
   const double* Qx = S.Qx + cb * n * n;
@@ -220,6 +224,7 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
       const int i = e / ldg, jj = e - i * ldg;
       Pd[e] = (jj < n) ? (float)Qx[i * n + jj] : 0.f;
       Ad[e] = 0.f;
+      ATd[e] = 0.f;
       Cd[e] = 0.f;
     }
     return;
@@ -272,6 +277,7 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
     }
     Pd[e] = (float)p;
     Ad[e] = (float)a;
+    if (jj < n) ATd[jj * ldg + i] = (float)a;
     Cd[e] = (float)cc;
   }
 }
@@ -286,12 +292,15 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   const int n = S.n, m = S.m, N = S.N, ldg = S.ldg;
   const size_t MS = (size_t)n * ldg;
   float* Mbase = S.Ms + (size_t)inst * S.mp_nslots * MS;
+  float* MTbase = S.MsT + (size_t)inst * S.mp_nslots * MS;
   if (k == N) {
     float* Ml = Mbase + (size_t)cell_of(N, j + 1, j) * MS;
+    float* MTl = MTbase + (size_t)cell_of(N, j + 1, j) * MS;
     const float* Ej = E + ((size_t)inst * N + j) * n * n;
     for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
       const int i = e / ldg, jj = e - i * ldg;
       Ml[e] = (jj < n) ? Ej[i * n + jj] : 0.f;
+      MTl[e] = (jj < n) ? Ej[jj * n + i] : 0.f;
     }
     return;
   }
@@ -346,6 +355,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   }
   __syncthreads();
   float* Ml = Mbase + (size_t)cell_of(N, k + 1, j) * MS;  // product leaf of position k
+  float* MTl = MTbase + (size_t)cell_of(N, k + 1, j) * MS;
   for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
     const int i = e / ldg, jj = e - i * ldg;
     double v = 0.0;
@@ -355,11 +365,12 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
       v = (double)Ak[i * n + jj] + s;
     }
     Ml[e] = (float)v;
+    if (jj < n) MTl[jj * ldg + i] = (float)v;
   }
 }
 
-// Matrix-product combine: M = M_later M_earlier (sls.py:217-218).
-__global__ void __launch_bounds__(512) k_matprod(float* Ms, long long inst_stride, int n, const int4* ops) {
+// Matrix-product combine: M = M_later M_earlier (sls.py:217-218), both orientations.
+__global__ void __launch_bounds__(512) k_matprod(float* Ms, float* MsT, long long inst_stride, int n, const int4* ops) {
   const int inst = blockIdx.y;
   const int4 op = ops[blockIdx.x];
   const int ldg = ldg_of(n), lds = lds_of(n);
@@ -368,10 +379,13 @@ __global__ void __launch_bounds__(512) k_matprod(float* Ms, long long inst_strid
   float* Lt = sm;
   float* Er = Lt + (size_t)n * lds;
   float* base = Ms + (size_t)inst * inst_stride;
-  cta_load_t(Lt, lds, base + (size_t)op.z * MS, ldg, n);
-  cta_load(Er, lds, base + (size_t)op.y * MS, ldg, n, n);
+  float* baseT = MsT + (size_t)inst * inst_stride;
+  cta_load_async(Lt, lds, baseT + (size_t)op.z * MS, n);
+  cta_load_async(Er, lds, base + (size_t)op.y * MS, n);
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
-  gemm_tn(n, Lt, Er, lds, EpiGlobal{base + (size_t)op.x * MS, nullptr, ldg});
+  gemm_tn(n, Lt, Er, lds, EpiGlobal{base + (size_t)op.x * MS, nullptr, ldg, n, baseT + (size_t)op.x * MS});
 }
 
 // Phi^u_{k,j} = K_{k,j} Phi^x_{k,j} (sls.py:310-318).
@@ -536,6 +550,7 @@ int sls_assemble(Ctx* c, const gsls_qp_t* qp, const double* tau, const double* t
   if (rc) return rc;
   DevSls& S = sls_of(c)->dev;
   const size_t sb = (size_t)S.cmax * sizeof(double) + 16;
+  ProfScope ps(P_SLS_ASSEMBLE, st, (double)S.ncell * c->dims.batch);
   k_sls_assemble<<<dim3(S.ncell, c->dims.batch), 256, sb, st>>>(S, *qp, tau, tau_term, Qbar, Rbar, QbarN,
                                                                   weights_per_instance ? 1 : 0);
   GSLS_CUDA_CHECK(cudaGetLastError());
@@ -573,18 +588,22 @@ int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st,
   {
     const size_t sb = (2 * m * m + 2 * m * n + 2 * n * m + wk) * sizeof(double);
     if ((rc = smem_attr((const void*)k_sls_leaf, sb))) return rc;
+    ProfScope ps(P_SLS_LEAF, st, (double)S.ncell * B);
     k_sls_leaf<<<dim3(S.ncell, B), 256, sb, st>>>(S, *qp);
     GSLS_CUDA_CHECK(cudaGetLastError());
   }
   for (int l = 0; l < s->cvf.layers; ++l) {
     const int o0 = s->cvf.layer_off[l], o1 = s->cvf.layer_off[l + 1];
-    CombineArgs a{n, S.cvf_ops + o0, o0, S.Ps, S.As, S.Cs, (long long)S.cvf_nslots * (long long)MS, nullptr, 0,
+    CombineArgs a{n, S.cvf_ops + o0, o0, S.Ps, S.As, S.Cs, S.ATs, (long long)S.cvf_nslots * (long long)MS, nullptr, 0,
                   nullptr, S.err, 1e-10f};
+    if (o1 == o0) continue;
+    ProfScope ps(P_SLS_CVF, st, (double)(o1 - o0) * B);
     if ((rc = launch_combine(a, o1 - o0, B, st))) return rc;
   }
   {
     const size_t sb = ((size_t)n * m + 3 * m * n + 2 * m * m + wk) * sizeof(double);
     if ((rc = smem_attr((const void*)k_sls_gains, sb))) return rc;
+    ProfScope ps(P_SLS_GAINS, st, (double)S.ncell * B);
     k_sls_gains<<<dim3(S.ncell, B), 256, sb, st>>>(S, *qp, E);
     GSLS_CUDA_CHECK(cudaGetLastError());
   }
@@ -594,7 +613,8 @@ int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st,
     for (int l = 0; l < s->mp.layers; ++l) {
       const int o0 = s->mp.layer_off[l], o1 = s->mp.layer_off[l + 1];
       if (o1 == o0) continue;
-      k_matprod<<<dim3(o1 - o0, B), combine_threads(n), sb, st>>>(S.Ms, (long long)S.mp_nslots * (long long)MS, n,
+      ProfScope ps(P_SLS_MATPROD, st, (double)(o1 - o0) * B);
+      k_matprod<<<dim3(o1 - o0, B), matmul_threads(n), sb, st>>>(S.Ms, S.MsT, (long long)S.mp_nslots * (long long)MS, n,
                                                                   S.mp_ops + o0);
       GSLS_CUDA_CHECK(cudaGetLastError());
     }
@@ -602,6 +622,7 @@ int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st,
   {
     const size_t sb = (size_t)n * ldg * sizeof(float);
     if ((rc = smem_attr((const void*)k_sls_phiu, sb))) return rc;
+    ProfScope ps(P_SLS_PHIU, st, (double)S.ncell * B);
     k_sls_phiu<<<dim3(S.ncell, B), 256, sb, st>>>(S);
     GSLS_CUDA_CHECK(cudaGetLastError());
   }
@@ -614,6 +635,7 @@ static int sls_rownorms(Ctx* c, const gsls_qp_t* qp, cudaStream_t st) {
   const size_t sb = ((size_t)S.n * S.ldg + S.m * S.n) * sizeof(float);
   int rc = smem_attr((const void*)k_sls_rownorm, sb);
   if (rc) return rc;
+  ProfScope ps(P_SLS_ROWNORM, st, (double)S.ncell * c->dims.batch);
   k_sls_rownorm<<<dim3(S.ncell, c->dims.batch), 256, sb, st>>>(S, *qp);
   GSLS_CUDA_CHECK(cudaGetLastError());
   return GSLS_OK;
@@ -637,6 +659,7 @@ int sls_tighten(Ctx* c, const gsls_qp_t* qp, double* h, double* hf, cudaStream_t
   }
   int rc = sls_rownorms(c, qp, st);
   if (rc) return rc;
+  ProfScope ps(P_SLS_SMALL, st, (double)c->dims.batch);
   k_sls_tighten<<<c->dims.batch, 256, 0, st>>>(s->dev, h, hf);
   GSLS_CUDA_CHECK(cudaGetLastError());
   return GSLS_OK;
@@ -649,6 +672,7 @@ int sls_duals(Ctx* c, const gsls_qp_t* qp, const double* lam, double eps, int us
   DevSls S = sls_of(c)->dev;
   S.have_response = use_response && S.have_response;
   if (S.have_response && !reuse_rownorms && (rc = sls_rownorms(c, qp, st))) return rc;
+  ProfScope ps(P_SLS_SMALL, st, (double)c->dims.batch);
   k_sls_duals<<<c->dims.batch, 256, 0, st>>>(S, lam, eps, tau, tau_term, beta, beta_term);
   GSLS_CUDA_CHECK(cudaGetLastError());
   return GSLS_OK;

@@ -54,10 +54,34 @@ __device__ inline void cta_store(float* __restrict__ dst, const float* src, int 
   }
 }
 
+// ---- async copies -------------------------------------------------------------
+
+__device__ inline void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ inline void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+template <int N>
+__device__ inline void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Issues 16-byte cp.async copies of an n x ldg(n) padded global matrix into smem
+// (ld = lds); the caller commits / waits.  Padding columns arrive as stored (zero).
+__device__ inline void cta_load_async(float* dst, int lds, const float* __restrict__ src, int n) {
+  const int q = ldg_of(n) >> 2;
+  for (int e = threadIdx.x; e < n * q; e += blockDim.x) {
+    const int i = e / q, j = (e - i * q) << 2;
+    cp_async16(dst + i * lds + j, src + (size_t)i * (q << 2) + j);
+  }
+}
+
 // ---- GEMM ---------------------------------------------------------------------
 
-// C[i][j] = sum_{k<n} At[k][i] * B[k][j] over the padded np x np output; the
-// epilogue is called once per tile row: epi(i, j0, float4) for i < n.
+// C[i][j] = sum_{k<n} At[k][i] * B[k][j] over the padded np x np output, 4x4
+// register tile per thread; the epilogue receives whole tiles: epi(i0, j0, acc)
+// and must ignore rows i >= n.
 template <class Epi>
 __device__ inline void gemm_tn(int n, const float* At, const float* B, int lds, Epi epi) {
   const int T = ldg_of(n) >> 2;
@@ -84,35 +108,52 @@ __device__ inline void gemm_tn(int n, const float* At, const float* B, int lds, 
         acc[r][3] = fmaf(av[r], b.w, acc[r][3]);
       }
     }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int i = 4 * ti + r;
-      if (i < n) epi(i, 4 * tj, make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]));
-    }
+    epi(4 * ti, 4 * tj, acc);
   }
 }
 
 // epilogues
 struct EpiSmem {  // C (smem) = acc (+ I)
   float* C;
-  int lds;
+  int lds, n;
   bool add_identity;
-  __device__ void operator()(int i, int j, float4 v) const {
-    if (add_identity && i >= j && i < j + 4) (&v.x)[i - j] += 1.f;
-    *reinterpret_cast<float4*>(C + i * lds + j) = v;
+  __device__ void operator()(int i0, int j0, float (&acc)[4][4]) const {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = i0 + r;
+      if (i >= n) break;
+      float4 v = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+      if (add_identity && i >= j0 && i < j0 + 4) (&v.x)[i - j0] += 1.f;
+      *reinterpret_cast<float4*>(C + i * lds + j0) = v;
+    }
   }
 };
 
-struct EpiGlobal {  // G (global, ld) = acc + add (global, may be null)
+struct EpiGlobal {  // G (global, ld) = acc + add (global, may be null); optional transposed copy Gt
   float* G;
   const float* add;
-  int ld;
-  __device__ void operator()(int i, int j, float4 v) const {
-    if (add) {
-      const float4 a = *reinterpret_cast<const float4*>(add + (size_t)i * ld + j);
-      v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+  int ld, n;
+  float* Gt;
+  __device__ void operator()(int i0, int j0, float (&acc)[4][4]) const {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = i0 + r;
+      if (i >= n) break;
+      float4 v = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+      if (add) {
+        const float4 a = *reinterpret_cast<const float4*>(add + (size_t)i * ld + j0);
+        v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+      }
+      *reinterpret_cast<float4*>(G + (size_t)i * ld + j0) = v;
     }
-    *reinterpret_cast<float4*>(G + (size_t)i * ld + j) = v;
+    if (Gt) {  // rows i >= n of the tile are zero (zero padding of the operands)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int j = j0 + c;
+        if (j >= n) break;
+        *reinterpret_cast<float4*>(Gt + (size_t)j * ld + i0) = make_float4(acc[0][c], acc[1][c], acc[2][c], acc[3][c]);
+      }
+    }
   }
 };
 
