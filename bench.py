@@ -232,6 +232,19 @@ def latency(tag, steps=30, warmup=5):
         if i >= warmup:
             times.append(e0.elapsed_time(e1))
     its = int(eng.stats.iterations[0])
+    # per-kernel-family breakdown of the same step (separate, profiled pass)
+    from paper_2604_07644_b200 import _native as nat
+    lib = nat.load()
+    lib.gsls_prof_enable(1)
+    lib.gsls_prof_read(None, None, None, 0)
+    for _ in range(5):
+        eng.step(xb, px, pu, tau=tc, tau_term=tt)
+    torch.cuda.synchronize()
+    lib.gsls_prof_enable(0)
+    nfam = len(nat.PROF_FAMILIES)
+    pm, pl = np.zeros(nfam), np.zeros(nfam, np.int64)
+    lib.gsls_prof_read(pm.ctypes.data, None, pl.ctypes.data, nfam)
+    phases = {k: round(float(v) / 5, 4) for k, v, c in zip(nat.PROF_FAMILIES, pm, pl) if c}
     # end to end through the public drop-in API (numpy in, numpy out)
     tau = sls.SlsDuals.zero(wl.N, m.nc, m.nf, rs.eps)
     tau.tau, tau.tau_term = wl.tau, wl.tau_term
@@ -245,7 +258,7 @@ def latency(tag, steps=30, warmup=5):
             e2e.append(1e3 * (time.perf_counter() - t))
     del eng
     return {"p50": statistics.median(times), "p90": float(np.percentile(times, 90)), "admm_iterations": its,
-            "e2e_p50": statistics.median(e2e)}
+            "e2e_p50": statistics.median(e2e), "phases_ms": phases}
 
 
 def run_ours(args):
@@ -402,6 +415,7 @@ def run_ours(args):
            "latency_ms_p90": {k: v["p90"] for k, v in lat.items()},
            "latency_e2e_ms_p50": {k: v["e2e_p50"] for k, v in lat.items()},
            "latency_admm_iterations": {k: v["admm_iterations"] for k, v in lat.items()},
+           "latency_phases_ms": {k: v["phases_ms"] for k, v in lat.items()},
            "admm_iterations_mean": total_iters / its_all.numel(),
            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
            "gpu_launches": launches, "roofline": roof, "roofline_by_kernel": rl, "phases": phases,

@@ -76,22 +76,43 @@ size_t replay_smem_floats(const Ctx* c) {
   return (size_t)vec_layout(c->dims.nx, c->dims.nu, c->dims.N, c->mtot, c->cvf.nslots, c->cot.nslots, ml).total;
 }
 
-// y[row] = add[row] + sgn * sum_k Mcm[k*ldg + row] x[k] for one 8-row block
-// (fp32 recorded matrix, fp64 vectors and accumulation).
+// y[row] = add[row] + sgn * sum_k Mcm[k*ldg + row] x[k] for one 32-row block
+// (fp32 recorded matrix, fp64 vectors and accumulation).  Lane (rq, g): rows
+// 32rb + 4rq .. +3 as one 16-byte load, k = g, g+4, ...; 8 lanes of equal g
+// read one full 128-byte line per k.  Padding rows (< ldg) are zero.
 __device__ inline void warp_cm_matvec(const float* __restrict__ Mcm, int ldg, int n, int rb, const double* x,
                                       const double* add, double sgn, double* y) {
   const int lane = threadIdx.x & 31;
-  const int rs = lane & 7, g = lane >> 3;
-  const int row = rb * 8 + rs;
-  double acc = 0.0;
-  if (row < n) {
-    const float* p = Mcm + row;
-#pragma unroll 4
-    for (int k = g; k < n; k += 4) acc = fma((double)__ldg(p + (size_t)k * ldg), x[k], acc);
+  const int rq = lane & 7, g = lane >> 3;
+  const int row0 = rb * 32 + 4 * rq;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (row0 < ldg) {
+    const float* p = Mcm + row0;
+#pragma unroll 8
+    for (int k = g; k < n; k += 4) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(p + (size_t)k * ldg));
+      const double xk = x[k];
+      a0 = fma((double)v.x, xk, a0);
+      a1 = fma((double)v.y, xk, a1);
+      a2 = fma((double)v.z, xk, a2);
+      a3 = fma((double)v.w, xk, a3);
+    }
   }
-  acc += __shfl_xor_sync(0xffffffffu, acc, 8);
-  acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-  if (g == 0 && row < n) y[row] = add[row] + sgn * acc;
+#pragma unroll
+  for (int o = 8; o <= 16; o <<= 1) {
+    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+  }
+  if (g == 0) {
+    const double av[4] = {a0, a1, a2, a3};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int row = row0 + r;
+      if (row < n) y[row] = add[row] + sgn * av[r];
+    }
+  }
 }
 
 __device__ inline double block_max_d(double v, double* red) {
@@ -164,7 +185,7 @@ __global__ void __launch_bounds__(512, 1) k_replay(ReplayArgs a) {
     for (int e = tid; e < mtot; e += nthr) { z[e] = zg[e]; lam[e] = lg[e]; y[e] = yg[e]; }
     __syncthreads();
   }
-  const int RB = (n + 7) >> 3;
+  const int RB = (n + 31) >> 5;  // 32-row blocks per matvec
 
   for (;;) {
     // ---- linear terms q + rho C'(y - z), r + rho D'(y - z) and CVF leaves --------

@@ -150,7 +150,8 @@ static int sls_init(Ctx* c) {
 
 // [C D]' diag(tau) [C D] + blkdiag(Qbar, Rbar) per cell; terminal cells (k = N)
 // get CN' diag(tau_N) CN + QbarN.  Weights are per instance (stride wst, 0 = shared).
-// float64 throughout; Qx is stored unpadded n x n.
+// float64 throughout; Qx is stored unpadded n x n.  Rows with tau = 0 (inactive
+// constraints) contribute nothing and are skipped.
 __global__ void __launch_bounds__(256) k_sls_assemble(DevSls S, gsls_qp_t qp, const double* tau,
                                                       const double* tau_term, const float* Qbar, const float* Rbar,
                                                       const float* QbarN, long long wst) {
@@ -160,52 +161,78 @@ __global__ void __launch_bounds__(256) k_sls_assemble(DevSls S, gsls_qp_t qp, co
   const int n = S.n, m = S.m, c = S.c, nf = S.nf, N = S.N;
   const size_t cb = (size_t)inst * S.ncell + cell;
   double* Qx = S.Qx + cb * n * n;
+  const bool term = (k == N);
+  const int rows = term ? nf : c;
   extern __shared__ double smd[];
-  double* t = smd;  // c or nf
-  if (k == N) {
-    const float* CN = qp.CN + (size_t)inst * nf * n;
-    const float* QbN = QbarN + (size_t)inst * wst * n * n;
-    for (int f = threadIdx.x; f < nf; f += blockDim.x) t[f] = tau_term ? tau_term[((size_t)inst * N + j) * nf + f] : 0.0;
-    __syncthreads();
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-      const int i = e / n, jj = e - i * n;
-      double s = 0.0;
-      for (int f = 0; f < nf; ++f) s = fma((double)CN[f * n + i] * t[f], (double)CN[f * n + jj], s);
-      Qx[e] = s + (double)QbN[e];
-    }
-    return;
+  double* Cw = smd;                 // active rows: tau_r * C_r      (rows x n)
+  double* Cr = Cw + rows * n;       // active rows: C_r              (rows x n)
+  double* Dw = Cr + rows * n;       // tau_r * D_r                   (rows x m)
+  double* Dr = Dw + rows * m;       // D_r
+  int* act = reinterpret_cast<int*>(Dr + rows * m);
+  __shared__ int s_nact;
+  const float* Cg = term ? qp.CN + (size_t)inst * nf * n : qp.C + ((size_t)inst * N + k) * c * n;
+  const float* Dg = term ? nullptr : qp.D + ((size_t)inst * N + k) * c * m;
+  const double* tg = term ? (tau_term ? tau_term + ((size_t)inst * N + j) * nf : nullptr)
+                          : (tau ? tau + cb * c : nullptr);
+  if (threadIdx.x == 0) {
+    int na = 0;
+    if (tg)
+      for (int r = 0; r < rows; ++r)
+        if (tg[r] != 0.0) act[na++] = r;
+    s_nact = na;
   }
-  const size_t st = (size_t)inst * N + k;
-  const float* Ck = qp.C + st * c * n;
-  const float* Dk = qp.D + st * c * m;
-  for (int r = threadIdx.x; r < c; r += blockDim.x) t[r] = tau ? tau[cb * c + r] : 0.0;
   __syncthreads();
-  const float* Qb = Qbar + (size_t)inst * wst * n * n;
-  const float* Rb = Rbar + (size_t)inst * wst * m * m;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e / n, jj = e - i * n;
-    double s = 0.0;
-    for (int r = 0; r < c; ++r) s = fma((double)Ck[r * n + i] * t[r], (double)Ck[r * n + jj], s);
-    Qx[e] = s + (double)Qb[e];
+  const int na = s_nact;
+  for (int e = threadIdx.x; e < na * n; e += blockDim.x) {
+    const int a = e / n, i = e - a * n, r = act[a];
+    const double v = Cg[r * n + i];
+    Cr[e] = v;
+    Cw[e] = tg[r] * v;
   }
+  if (!term)
+    for (int e = threadIdx.x; e < na * m; e += blockDim.x) {
+      const int a = e / m, i = e - a * m, r = act[a];
+      const double v = Dg[r * m + i];
+      Dr[e] = v;
+      Dw[e] = tg[r] * v;
+    }
+  __syncthreads();
+  const float* Qb = term ? QbarN + (size_t)inst * wst * n * n : Qbar + (size_t)inst * wst * n * n;
+  const int q4 = (n + 3) >> 2;
+  for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
+    const int i = e / q4, j0 = (e - i * q4) << 2;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int a = 0; a < na; ++a) {
+      const double w = Cw[a * n + i];
+      const double* cr = Cr + a * n + j0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (j0 + t < n) acc[t] = fma(w, cr[t], acc[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (j0 + t < n) Qx[i * n + j0 + t] = acc[t] + (double)Qb[i * n + j0 + t];
+  }
+  if (term) return;
+  const float* Rb = Rbar + (size_t)inst * wst * m * m;
   double* Qu = S.Qu + cb * m * m;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    const int a = e / m, b = e - a * m;
+    const int a = e / m, b2 = e - a * m;
     double s = 0.0;
-    for (int r = 0; r < c; ++r) s = fma((double)Dk[r * m + a] * t[r], (double)Dk[r * m + b], s);
+    for (int r = 0; r < na; ++r) s = fma(Dw[r * m + a], Dr[r * m + b2], s);
     Qu[e] = s + (double)Rb[e];
   }
   double* Qux = S.Qux + cb * m * n;
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     const int a = e / n, i = e - a * n;
     double s = 0.0;
-    for (int r = 0; r < c; ++r) s = fma((double)Dk[r * m + a] * t[r], (double)Ck[r * n + i], s);
+    for (int r = 0; r < na; ++r) s = fma(Dw[r * m + a], Cr[r * n + i], s);
     Qux[e] = s;
   }
 }
 
 // Grid leaves (float64 algebra, float32 result): Qu^-1, P = Qx - Qux' Qu^-1 Qux,
-// A = A_k - B_k Qu^-1 Qux, C = B_k Qu^-1 B_k'.
+// A = A_k - B_k Qu^-1 Qux, C = B_k Qu^-1 B_k'.  1x4 output tiles.
 __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   const int cell = blockIdx.x, inst = blockIdx.y;
   const int2 kj = S.cell_kj[cell];
@@ -230,61 +257,78 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
     return;
   }
   extern __shared__ double smd[];
-  double* Qu = smd;            // m x m
-  double* Qi = Qu + m * m;     // m x m
-  double* Qux = Qi + m * m;    // m x n
-  double* QQ = Qux + m * n;    // m x n
-  double* Bk = QQ + m * n;     // n x m
-  double* BQ = Bk + n * m;     // n x m
-  double* wk = BQ + n * m;
+  const int np = ldg;                // row length of the n-vectors below (padded, zero tail)
+  double* Qu = smd;                  // m x m
+  double* Qi = Qu + m * m;           // m x m
+  double* Qux = Qi + m * m;          // m x np
+  double* QQ = Qux + m * np;         // m x np   Qu^-1 Qux
+  double* BT = QQ + m * np;          // m x np   B_k^T
+  double* BQT = BT + m * np;         // m x np   (B_k Qu^-1)^T
+  double* wk = BQT + m * np;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) Qu[e] = S.Qu[cb * m * m + e];
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) Qux[e] = S.Qux[cb * m * n + e];
   const size_t st = (size_t)inst * N + k;
-  for (int e = threadIdx.x; e < n * m; e += blockDim.x) Bk[e] = qp.B[st * n * m + e];
+  const float* Bg = qp.B + st * n * m;
+  for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
+    const int l = e / np, i = e - l * np;
+    Qux[e] = (i < n) ? S.Qux[cb * m * n + l * n + i] : 0.0;
+    BT[e] = (i < n) ? (double)Bg[i * m + l] : 0.0;
+  }
   __syncthreads();
   if (threadIdx.x < 32) {
     if (warp_spd_inverse(Qu, m, Qi, m, wk) && threadIdx.x == 0)
       raise_err(S.err + inst, GSLS_ERR_SINGULAR_STAGE, k, j, GSLS_LABEL_QU);
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
-    const int a = e / n, i = e - a * n;
-    double s = 0.0;
-    for (int b = 0; b < m; ++b) s = fma(Qi[a * m + b], Qux[b * n + i], s);
-    QQ[e] = s;
-  }
-  for (int e = threadIdx.x; e < n * m; e += blockDim.x) {
-    const int i = e / m, a = e - i * m;
-    double s = 0.0;
-    for (int b = 0; b < m; ++b) s = fma(Bk[i * m + b], Qi[b * m + a], s);
-    BQ[e] = s;
+  for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
+    const int a = e / np, i = e - a * np;
+    double s1 = 0.0, s2 = 0.0;
+    for (int b2 = 0; b2 < m; ++b2) {
+      const double qi = Qi[b2 * m + a];  // Qi symmetric in exact arithmetic; use Qi^T consistently
+      s1 = fma(qi, Qux[b2 * np + i], s1);
+      s2 = fma(qi, BT[b2 * np + i], s2);
+    }
+    QQ[e] = s1;
+    BQT[e] = s2;
   }
   __syncthreads();
   const float* Ak = qp.A + st * n * n;
-  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
-    const int i = e / ldg, jj = e - i * ldg;
-    double p = 0.0, a = 0.0, cc = 0.0;
-    if (jj < n) {
-      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      for (int l = 0; l < m; ++l) {
-        s1 = fma(Qux[l * n + i], QQ[l * n + jj], s1);
-        s2 = fma(Bk[i * m + l], QQ[l * n + jj], s2);
-        s3 = fma(BQ[i * m + l], Bk[jj * m + l], s3);
+  const int q4 = np >> 2;
+  for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
+    const int i = e / q4, j0 = (e - i * q4) << 2;
+    double p4[4] = {0.0, 0.0, 0.0, 0.0}, a4[4] = {0.0, 0.0, 0.0, 0.0}, c4[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int l = 0; l < m; ++l) {
+      const double qx = Qux[l * np + i], bt = BT[l * np + i], bq = BQT[l * np + i];
+      const double2 q01 = *reinterpret_cast<const double2*>(QQ + l * np + j0);
+      const double2 q23 = *reinterpret_cast<const double2*>(QQ + l * np + j0 + 2);
+      const double2 b01 = *reinterpret_cast<const double2*>(BT + l * np + j0);
+      const double2 b23 = *reinterpret_cast<const double2*>(BT + l * np + j0 + 2);
+      const double qq[4] = {q01.x, q01.y, q23.x, q23.y}, bb[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        p4[t] = fma(qx, qq[t], p4[t]);
+        a4[t] = fma(bt, qq[t], a4[t]);
+        c4[t] = fma(bq, bb[t], c4[t]);
       }
-      p = Qx[i * n + jj] - s1;
-      a = (double)Ak[i * n + jj] - s2;
-      cc = s3;
     }
-    Pd[e] = (float)p;
-    Ad[e] = (float)a;
-    if (jj < n) ATd[jj * ldg + i] = (float)a;
-    Cd[e] = (float)cc;
+    float po[4], ao[4], co[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int jj = j0 + t;
+      const bool in = jj < n;
+      po[t] = in ? (float)(Qx[i * n + jj] - p4[t]) : 0.f;
+      ao[t] = in ? (float)((double)Ak[i * n + jj] - a4[t]) : 0.f;
+      co[t] = in ? (float)c4[t] : 0.f;
+      if (in) ATd[(size_t)jj * ldg + i] = ao[t];
+    }
+    *reinterpret_cast<float4*>(Pd + (size_t)i * ldg + j0) = make_float4(po[0], po[1], po[2], po[3]);
+    *reinterpret_cast<float4*>(Ad + (size_t)i * ldg + j0) = make_float4(ao[0], ao[1], ao[2], ao[3]);
+    *reinterpret_cast<float4*>(Cd + (size_t)i * ldg + j0) = make_float4(co[0], co[1], co[2], co[3]);
   }
 }
 
 // Gains on cell (k, j), k <= N-1, from P+ = P(k+1, j); closed loop -> product
-// leaf of position k (float64 algebra).  Cell (N, j) writes E_j into the leaf
-// of position j.
+// leaf of position k (float64 algebra, 1x4 tiles).  Cell (N, j) writes E_j into
+// the leaf of position j.
 __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const float* E) {
   const int cell = blockIdx.x, inst = blockIdx.y;
   const int2 kj = S.cell_kj[cell];
@@ -305,39 +349,73 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
     return;
   }
   extern __shared__ double smd[];
-  double* Bst = smd;             // n x m
-  double* BtP = Bst + n * m;     // m x n
-  double* H = BtP + m * n;       // m x m
-  double* Gm = H + m * m;        // m x n
-  double* Ga = Gm + m * n;       // m x m
-  double* Ks = Ga + m * m;       // m x n
-  double* wk = Ks + m * n;
-  const float* Pn = S.Ps + ((size_t)inst * S.cvf_nslots + S.cvf_out[cell_of(N, k + 1, j)]) * MS;
+  const int np = ldg, lds = lds_of(n);
+  double* BT = smd;              // m x np   B_k^T
+  double* BtP = BT + m * np;     // m x np   B' P+
+  double* Gm = BtP + m * np;     // m x np
+  double* Ks = Gm + m * np;      // m x np
+  double* H = Ks + m * np;       // m x m
+  double* Ga = H + m * m;        // m x m
+  double* wk = Ga + m * m;
+  float* Pn = reinterpret_cast<float*>(wk + 2 * kMaxM * (kMaxM + 1) + 8);  // n x lds
+  float* Ak = Pn + n * lds;                                                // n x lds
+  const float* Pg = S.Ps + ((size_t)inst * S.cvf_nslots + S.cvf_out[cell_of(N, k + 1, j)]) * MS;
+  cta_load_async(Pn, lds, Pg, n);
+  cp_async_commit();
   const size_t st = (size_t)inst * N + k;
-  for (int e = threadIdx.x; e < n * m; e += blockDim.x) Bst[e] = qp.B[st * n * m + e];
+  const float* Bg = qp.B + st * n * m;
+  const float* Ag = qp.A + st * n * n;
+  for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
+    const int l = e / np, i = e - l * np;
+    BT[e] = (i < n) ? (double)Bg[i * m + l] : 0.0;
+  }
+  for (int e = threadIdx.x; e < n * np; e += blockDim.x) {
+    const int i = e / np, jj = e - i * np;
+    Ak[i * lds + jj] = (jj < n) ? Ag[i * n + jj] : 0.f;
+  }
+  cp_async_wait<0>();
   __syncthreads();
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
-    const int l = e / n, jj = e - l * n;
-    double s = 0.0;
-    for (int i = 0; i < n; ++i) s = fma(Bst[i * m + l], (double)Pn[i * ldg + jj], s);
-    BtP[e] = s;
+  const int q4 = np >> 2;
+  for (int e = threadIdx.x; e < m * q4; e += blockDim.x) {  // B' P+ (1x4 tiles)
+    const int l = e / q4, j0 = (e - l * q4) << 2;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = 0; i < n; ++i) {
+      const double b = BT[l * np + i];
+      const float4 pv = *reinterpret_cast<const float4*>(Pn + i * lds + j0);
+      acc[0] = fma(b, (double)pv.x, acc[0]);
+      acc[1] = fma(b, (double)pv.y, acc[1]);
+      acc[2] = fma(b, (double)pv.z, acc[2]);
+      acc[3] = fma(b, (double)pv.w, acc[3]);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) BtP[l * np + j0 + t] = acc[t];
   }
   __syncthreads();
-  const float* Ak = qp.A + st * n * n;
   const size_t cb = (size_t)inst * S.ncell + cell;
   const double* Qu = S.Qu + cb * m * m;
   const double* Qux = S.Qux + cb * m * n;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
     const int l = e / m, t = e - l * m;
     double s = 0.0;
-    for (int i = 0; i < n; ++i) s = fma(BtP[l * n + i], Bst[i * m + t], s);
+    for (int i = 0; i < n; ++i) s = fma(BtP[l * np + i], BT[t * np + i], s);
     H[e] = Qu[e] + s;
   }
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
-    const int l = e / n, jj = e - l * n;
-    double s = 0.0;
-    for (int i = 0; i < n; ++i) s = fma(BtP[l * n + i], (double)Ak[i * n + jj], s);
-    Gm[e] = Qux[e] + s;
+  for (int e = threadIdx.x; e < m * q4; e += blockDim.x) {  // Qux + B' P+ A (1x4 tiles)
+    const int l = e / q4, j0 = (e - l * q4) << 2;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = 0; i < n; ++i) {
+      const double b = BtP[l * np + i];
+      const float4 av = *reinterpret_cast<const float4*>(Ak + i * lds + j0);
+      acc[0] = fma(b, (double)av.x, acc[0]);
+      acc[1] = fma(b, (double)av.y, acc[1]);
+      acc[2] = fma(b, (double)av.z, acc[2]);
+      acc[3] = fma(b, (double)av.w, acc[3]);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int jj = j0 + t;
+      Gm[l * np + jj] = (jj < n) ? Qux[l * n + jj] + acc[t] : 0.0;
+    }
   }
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -346,26 +424,38 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   }
   __syncthreads();
   float* Kg = S.Kc + cb * m * n;
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
-    const int l = e / n, jj = e - l * n;
+  for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
+    const int l = e / np, jj = e - l * np;
     double s = 0.0;
-    for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Gm[t * n + jj], s);
+    for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Gm[t * np + jj], s);
     Ks[e] = -s;
-    Kg[e] = (float)(-s);
+    if (jj < n) Kg[l * n + jj] = (float)(-s);
   }
   __syncthreads();
   float* Ml = Mbase + (size_t)cell_of(N, k + 1, j) * MS;  // product leaf of position k
   float* MTl = MTbase + (size_t)cell_of(N, k + 1, j) * MS;
-  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
-    const int i = e / ldg, jj = e - i * ldg;
-    double v = 0.0;
-    if (jj < n) {
-      double s = 0.0;
-      for (int l = 0; l < m; ++l) s = fma(Bst[i * m + l], Ks[l * n + jj], s);
-      v = (double)Ak[i * n + jj] + s;
+  for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {  // A + B K (1x4 tiles)
+    const int i = e / q4, j0 = (e - i * q4) << 2;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int l = 0; l < m; ++l) {
+      const double b = BT[l * np + i];
+      const double2 k01 = *reinterpret_cast<const double2*>(Ks + l * np + j0);
+      const double2 k23 = *reinterpret_cast<const double2*>(Ks + l * np + j0 + 2);
+      acc[0] = fma(b, k01.x, acc[0]);
+      acc[1] = fma(b, k01.y, acc[1]);
+      acc[2] = fma(b, k23.x, acc[2]);
+      acc[3] = fma(b, k23.y, acc[3]);
     }
-    Ml[e] = (float)v;
-    if (jj < n) MTl[jj * ldg + i] = (float)v;
+    const float4 av = *reinterpret_cast<const float4*>(Ak + i * lds + j0);
+    const float a4[4] = {av.x, av.y, av.z, av.w};
+    float o[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int jj = j0 + t;
+      o[t] = (jj < n) ? (float)((double)a4[t] + acc[t]) : 0.f;
+      if (jj < n) MTl[(size_t)jj * ldg + i] = o[t];
+    }
+    *reinterpret_cast<float4*>(Ml + (size_t)i * ldg + j0) = make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -549,7 +639,10 @@ int sls_assemble(Ctx* c, const gsls_qp_t* qp, const double* tau, const double* t
   int rc = sls_init(c);
   if (rc) return rc;
   DevSls& S = sls_of(c)->dev;
-  const size_t sb = (size_t)S.cmax * sizeof(double) + 16;
+  const size_t rows = (size_t)S.cmax;
+  const size_t sb = (rows * (2 * S.n + 2 * S.m)) * sizeof(double) + rows * sizeof(int) + 16;
+  int rc2 = smem_attr((const void*)k_sls_assemble, sb);
+  if (rc2) return rc2;
   ProfScope ps(P_SLS_ASSEMBLE, st, (double)S.ncell * c->dims.batch);
   k_sls_assemble<<<dim3(S.ncell, c->dims.batch), 256, sb, st>>>(S, *qp, tau, tau_term, Qbar, Rbar, QbarN,
                                                                   weights_per_instance ? 1 : 0);
@@ -586,7 +679,7 @@ int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st,
   const size_t MS = mat_elems(n);
   const size_t wk = 2 * kMaxM * (kMaxM + 1) + 8;
   {
-    const size_t sb = (2 * m * m + 2 * m * n + 2 * n * m + wk) * sizeof(double);
+    const size_t sb = (2 * m * m + 4 * (size_t)m * ldg + wk) * sizeof(double);
     if ((rc = smem_attr((const void*)k_sls_leaf, sb))) return rc;
     ProfScope ps(P_SLS_LEAF, st, (double)S.ncell * B);
     k_sls_leaf<<<dim3(S.ncell, B), 256, sb, st>>>(S, *qp);
@@ -601,7 +694,7 @@ int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st,
     if ((rc = launch_combine(a, o1 - o0, B, st))) return rc;
   }
   {
-    const size_t sb = ((size_t)n * m + 3 * m * n + 2 * m * m + wk) * sizeof(double);
+    const size_t sb = (4 * (size_t)m * ldg + 2 * m * m + wk) * sizeof(double) + 2 * (size_t)n * lds_of(n) * sizeof(float);
     if ((rc = smem_attr((const void*)k_sls_gains, sb))) return rc;
     ProfScope ps(P_SLS_GAINS, st, (double)S.ncell * B);
     k_sls_gains<<<dim3(S.ncell, B), 256, sb, st>>>(S, *qp, E);
