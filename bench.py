@@ -6,7 +6,8 @@
 Our arm (default): BASELINE cfg-D — one robust RTI step (sls.rti_robust_step:
 linearize, SLS synthesis + tube tightening, tightened ADMM QP, duals) per
 scenario for a batch of 1024 perturbed 61D-quadruped scenarios per GPU
-(weak scaling; ranks gather u0 with NCCL after every step).  ``value`` is
+(weak scaling; ranks all-gather one result record per instance with NCCL
+after every step).  ``value`` is
 whole-job solves/s timed with CUDA events; ``e2e`` is the same through the
 public API with inputs copied from pinned host memory and u0/plan read
 back every step.  Single-instance step latency p50/p90 at 61D and 75D is
@@ -204,7 +205,7 @@ def workload_config(batch, world):
     return {"workload": "cfg-D: 61D/12u synthetic quadruped, one robust RTI step (linearize + SLS synthesis/"
                         "tightening + tightened ADMM QP + duals) per scenario, N=25, nc=26, nf=2",
             "batch_per_gpu": batch, "N": 25, "nx": 61, "nu": 12, "parallelism": f"dp{world} (independent scenarios; "
-            "NCCL all_gather of u0 per step)", "l2": "inputs larger than L2 (per-step SLS/LQR workspace >> 126 MB)",
+            "one NCCL all_gather of a per-instance result record (u0, ADMM stats, cost) per step)", "l2": "inputs larger than L2 (per-step SLS/LQR workspace >> 126 MB)",
             "timing": "CUDA events on the launching stream, max over ranks"}
 
 
@@ -287,18 +288,20 @@ def run_ours(args):
     rs = scenarios.our_settings()(m)
     eng = RtiEngine(m, N, B, rs)
     d = lambda a: torch.as_tensor(np.asarray(a), dtype=torch.float64, device="cuda").contiguous()  # noqa: E731
-    xs = wl.scenario_states(rank * B, B)
+    xs = wl.scenario_states(rank * B, B)   # weak scaling: rank r owns scenarios [rB, (r+1)B)
     host = {"xbar0": xs, "prev_x": np.broadcast_to(wl.prev_x, (B,) + wl.prev_x.shape).copy(),
             "prev_u": np.broadcast_to(wl.prev_u, (B,) + wl.prev_u.shape).copy(),
             "tau": np.broadcast_to(ragged_to_cells(wl.tau, N, (c,)), (B, N * (N + 1) // 2, c)).copy(),
             "tau_term": np.broadcast_to(wl.tau_term, (B, N, nf)).copy()}
     dev = {k: d(v) for k, v in host.items()}
-    gathered = torch.empty(world * B, mu, dtype=torch.float64, device="cuda")
+    from paper_2604_07644_b200 import dist as D
+    rec = torch.empty(B, mu + len(D.RESULT_FIELDS), dtype=torch.float64, device="cuda")
+    gathered = torch.empty(world * B, rec.shape[1], dtype=torch.float64, device="cuda")
 
     def step(inp):
         eng.step(inp["xbar0"], inp["prev_x"], inp["prev_u"], tau=inp["tau"], tau_term=inp["tau_term"])
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, eng.u0)
+        if world > 1:   # the only collective: one record per instance (u0 + ADMM stats + cost)
+            D.gather_results(D.pack_engine(eng, rec), world, out=gathered)
 
     def barrier():
         if world > 1:

@@ -1,0 +1,88 @@
+"""Batches of independent MPC instances partitioned across GPUs.
+
+A single solve stays on one GPU (north star); a batch of scenarios is split
+into contiguous per-rank blocks with no communication inside the step.  After
+each batched step the ranks exchange one compact result record per instance
+(``RESULT_FIELDS``) with a single ``all_gather_into_tensor`` — NCCL over
+NVLink on the GPU box, gloo in the CPU tests.  The reference has no
+multi-process path at all (scan.py:97-128 is thread-level only); this module
+is the build's addition on top of the drop-in entry points.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+# one float64 row per instance: u0 (nu) followed by these scalars
+RESULT_FIELDS = ("admm_iterations", "converged", "rho_changes", "cost")
+
+
+def env():
+    """(rank, local_rank, world) from the torchrun environment (1 process = 1 GPU)."""
+    import os
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def shard(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous block (first, count) of ``total`` instances owned by ``rank``;
+    the first ``total % world`` ranks take one extra instance."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} / world {world}")
+    if total < 0:
+        raise ValueError("total must be >= 0")
+    base, extra = divmod(total, world)
+    first = rank * base + min(rank, extra)
+    return first, base + (1 if rank < extra else 0)
+
+
+def pack_results(u0: torch.Tensor, iterations: torch.Tensor, converged: torch.Tensor, rho_changes: torch.Tensor,
+                 cost: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """(B, nu + 4) float64 record of one batched step, on the engine's device."""
+    B, nu = u0.shape
+    if out is None:
+        out = torch.empty(B, nu + len(RESULT_FIELDS), dtype=torch.float64, device=u0.device)
+    out[:, :nu] = u0
+    out[:, nu] = iterations
+    out[:, nu + 1] = converged
+    out[:, nu + 2] = rho_changes
+    out[:, nu + 3] = cost
+    return out
+
+
+def pack_engine(engine, out: torch.Tensor | None = None) -> torch.Tensor:
+    s = engine.stats
+    return pack_results(engine.u0, s.iterations, s.converged, s.rho_changes, engine.cost, out)
+
+
+def gather_results(local: torch.Tensor, world: int, out: torch.Tensor | None = None,
+                   counts: list[int] | None = None) -> torch.Tensor:
+    """All ranks receive every rank's records in global instance order.
+
+    Equal blocks go through one ``all_gather_into_tensor``; ragged blocks
+    (``counts`` from ``shard``) are padded to the largest block and trimmed."""
+    if world == 1:
+        return local if out is None else out.copy_(local)
+    rows, width = local.shape
+    if counts is None or len(set(counts)) == 1:
+        if out is None:
+            out = torch.empty(world * rows, width, dtype=local.dtype, device=local.device)
+        dist.all_gather_into_tensor(out, local.contiguous())
+        return out
+    mx = max(counts)
+    pad = torch.zeros(mx, width, dtype=local.dtype, device=local.device)
+    pad[:rows] = local
+    buf = torch.empty(world * mx, width, dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(buf, pad)
+    parts = [buf[r * mx:r * mx + c] for r, c in enumerate(counts)]
+    full = torch.cat(parts, 0)
+    return full if out is None else out.copy_(full)
+
+
+def max_over_ranks(ms: float, world: int, device=None) -> float:
+    """Timing convention: the slowest rank's device time."""
+    if world == 1:
+        return float(ms)
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t)
