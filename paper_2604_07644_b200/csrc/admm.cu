@@ -15,6 +15,8 @@
 //   ADMM step        constraint_values / project_and_ascend / residuals /
 //                    update_rho (admm.py:91-97, :130-150, :184-199)
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -43,14 +45,19 @@ struct ReplayArgs {
   double* gscratch;
   long long scratch_floats;
   int max_layer;  // max ops in any scan layer (t1/t2 sizing)
+  unsigned long long* trace;  // GSLS_REPLAY_TRACE: phase timestamps of the first iteration (rank 0)
 };
+
+constexpr int kReplayThreads = 512;
+constexpr int kMaxCluster = 16;
 
 // Replay vectors (all float64).
 struct VecLayout {
-  int pv, bv, cb, t1, t2, z, lam, y, rhat, om, kf, du, red, total;
+  int pv, bv, cb, t1, t2, z, lam, y, w, rhat, om, kf, du, red, part, redall, masks, plan, total;
 };
 
-__host__ __device__ inline VecLayout vec_layout(int n, int m, int N, int mtot, int s_cvf, int s_cot, int max_layer) {
+__host__ __device__ inline VecLayout vec_layout(int n, int m, int N, int mtot, int s_cvf, int s_cot, int max_layer,
+                                                int nops_cvf, int nops_cot, int lay_cvf, int lay_cot) {
   VecLayout v;
   int o = 0;
   auto take = [&](int sz) { int r = o; o += (sz + 1) & ~1; return r; };
@@ -62,18 +69,24 @@ __host__ __device__ inline VecLayout vec_layout(int n, int m, int N, int mtot, i
   v.z = take(mtot);
   v.lam = take(mtot);
   v.y = take(mtot);
+  v.w = take(mtot);  // y - z
   v.rhat = take(N * m);
   v.om = take(N * m);  // also the feedforward inner vector
   v.kf = take(N * m);
   v.du = take(N * m);
   v.red = take(64);
+  v.part = take(kReplayThreads);     // split-K partial sums (kReplayThreads / 32 warps x 32 rows)
+  v.redall = take(2 * kMaxCluster);  // per-rank partial maxima of the residuals
+  v.masks = take((s_cvf + s_cot + 1) / 2 + 1);  // consumer-rank masks per slot (uint32)
+  v.plan = take(2 * (nops_cvf + nops_cot) + (lay_cvf + lay_cot + 2 + 2 * N + 2) / 2 + 2);  // scan plan copy
   v.total = o;
   return v;
 }
 
 size_t replay_smem_floats(const Ctx* c) {
   const int ml = std::max(1, std::max(c->cvf_max_layer, c->cot_max_layer));
-  return (size_t)vec_layout(c->dims.nx, c->dims.nu, c->dims.N, c->mtot, c->cvf.nslots, c->cot.nslots, ml).total;
+  return (size_t)vec_layout(c->dims.nx, c->dims.nu, c->dims.N, c->mtot, c->cvf.nslots, c->cot.nslots, ml,
+                           (int)c->cvf.ops.size(), (int)c->cot.ops.size(), c->cvf.layers, c->cot.layers).total;
 }
 
 // y[row] = add[row] + sgn * sum_k Mcm[k*ldg + row] x[k] for one 32-row block
@@ -138,23 +151,260 @@ __device__ inline void write_last(const DevLqr& L, int inst, const double* kf, c
   }
 }
 
-__global__ void __launch_bounds__(512, 1) k_replay(ReplayArgs a) {
+// ---- thread-block-cluster plumbing ---------------------------------------------
+// A replay instance runs on a cluster of CS CTAs (CS = 1 for large batches).
+// Every CTA holds a full replica of the replay vectors in its shared memory;
+// each phase's outputs are written to all replicas (DSMEM stores) and phases
+// are separated by cluster barriers, so every read is CTA-local.
+
+__device__ inline unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ inline unsigned cluster_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ inline void st_remote(const double* local, unsigned rank, double v) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(local);
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+}
+
+struct Cl {
+  unsigned rank, cs;
+  __device__ void put(double* p, double v) const {  // write v to p in every replica
+    *p = v;
+    for (unsigned r = 0; r < cs; ++r)
+      if (r != rank) st_remote(p, r, v);
+  }
+  __device__ void put_mask(double* p, double v, unsigned mask) const {  // local + consumer replicas
+    *p = v;
+    mask &= ~(1u << rank);
+    while (mask) {
+      const unsigned r = __ffs(mask) - 1;
+      mask &= mask - 1;
+      st_remote(p, r, v);
+    }
+  }
+  __device__ void sync() const {
+    if (cs == 1) {
+      __syncthreads();
+    } else {
+      asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+  }
+};
+
+// Partial column-major matvec over k in [k0, k1) for one 32-row block: lanes
+// with g == 0 return the sums of rows 32rb + 4rq .. +3 (see warp_cm_matvec).
+__device__ __noinline__ void warp_cm_partial(const float* __restrict__ Mcm, int ldg, int rb, const double* x, int k0,
+                                       int k1, double (&acc)[4]) {
+  const int lane = threadIdx.x & 31;
+  const int rq = lane & 7, g = lane >> 3;
+  const int row0 = rb * 32 + 4 * rq;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (row0 < ldg) {
+    const float* p = Mcm + row0;
+#pragma unroll 8
+    for (int k = k0 + g; k < k1; k += 4) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(p + (size_t)k * ldg));
+      const double xk = x[k];
+      a0 = fma((double)v.x, xk, a0);
+      a1 = fma((double)v.y, xk, a1);
+      a2 = fma((double)v.z, xk, a2);
+      a3 = fma((double)v.w, xk, a3);
+    }
+  }
+#pragma unroll
+  for (int o = 8; o <= 16; o <<= 1) {
+    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+  }
+  acc[0] = a0; acc[1] = a1; acc[2] = a2; acc[3] = a3;
+}
+
+// Stage operator product for one (4*RQ)-row block: acc = M x (+ M2 x2), both
+// column-major with leading dimension ld (rows padded with zeros).  Lane
+// (rq, g): rows 4rq..4rq+3 of the block as one 16-byte load per column, k =
+// g, g + 32/RQ, ...  Lanes with g == 0 return the sums.
+template <int RQ>
+__device__ __noinline__ void warp_stage_mv(const float* __restrict__ M, int ld, int rb, const double* x, int klen,
+                                     const float* __restrict__ M2, const double* x2, int klen2, double (&acc)[4]) {
+  constexpr int KG = 32 / RQ;
+  const int lane = threadIdx.x & 31;
+  const int rq = lane % RQ, g = lane / RQ;
+  const int row0 = rb * 4 * RQ + 4 * rq;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (row0 < ld) {
+#pragma unroll 4
+    for (int k = g; k < klen; k += KG) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(M + (size_t)k * ld + row0));
+      const double xk = x[k];
+      a0 = fma((double)v.x, xk, a0);
+      a1 = fma((double)v.y, xk, a1);
+      a2 = fma((double)v.z, xk, a2);
+      a3 = fma((double)v.w, xk, a3);
+    }
+    if (M2) {
+#pragma unroll 4
+      for (int k = g; k < klen2; k += KG) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(M2 + (size_t)k * ld + row0));
+        const double xk = x2[k];
+        a0 = fma((double)v.x, xk, a0);
+        a1 = fma((double)v.y, xk, a1);
+        a2 = fma((double)v.z, xk, a2);
+        a3 = fma((double)v.w, xk, a3);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = RQ; o < 32; o <<= 1) {
+    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+  }
+  acc[0] = a0; acc[1] = a1; acc[2] = a2; acc[3] = a3;
+}
+
+// One matvec of a replay round: y = add + sgn * M x (M column-major, fp32).
+struct MvTask {
+  const float* M;
+  const double* x;
+  const double* add;
+  double sgn;
+  double* y;
+  unsigned mask;  // ranks (besides this one) whose replica of y consumes the result
+};
+
+// Runs `ntask` independent matvecs (descriptors from desc(i)) with the CTA's
+// warps, splitting the k range over up to 4 warps when there are fewer
+// (task, row block) pairs than warps.  Partial sums are combined in a fixed
+// order, so the result does not depend on timing.  Ends with __syncthreads
+// (outputs are complete in this CTA; remote replicas need the caller's
+// cluster barrier).
+__device__ inline unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <class Desc>
+__device__ void mv_round(int ntask, int n, int ldg, double* part, const Cl& cl, Desc desc,
+                         unsigned long long* dbg = nullptr) {
+  auto D = [&](int j) { if (dbg && threadIdx.x == 0) dbg[j] = clock64(); };
+  D(0);
+  const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, nwarp = nthr >> 5, lane = tid & 31;
+  const int RB = (n + 31) >> 5;
+  const int base = ntask * RB;
+  int KS = 1;
+  while (KS < 4 && base * KS * 2 <= nwarp) KS <<= 1;
+  if (KS == 1) {
+    for (int t = warp; t < base; t += nwarp) {
+      const int ti = t / RB, rb = t - ti * RB;
+      const MvTask d = desc(ti);
+      double acc[4];
+      warp_cm_partial(d.M, ldg, rb, d.x, 0, n, acc);
+      if ((lane >> 3) == 0) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int row = rb * 32 + 4 * (lane & 7) + r;
+          if (row < n) {
+            const double v = d.add[row] + d.sgn * acc[r];
+            cl.put_mask(d.y + row, v, d.mask);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    return;
+  }
+  const int kc = ((n + KS - 1) / KS + 3) & ~3;  // slice length, multiple of 4 (keeps the lane interleave)
+  for (int t = warp; t < base * KS; t += nwarp) {
+    const int tb = t / KS, ks = t - tb * KS;
+    const int ti = tb / RB, rb = tb - ti * RB;
+    const MvTask d = desc(ti);
+    if (t == 0) D(1);
+    double acc[4];
+    const int k0 = ks * kc;
+    warp_cm_partial(d.M, ldg, rb, d.x, k0, min(n, k0 + kc), acc);
+    if (t == 0) D(2);
+    if ((lane >> 3) == 0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) part[(tb * KS + ks) * 32 + 4 * (lane & 7) + r] = acc[r];
+    }
+  }
+  __syncthreads();
+  D(3);
+  for (int e = tid; e < base * 32; e += nthr) {
+    const int tb = e >> 5, ro = e & 31;
+    const int ti = tb / RB, rb = tb - ti * RB;
+    const int row = rb * 32 + ro;
+    if (row >= n) continue;
+    double s = 0.0;
+    for (int ks = 0; ks < KS; ++ks) s += part[(tb * KS + ks) * 32 + ro];
+    const MvTask d = desc(ti);
+    const double v = d.add[row] + d.sgn * s;
+    cl.put_mask(d.y + row, v, d.mask);
+  }
+  D(4);
+  __syncthreads();
+}
+
+// Cooperative dot products: G lanes per output, outputs spread over the whole
+// cluster (gt / gs = cluster-wide thread index / stride).  out(e, s) is called
+// by the group's first lane with s = sum_t term(e, t), t < len.
+template <int G, class Term, class Out>
+__device__ inline void gdot(int total, int len, int gt, int gs, Term term, Out out) {
+  const int lane = threadIdx.x & 31, lg = lane & (G - 1);
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  for (int e = gt / G; e < total; e += gs / G) {
+    double s = 0.0;
+#pragma unroll 16
+    for (int t = lg; t < len; t += G) s += term(e, t);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(gmask, s, o);
+    if (lg == 0) out(e, s);
+  }
+}
+
+// Single CTA per instance (large batches): one thread per output keeps more
+// independent work in flight per warp; clusters: G lanes per output.
+template <int G, class Term, class Out>
+__device__ inline void gdotc(int cs, int total, int len, int gt, int gs, Term term, Out out) {
+  if (cs == 1) gdot<1>(total, len, gt, gs, term, out);
+  else gdot<G>(total, len, gt, gs, term, out);
+}
+
+__global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
   const DevLqr& L = a.L;
   const int inst = a.list ? a.list[blockIdx.y] : (int)blockIdx.y;
   const int n = L.n, m = L.m, c = L.c, nf = L.nf, N = L.N, ldg = L.ldg, mtot = L.mtot;
   const size_t MS = (size_t)n * ldg;
-  const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, nwarp = nthr >> 5;
-  const VecLayout V = vec_layout(n, m, N, mtot, L.cvf_nslots, L.cot_nslots, a.max_layer);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  Cl cl;
+  cl.rank = cluster_rank();
+  cl.cs = cluster_size();
+  const int rank = (int)cl.rank, cs = (int)cl.cs;
+  const int gt = rank * nthr + tid, gs = cs * nthr;  // cluster-wide thread index / stride
+  const VecLayout V = vec_layout(n, m, N, mtot, L.cvf_nslots, L.cot_nslots, a.max_layer, L.cvf_nops, L.cot_nops,
+                                 L.cvf_layers, L.cot_layers);
   extern __shared__ double smem[];
   double* vs = a.gscratch ? a.gscratch + (size_t)inst * a.scratch_floats : smem;
   double *pv = vs + V.pv, *bv = vs + V.bv, *cb = vs + V.cb, *t1 = vs + V.t1, *t2 = vs + V.t2;
   double *z = vs + V.z, *lam = vs + V.lam, *y = vs + V.y;
   double *rhat = vs + V.rhat, *om = vs + V.om, *kf = vs + V.kf, *du = vs + V.du, *red = vs + V.red;
+  double *part = vs + V.part, *redall = vs + V.redall;
   __shared__ int s_flag;  // 0 continue, 1 done, 2 rebuild
+  __shared__ double s_rho;
 
   const size_t sN = (size_t)inst * N;
-  const float* Cq = a.qp.C + sN * c * n;
-  const float* Dq = a.qp.D + sN * c * m;
   const float* Bq = a.qp.B + sN * n * m;
   const double* bq = a.qp.b + sN * n;
   const float* CNq = a.qp.CN + (size_t)inst * nf * n;
@@ -170,8 +420,33 @@ __global__ void __launch_bounds__(512, 1) k_replay(ReplayArgs a) {
   const float* cvf_rec = L.cvf_rec + (size_t)inst * L.cvf_nops * 4 * MS;
   const float* cot_rec = L.cot_rec + (size_t)inst * L.cot_nops * MS;
   const double* dx0 = a.qp.dx0 + (size_t)inst * n;
+  const float* X23 = L.X23 + sN * c * L.ld2n;
+  const double* pb0 = L.pb0 + sN * 2 * n;
+  const float* X5 = L.X5 + sN * n * L.ldm;
+  const float* X4 = L.X4 + sN * c * L.ldm;
+  const double* kk0 = L.kk0 + sN * m;
+  const float* Bcm = L.Bcm + sN * m * L.ldn;
+  const float* Zcm = L.Zcm + sN * n * L.ldc;
+  const float* Dcm = L.Dcm + sN * m * L.ldc;
+  const int warp = tid >> 5, lane = tid & 31, nwarp = nthr >> 5;
+
+  double* w = vs + V.w;
+  // the scan plans, copied to shared memory (every op / layer lookup is on a phase's critical path)
+  int4* s_cvf_ops = reinterpret_cast<int4*>(vs + V.plan);
+  int4* s_cot_ops = s_cvf_ops + L.cvf_nops;
+  int* s_cvf_loff = reinterpret_cast<int*>(s_cot_ops + L.cot_nops);
+  int* s_cot_loff = s_cvf_loff + L.cvf_layers + 1;
+  int* s_cvf_out = s_cot_loff + L.cot_layers + 1;
+  int* s_cot_out = s_cvf_out + N + 1;
+  for (int i = tid; i < L.cvf_nops; i += nthr) s_cvf_ops[i] = L.cvf_ops[i];
+  for (int i = tid; i < L.cot_nops; i += nthr) s_cot_ops[i] = L.cot_ops[i];
+  for (int i = tid; i <= L.cvf_layers; i += nthr) s_cvf_loff[i] = L.cvf_loff[i];
+  for (int i = tid; i <= L.cot_layers; i += nthr) s_cot_loff[i] = (N > 0) ? L.cot_loff[i] : 0;
+  for (int i = tid; i <= N; i += nthr) s_cvf_out[i] = L.cvf_out[i];
+  for (int i = tid; i < N; i += nthr) s_cot_out[i] = L.cot_out[i];
+  __syncthreads();
   // dx_k lives in the COT outputs (k >= 1) or dx0
-  auto dxp = [&](int k) -> const double* { return k == 0 ? dx0 : cb + (size_t)L.cot_out[k - 1] * n; };
+  auto dxp = [&](int k) -> const double* { return k == 0 ? dx0 : cb + (size_t)s_cot_out[k - 1] * n; };
 
   const bool admm = a.mode == MODE_ADMM;
   double rho = 0.0;
@@ -182,193 +457,312 @@ __global__ void __launch_bounds__(512, 1) k_replay(ReplayArgs a) {
     const double* zg = a.state.z + (size_t)inst * mtot;
     const double* lg = a.state.lam + (size_t)inst * mtot;
     const double* yg = a.state.y + (size_t)inst * mtot;
-    for (int e = tid; e < mtot; e += nthr) { z[e] = zg[e]; lam[e] = lg[e]; y[e] = yg[e]; }
-    __syncthreads();
+    for (int e = tid; e < mtot; e += nthr) {
+      z[e] = zg[e]; lam[e] = lg[e]; y[e] = yg[e];
+      w[e] = yg[e] - zg[e];
+    }
   }
-  const int RB = (n + 31) >> 5;  // 32-row blocks per matvec
+  // Consumer ranks of every scan slot (clusters only).  Stage k's leaf terms,
+  // feedforward, constraint rows and state live on rank srank(k) = k % cs; op
+  // oi of a layer runs on rank oi / ceil(ops / cs).  A slot goes to the ranks
+  // of the ops that read it and of the stage that reads it as p+ / dx.
+  unsigned* cvf_mask = reinterpret_cast<unsigned*>(vs + V.masks);
+  unsigned* cot_mask = cvf_mask + L.cvf_nslots;
+  auto srank = [&](int k) { return k % cs; };
+  for (int i = tid; i < L.cvf_nslots + L.cot_nslots; i += nthr) cvf_mask[i] = 0u;
+  __syncthreads();
+  if (cs > 1) {
+    for (int lay = 0; lay < L.cvf_layers; ++lay) {
+      const int o0 = s_cvf_loff[lay], no = s_cvf_loff[lay + 1] - o0, per = (no + cs - 1) / cs;
+      for (int oi = tid; oi < no; oi += nthr) {
+        const int4 op = s_cvf_ops[o0 + oi];
+        atomicOr(cvf_mask + op.y, 1u << (oi / per));
+        atomicOr(cvf_mask + op.z, 1u << (oi / per));
+      }
+    }
+    for (int p = tid; p <= N; p += nthr) atomicOr(cvf_mask + s_cvf_out[p], 1u << srank(max(p - 1, 0)));
+    for (int lay = 0; lay < L.cot_layers; ++lay) {
+      const int o0 = s_cot_loff[lay], no = s_cot_loff[lay + 1] - o0, per = (no + cs - 1) / cs;
+      for (int oi = tid; oi < no; oi += nthr) {
+        const int4 op = s_cot_ops[o0 + oi];
+        atomicOr(cot_mask + op.y, 1u << (oi / per));
+        atomicOr(cot_mask + op.z, 1u << (oi / per));
+      }
+    }
+    for (int k = 1 + tid; k <= N; k += nthr) atomicOr(cot_mask + s_cot_out[k - 1], 1u << srank(k));
+  }
+  // stages owned by this rank: k = rank, rank + cs, ... < N
+  const int nls = (rank < N) ? (N - rank + cs - 1) / cs : 0;
+  cl.sync();  // replicas of every CTA exist before the first remote store
+  bool tr_on = a.trace != nullptr && rank == 0 && tid == 0 && blockIdx.y == 0;
+  int tn = 0;
+  auto TR = [&]() {
+    if (tr_on && tn < 255) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[++tn] = t;
+      a.trace[0] = tn;
+    }
+  };
+  TR();
 
   for (;;) {
-    // ---- linear terms q + rho C'(y - z), r + rho D'(y - z) and CVF leaves --------
-    for (int e = tid; e < N * m; e += nthr) {
-      const int k = e / m, i = e - k * m;
-      double s = 0.0;
-      if (admm)
-        for (int r = 0; r < c; ++r) s = fma((double)Dq[((size_t)k * c + r) * m + i], y[k * c + r] - z[k * c + r], s);
-      rhat[e] = admm ? r_lin[e] + rho * s : r_lin[e];
-    }
-    for (int e = tid; e < N * n; e += nthr) {
-      const int k = e / n, i = e - k * n;
-      double s = 0.0;
-      if (admm)
-        for (int r = 0; r < c; ++r) s = fma((double)Cq[((size_t)k * c + r) * n + i], y[k * c + r] - z[k * c + r], s);
-      pv[e] = admm ? q_lin[e] + rho * s : q_lin[e];
-    }
-    for (int i = tid; i < n; i += nthr) {
-      double s = 0.0;
-      if (admm)
-        for (int f = 0; f < nf; ++f) s = fma((double)CNq[f * n + i], y[N * c + f] - z[N * c + f], s);
-      pv[N * n + i] = admm ? qN_lin[i] + rho * s : qN_lin[i];
-      bv[N * n + i] = 0.0;
-    }
-    __syncthreads();
-    for (int e = tid; e < N * m; e += nthr) {
-      const int k = e / m, i = e - k * m;
-      double s = 0.0;
-      for (int t = 0; t < m; ++t) s = fma((double)Rinv[((size_t)k * m + i) * m + t], rhat[k * m + t], s);
-      om[e] = s;
-    }
-    __syncthreads();
-    for (int e = tid; e < N * n; e += nthr) {
-      const int k = e / n, i = e - k * n;
-      double s1 = 0.0, s2 = 0.0;
-      for (int l = 0; l < m; ++l) {
-        const double o = om[k * m + l];
-        s1 = fma((double)Shat[((size_t)k * m + l) * n + i], o, s1);
-        s2 = fma((double)Bq[((size_t)k * n + i) * m + l], o, s2);
+    // ---- CVF leaves: [p; b]_k = pb0_k + X23_k (y - z)_k (fused augment_linear +
+    //      _linear_element_terms, admm.py:113-121, lqr.py:338-342) --------------------
+    if (admm) {
+      const int RB2 = (2 * n + 31) >> 5;
+      for (int t = warp; t < nls * RB2; t += nwarp) {
+        const int k = rank + (t / RB2) * cs, rb = t % RB2;
+        double acc[4];
+        warp_stage_mv<8>(X23 + (size_t)k * c * L.ld2n, L.ld2n, rb, w + k * c, c, nullptr, nullptr, 0, acc);
+        if (lane < 8) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int row = rb * 32 + 4 * lane + r;
+            if (row < 2 * n) {
+              const double v = pb0[(size_t)k * 2 * n + row] + acc[r];
+              if (row < n) cl.put_mask(pv + k * n + row, v, cvf_mask[k]);
+              else cl.put_mask(bv + k * n + row - n, v, cvf_mask[k]);
+            }
+          }
+        }
       }
-      pv[e] = pv[e] - s1;
-      bv[e] = bq[e] - s2;
+      if (rank == srank(N))
+        for (int i = tid; i < n; i += nthr) {
+          double s = 0.0;
+          for (int f = 0; f < nf; ++f) s = fma((double)CNq[f * n + i], w[N * c + f], s);
+          cl.put_mask(pv + N * n + i, qN_lin[i] + rho * s, cvf_mask[N]);
+          cl.put_mask(bv + N * n + i, 0.0, cvf_mask[N]);
+        }
+      cl.sync();
+      TR();
+    } else {  // LQR mode: plain linear terms (lqr.py:338-342)
+      for (int e = gt; e < N * m; e += gs) cl.put(rhat + e, r_lin[e]);
+      for (int e = gt; e < N * n; e += gs) cl.put(pv + e, q_lin[e]);
+      for (int i = gt; i < n; i += gs) {
+        cl.put(pv + N * n + i, qN_lin[i]);
+        cl.put(bv + N * n + i, 0.0);
+      }
+      cl.sync();
+      TR();
+      gdotc<4>(cs, N * m, m, gt, gs,
+              [&](int e, int t) { const int k = e / m, i = e - k * m;
+                                  return (double)Rinv[((size_t)k * m + i) * m + t] * rhat[k * m + t]; },
+              [&](int e, double s) { cl.put(om + e, s); });
+      cl.sync();
+      TR();
+      gdotc<4>(cs, N * n, m, gt, gs,
+              [&](int e, int l) { const int k = e / n, i = e - k * n;
+                                  return (double)Shat[((size_t)k * m + l) * n + i] * om[k * m + l]; },
+              [&](int e, double s) { cl.put(pv + e, pv[e] - s); });
+      gdotc<4>(cs, N * n, m, gt, gs,
+              [&](int e, int l) { const int k = e / n, i = e - k * n;
+                                  return (double)Bq[((size_t)k * n + i) * m + l] * om[k * m + l]; },
+              [&](int e, double s) { cl.put(bv + e, bq[e] - s); });
+      cl.sync();
+      TR();
     }
-    __syncthreads();
 
-    // ---- CVF replay (reverse tree): 2 rounds per layer -----------------------
+    // ---- CVF replay (reverse tree): ops of a layer spread over the cluster ------
     for (int lay = 0; lay < L.cvf_layers; ++lay) {
-      const int o0 = L.cvf_loff[lay], no = L.cvf_loff[lay + 1] - o0;
+      const int o0 = s_cvf_loff[lay], no = s_cvf_loff[lay + 1] - o0;
       if (no == 0) continue;
-      const int tasks = no * 2 * RB;
-      for (int t = warp; t < tasks; t += nwarp) {
-        const int oi = t / (2 * RB), rem = t - oi * 2 * RB, which = rem / RB, rb = rem - which * RB;
-        const int4 op = L.cvf_ops[o0 + oi];
-        const float* rec = cvf_rec + (size_t)(o0 + oi) * 4 * MS;
-        if (which == 0)  // t1 = p_later + Pr b_earlier
-          warp_cm_matvec(rec + 1 * MS, ldg, n, rb, bv + op.y * n, pv + op.z * n, 1.0, t1 + oi * n);
-        else             // t2 = b_earlier - Cl p_later
-          warp_cm_matvec(rec + 3 * MS, ldg, n, rb, pv + op.z * n, bv + op.y * n, -1.0, t2 + oi * n);
+      const int per = (no + cs - 1) / cs;
+      const int lo = min(no, rank * per), nl = min(no, lo + per) - lo;
+      if (nl > 0) {
+        mv_round(2 * nl, n, ldg, part, cl, [&](int ti) {
+          const int oi = lo + (ti >> 1);
+          const int4 op = s_cvf_ops[o0 + oi];
+          const float* rec = cvf_rec + (size_t)(o0 + oi) * 4 * MS;
+          if ((ti & 1) == 0)  // t1 = p_later + Pr b_earlier
+            return MvTask{rec + 1 * MS, bv + op.y * n, pv + op.z * n, 1.0, t1 + (oi - lo) * n, 0u};
+          // t2 = b_earlier - Cl p_later
+          return MvTask{rec + 3 * MS, pv + op.z * n, bv + op.y * n, -1.0, t2 + (oi - lo) * n, 0u};
+        }, (tr_on && lay == 3) ? a.trace + 200 : nullptr);
+        TR();
+        mv_round(2 * nl, n, ldg, part, cl, [&](int ti) {
+          const int oi = lo + (ti >> 1);
+          const int4 op = s_cvf_ops[o0 + oi];
+          const float* rec = cvf_rec + (size_t)(o0 + oi) * 4 * MS;
+          if ((ti & 1) == 0)  // p = Ups t1 + p_earlier
+            return MvTask{rec + 0 * MS, t1 + (oi - lo) * n, pv + op.y * n, 1.0, pv + op.x * n, cvf_mask[op.x]};
+          // b = Psi t2 + b_later
+          return MvTask{rec + 2 * MS, t2 + (oi - lo) * n, bv + op.z * n, 1.0, bv + op.x * n, cvf_mask[op.x]};
+        });
       }
-      __syncthreads();
-      for (int t = warp; t < tasks; t += nwarp) {
-        const int oi = t / (2 * RB), rem = t - oi * 2 * RB, which = rem / RB, rb = rem - which * RB;
-        const int4 op = L.cvf_ops[o0 + oi];
-        const float* rec = cvf_rec + (size_t)(o0 + oi) * 4 * MS;
-        if (which == 0)  // p = Ups t1 + p_earlier
-          warp_cm_matvec(rec + 0 * MS, ldg, n, rb, t1 + oi * n, pv + op.y * n, 1.0, pv + op.x * n);
-        else             // b = Psi t2 + b_later
-          warp_cm_matvec(rec + 2 * MS, ldg, n, rb, t2 + oi * n, bv + op.z * n, 1.0, bv + op.x * n);
-      }
-      __syncthreads();
+      cl.sync();
+      TR();
     }
 
     // ---- feedforward k = -Gamma (B'(p+ + P+ b) + r) and COT leaves ---------------
-    for (int e = tid; e < N * m; e += nthr) {
-      const int k = e / m, l = e - k * m;
-      const double* pn = pv + (size_t)L.cvf_out[k + 1] * n;
-      const double* cvk = cvec + (size_t)k * n;
-      double s = 0.0;
-      for (int i = 0; i < n; ++i) s = fma((double)Bq[((size_t)k * n + i) * m + l], pn[i] + cvk[i], s);
-      om[e] = s + rhat[e];
+    //      (lqr.py:345-356; ADMM: kf = kk0 + X5 p+ + X4 (y - z), cb = B kf + b)
+    if (admm) {
+      const int RBm = (m + 15) >> 4;
+      for (int t = warp; t < nls * RBm; t += nwarp) {
+        const int k = rank + (t / RBm) * cs, rb = t % RBm;
+        double acc[4];
+        warp_stage_mv<4>(X5 + (size_t)k * n * L.ldm, L.ldm, rb, pv + (size_t)s_cvf_out[k + 1] * n, n,
+                         X4 + (size_t)k * c * L.ldm, w + k * c, c, acc);
+        if (lane < 4) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int row = rb * 16 + 4 * lane + r;
+            if (row < m) kf[k * m + row] = kk0[(size_t)k * m + row] + acc[r];  // read on this rank only
+          }
+        }
+      }
+      __syncthreads();
+      TR();
+      const int RBn = (n + 31) >> 5;
+      for (int t = warp; t < nls * RBn; t += nwarp) {
+        const int k = rank + (t / RBn) * cs, rb = t % RBn;
+        double acc[4];
+        warp_stage_mv<8>(Bcm + (size_t)k * m * L.ldn, L.ldn, rb, kf + k * m, m, nullptr, nullptr, 0, acc);
+        if (lane < 8) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int row = rb * 32 + 4 * lane + r;
+            if (row < n) {
+              const double bb = acc[r] + bq[(size_t)k * n + row];
+              cl.put_mask(cb + k * n + row, (k == 0) ? v0[row] + bb : bb, cot_mask[k]);
+            }
+          }
+        }
+      }
+      cl.sync();
+      TR();
+    } else {
+      gdotc<8>(cs, N * m, n, gt, gs,
+              [&](int e, int i) { const int k = e / m, l = e - k * m;
+                                  return (double)Bq[((size_t)k * n + i) * m + l] *
+                                         (pv[(size_t)s_cvf_out[k + 1] * n + i] + cvec[(size_t)k * n + i]); },
+              [&](int e, double s) { cl.put(om + e, s + rhat[e]); });
+      cl.sync();
+      TR();
+      gdotc<4>(cs, N * m, m, gt, gs,
+              [&](int e, int t) { const int k = e / m, l = e - k * m;
+                                  return (double)Gam[((size_t)k * m + l) * m + t] * om[k * m + t]; },
+              [&](int e, double s) { cl.put(kf + e, -s); });
+      cl.sync();
+      TR();
+      gdotc<4>(cs, N * n, m, gt, gs,
+              [&](int e, int l) { const int k = e / n;
+                                  return (double)Bq[(size_t)e * m + l] * kf[k * m + l]; },
+              [&](int e, double s) { const int k = e / n, i = e - k * n;
+                                     const double bb = s + bq[e];
+                                     cl.put(cb + e, (k == 0) ? v0[i] + bb : bb); });
+      cl.sync();
+      TR();
     }
-    __syncthreads();
-    for (int e = tid; e < N * m; e += nthr) {
-      const int k = e / m, l = e - k * m;
-      double s = 0.0;
-      for (int t = 0; t < m; ++t) s = fma((double)Gam[((size_t)k * m + l) * m + t], om[k * m + t], s);
-      kf[e] = -s;
-    }
-    __syncthreads();
-    for (int e = tid; e < N * n; e += nthr) {
-      const int k = e / n, i = e - k * n;
-      double s = 0.0;
-      for (int l = 0; l < m; ++l) s = fma((double)Bq[((size_t)k * n + i) * m + l], kf[k * m + l], s);
-      const double bb = s + bq[e];
-      cb[e] = (k == 0) ? v0[i] + bb : bb;
-    }
-    __syncthreads();
 
     // ---- COT replay (forward tree): 1 round per layer -------------------------
     for (int lay = 0; lay < L.cot_layers; ++lay) {
-      const int o0 = L.cot_loff[lay], no = L.cot_loff[lay + 1] - o0;
+      const int o0 = s_cot_loff[lay], no = s_cot_loff[lay + 1] - o0;
       if (no == 0) continue;
-      const int tasks = no * RB;
-      for (int t = warp; t < tasks; t += nwarp) {
-        const int oi = t / RB, rb = t - oi * RB;
-        const int4 op = L.cot_ops[o0 + oi];
-        warp_cm_matvec(cot_rec + (size_t)(o0 + oi) * MS, ldg, n, rb, cb + op.y * n, cb + op.z * n, 1.0,
-                       cb + op.x * n);
-      }
-      __syncthreads();
+      const int per = (no + cs - 1) / cs;
+      const int lo = min(no, rank * per), nl = min(no, lo + per) - lo;
+      if (nl > 0)
+        mv_round(nl, n, ldg, part, cl, [&](int ti) {
+          const int oi = lo + ti;
+          const int4 op = s_cot_ops[o0 + oi];
+          return MvTask{cot_rec + (size_t)(o0 + oi) * MS, cb + op.y * n, cb + op.z * n, 1.0, cb + op.x * n,
+                        cot_mask[op.x]};
+        });
+      cl.sync();
+      TR();
     }
-
-    // ---- du = K dx + k ------------------------------------------------------------
-    for (int e = tid; e < N * m; e += nthr) {
-      const int k = e / m, l = e - k * m;
-      const double* xk = dxp(k);
-      double s = 0.0;
-      for (int i = 0; i < n; ++i) s = fma((double)Kg[((size_t)k * m + l) * n + i], xk[i], s);
-      du[e] = s + kf[e];
-    }
-    __syncthreads();
 
     if (!admm) {
-      write_last(L, inst, kf, pv, tid, nthr);
-      double* gdx = a.dx + (size_t)inst * (N + 1) * n;
-      double* gdu = a.du + (size_t)inst * N * m;
-      for (int e = tid; e < (N + 1) * n; e += nthr) gdx[e] = dxp(e / n)[e % n];
-      for (int e = tid; e < N * m; e += nthr) gdu[e] = du[e];
-      if (a.k_out)
-        for (int e = tid; e < N * m; e += nthr) a.k_out[(size_t)inst * N * m + e] = kf[e];
-      if (a.p_out)
-        for (int e = tid; e < (N + 1) * n; e += nthr) {
-          const int k = e / n, i = e - k * n;
-          a.p_out[(size_t)inst * (N + 1) * n + e] = pv[L.cvf_out[k] * n + i];
-        }
+      // ---- du = K dx + k ------------------------------------------------------------
+      gdotc<8>(cs, N * m, n, gt, gs,
+              [&](int e, int i) { const int k = e / m;
+                                  return (double)Kg[(size_t)e * n + i] * dxp(k)[i]; },
+              [&](int e, double s) { cl.put(du + e, s + kf[e]); });
+      cl.sync();
+      TR();
+      if (rank == 0) {
+        write_last(L, inst, kf, pv, tid, nthr);
+        double* gdx = a.dx + (size_t)inst * (N + 1) * n;
+        double* gdu = a.du + (size_t)inst * N * m;
+        for (int e = tid; e < (N + 1) * n; e += nthr) gdx[e] = dxp(e / n)[e % n];
+        for (int e = tid; e < N * m; e += nthr) gdu[e] = du[e];
+        if (a.k_out)
+          for (int e = tid; e < N * m; e += nthr) a.k_out[(size_t)inst * N * m + e] = kf[e];
+        if (a.p_out)
+          for (int e = tid; e < (N + 1) * n; e += nthr) {
+            const int k = e / n, i = e - k * n;
+            a.p_out[(size_t)inst * (N + 1) * n + e] = pv[s_cvf_out[k] * n + i];
+          }
+      }
+      cl.sync();  // no CTA leaves while others may still store into its replica
       return;
     }
 
-    // ---- ADMM: G = C dx + D du, projection, dual ascent, residuals ---------------
+    // ---- ADMM: G = Z dx + D kf (= C dx + D du), projection, dual ascent,
+    //      residuals (admm.py:91-97, :130-135, :184-189) ----------------------------
     const double* fst = a.qp.f + sN * c;
     const double* fN = a.qp.fN + (size_t)inst * nf;
     double rp = 0.0, rdz = 0.0;
-    for (int e = tid; e < mtot; e += nthr) {
-      double g, fe;
-      if (e < N * c) {
-        const int k = e / c, r = e - k * c;
-        const float* Cr = Cq + ((size_t)k * c + r) * n;
-        const float* Dr = Dq + ((size_t)k * c + r) * m;
-        const double* xk = dxp(k);
-        double s1 = 0.0, s2 = 0.0;
-        for (int i = 0; i < n; ++i) s1 = fma((double)Cr[i], xk[i], s1);
-        for (int l = 0; l < m; ++l) s2 = fma((double)Dr[l], du[k * m + l], s2);
-        g = s1 + s2;
-        fe = fst[e];
-      } else {
-        const int f = e - N * c;
-        const double* xN = dxp(N);
-        double s = 0.0;
-        for (int i = 0; i < n; ++i) s = fma((double)CNq[f * n + i], xN[i], s);
-        g = s;
-        fe = fN[f];
-      }
+    auto project = [&](int e, double g, double fe) {
       const double zo = z[e];
       const double zn = fmin(g + y[e], fe);
       const double ln = lam[e] + rho * (g - zn);
-      lam[e] = ln;
-      y[e] = ln / rho;
+      const double yn = ln / rho;
+      lam[e] = ln;  // stage rows live on their owner rank only
+      y[e] = yn;
       z[e] = zn;
+      w[e] = yn - zn;
       rp = fmax(rp, fabs(g - zn));
       rdz = fmax(rdz, fabs(zn - zo));
+    };
+    {
+      const int RBc = (c + 31) >> 5;
+      for (int t = warp; t < nls * RBc; t += nwarp) {
+        const int k = rank + (t / RBc) * cs, rb = t % RBc;
+        double acc[4];
+        warp_stage_mv<8>(Zcm + (size_t)k * n * L.ldc, L.ldc, rb, dxp(k), n, Dcm + (size_t)k * m * L.ldc,
+                         kf + k * m, m, acc);
+        if (lane < 8) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int row = rb * 32 + 4 * lane + r;
+            if (row < c) project(k * c + row, acc[r], fst[(size_t)k * c + row]);
+          }
+        }
+      }
+      for (int f = (rank == srank(N)) ? tid : nf; f < nf; f += nthr) {
+        const double* xN = dxp(N);
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s = fma((double)CNq[f * n + i], xN[i], s);
+        project(N * c + f, s, fN[f]);
+      }
     }
     rp = block_max_d(rp, red);
     rdz = block_max_d(rdz, red + 32);
     if (tid == 0) {
+      cl.put(redall + 2 * rank, rp);
+      cl.put(redall + 2 * rank + 1, rdz);
+    }
+    cl.sync();
+    TR();
+    if (tid == 0) {
+      double r_p = 0.0, r_dz = 0.0;
+      for (int r = 0; r < cs; ++r) {
+        r_p = fmax(r_p, redall[2 * r]);
+        r_dz = fmax(r_dz, redall[2 * r + 1]);
+      }
       ++it;
-      a.state.iteration[inst] += 1;
-      const double r_p = rp;
-      const double r_d = rho * rdz;
-      a.state.r_primal[inst] = r_p;
-      a.state.r_dual[inst] = r_d;
+      const double r_d = rho * r_dz;
+      const bool lead = rank == 0;
+      if (lead) {
+        a.state.iteration[inst] += 1;
+        a.state.r_primal[inst] = r_p;
+        a.state.r_dual[inst] = r_d;
+      }
       int flag = 0;
+      double rho_new = rho;
       if (r_p <= a.set.tol_primal && r_d <= a.set.tol_dual) {
-        a.stats.converged[inst] = 1;
+        if (lead) a.stats.converged[inst] = 1;
         flag = 1;
       } else {
         bool changed = false;
@@ -376,43 +770,105 @@ __global__ void __launch_bounds__(512, 1) k_replay(ReplayArgs a) {
           const double ratio = sqrt(fmax(r_p, 1e-30) / fmax(r_d, 1e-30));
           const double prop = fmin(fmax(rho * ratio, a.set.rho_min), a.set.rho_max);
           if (prop > 5.0 * rho || prop < rho / 5.0) {
-            a.state.rho[inst] = prop;
-            a.state.generation[inst] += 1;
-            a.stats.rho_changes[inst] += 1;
+            rho_new = prop;
+            if (lead) {
+              a.state.rho[inst] = prop;
+              a.state.generation[inst] += 1;
+              a.stats.rho_changes[inst] += 1;
+            }
             changed = true;
           }
         }
         if (it >= a.set.max_iter) flag = 1;
         else if (changed) flag = 2;
       }
-      a.stats.iterations[inst] = it;
+      if (lead) a.stats.iterations[inst] = it;
       s_flag = flag;
+      s_rho = rho_new;
     }
     __syncthreads();
     const int flag = s_flag;
+    tr_on = false;
     if (flag == 0) continue;
-    const double rho_new = a.state.rho[inst];
+    const double rho_new = s_rho;
+    // each rank writes back what it owns: stage k's rows on srank(k), terminal rows on srank(N)
+    auto owns_row = [&](int e) { return srank(e < N * c ? e / c : N) == rank; };
     if (rho_new != rho)  // committed change rescales y = lam / rho (admm.py:149)
-      for (int e = tid; e < mtot; e += nthr) y[e] = lam[e] / rho_new;
+      for (int e = tid; e < mtot; e += nthr)
+        if (owns_row(e)) y[e] = lam[e] / rho_new;
     __syncthreads();
-    double* zg = a.state.z + (size_t)inst * mtot;
-    double* lg = a.state.lam + (size_t)inst * mtot;
-    double* yg = a.state.y + (size_t)inst * mtot;
-    for (int e = tid; e < mtot; e += nthr) { zg[e] = z[e]; lg[e] = lam[e]; yg[e] = y[e]; }
-    if (flag == 1) {
-      write_last(L, inst, kf, pv, tid, nthr);
-      double* gdx = a.dx + (size_t)inst * (N + 1) * n;
-      double* gdu = a.du + (size_t)inst * N * m;
-      for (int e = tid; e < (N + 1) * n; e += nthr) gdx[e] = dxp(e / n)[e % n];
-      for (int e = tid; e < N * m; e += nthr) gdu[e] = du[e];
+    {
+      double* zg = a.state.z + (size_t)inst * mtot;
+      double* lg = a.state.lam + (size_t)inst * mtot;
+      double* yg = a.state.y + (size_t)inst * mtot;
+      for (int e = tid; e < mtot; e += nthr)
+        if (owns_row(e)) { zg[e] = z[e]; lg[e] = lam[e]; yg[e] = y[e]; }
+      if (flag == 1) {
+        double* gdx = a.dx + (size_t)inst * (N + 1) * n;
+        double* gdu = a.du + (size_t)inst * N * m;
+        for (int e = tid; e < (N + 1) * n; e += nthr) {
+          const int p = e / n, i = e - p * n;
+          if ((p == 0 ? 0 : srank(p)) == rank) gdx[e] = dxp(p)[i];
+          if (srank(max(p - 1, 0)) == rank)  // cost-to-go gradient of the last replay
+            L.last_p[(size_t)inst * (N + 1) * n + e] = pv[s_cvf_out[p] * n + i];
+        }
+        for (int e = tid; e < N * m; e += nthr) {  // du = K dx + k (lqr.py:359-363), once at exit
+          const int k = e / m;
+          if (srank(k) != rank) continue;
+          const double* xk = dxp(k);
+          double s = 0.0;
+          for (int i = 0; i < n; ++i) s = fma((double)Kg[(size_t)e * n + i], xk[i], s);
+          gdu[e] = s + kf[e];
+          L.last_k[(size_t)inst * N * m + e] = kf[e];
+        }
+      }
+      if (rank == 0 && tid == 0) a.status[inst] = (flag == 2) ? ST_REBUILD : ST_DONE;
     }
-    if (tid == 0) a.status[inst] = (flag == 2) ? ST_REBUILD : ST_DONE;
+    cl.sync();
+    TR();
     return;
   }
 }
 
 // ---------------------------------------------------------------------------
 // host side
+
+// Cluster size for a replay launch: spread each instance over up to 16 SMs
+// while the whole batch still fits in one wave (small batches are latency-
+// bound on one SM's L2 bandwidth); 1 for large batches.  GSLS_REPLAY_CLUSTER
+// overrides (power of two <= 16).
+static int replay_cluster(Ctx* c, int count, size_t smem_bytes) {
+  if (c->d_scratch) return 1;  // vectors in global memory: no DSMEM replicas
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int want = 16;
+  if (const char* e = getenv("GSLS_REPLAY_CLUSTER")) want = std::max(1, std::min(16, atoi(e)));
+  for (int cs = want; cs >= 2; cs >>= 1) {
+    if ((long long)count * cs > sms) continue;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cs, count);
+    cfg.blockDim = dim3(kReplayThreads);
+    cfg.dynamicSmemBytes = smem_bytes;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)k_replay, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (ncl >= count) return cs;
+  }
+  return 1;
+}
 
 static int launch_replay(Ctx* c, ReplayArgs& a, int count, cudaStream_t st) {
   if (count == 0) return GSLS_OK;
@@ -426,12 +882,48 @@ static int launch_replay(Ctx* c, ReplayArgs& a, int count, cudaStream_t st) {
     a.gscratch = nullptr;
     a.scratch_floats = 0;
     sb = c->scratch_floats * sizeof(double);
-    if (sb > 48 * 1024)
-      GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
   }
-  ProfScope ps(P_REPLAY, st, (double)count);
-  k_replay<<<dim3(1, count), 512, sb, st>>>(a);
-  GSLS_CUDA_CHECK(cudaGetLastError());
+  static bool attrs_set = false;
+  if (!attrs_set) {
+    GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kReplaySmemMax)));
+    GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_replay, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attrs_set = true;
+  }
+  const int cs = (a.mode == MODE_ADMM) ? replay_cluster(c, count, sb) : 1;  // LQR-mode phases broadcast
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(cs, count);
+  cfg.blockDim = dim3(kReplayThreads);
+  cfg.dynamicSmemBytes = sb;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static unsigned long long* trace = nullptr;
+  const bool tracing = getenv("GSLS_REPLAY_TRACE") != nullptr;
+  if (tracing && !trace) GSLS_CUDA_CHECK(cudaMalloc(&trace, 256 * sizeof(unsigned long long)));
+  a.trace = tracing ? trace : nullptr;
+  if (tracing) GSLS_CUDA_CHECK(cudaMemsetAsync(trace, 0, 256 * sizeof(unsigned long long), st));
+  {
+    ProfScope ps(P_REPLAY, st, (double)count);
+    GSLS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_replay, a));
+    GSLS_CUDA_CHECK(cudaGetLastError());
+  }
+  if (tracing) {
+    unsigned long long h[256];
+    GSLS_CUDA_CHECK(cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st));
+    GSLS_CUDA_CHECK(cudaStreamSynchronize(st));
+    fprintf(stderr, "replay trace cs=%d count=%d:", cs, count);
+    for (unsigned long long i = 2; i <= h[0]; ++i) fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
+    fprintf(stderr, " | first iteration %.2f us | mv_round layer 3:", h[0] > 1 ? (h[h[0]] - h[1]) * 1e-3 : 0.0);
+    for (int j = 1; j < 5; ++j) fprintf(stderr, " %llu", h[200 + j] - h[200 + j - 1]);
+    fprintf(stderr, " cycles");
+    fprintf(stderr, "\n");
+  }
   return GSLS_OK;
 }
 

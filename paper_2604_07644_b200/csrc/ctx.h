@@ -40,6 +40,16 @@ struct DevLqr {
   double* v0;            // [batch][n]     Abar_0 dx0
   double* last_k;        // [batch][N][m]   feedforward of the last replay
   double* last_p;        // [batch][N+1][n] cost-to-go gradients of the last replay
+  // Fused per-stage operators of the ADMM iteration (rho-dependent, rebuilt with
+  // the cache), float32 column-major with padded leading dimensions so every
+  // per-iteration product is a coalesced 16-byte-load matvec (admm.cu):
+  //   [pv; bv]_k = pb0_k + X23_k (y - z)_k          X23: rows 2n, cols c, ld ld2n
+  //   kf_k       = kk0_k + X5_k p+_k + X4_k w_k     X5: m x n, X4: m x c, ld ldm
+  //   cb_k       = B_k kf_k + b_k                   Bcm: n x m, ld ldn
+  //   G_k        = Z_k dx_k + D_k kf_k              Zcm: c x n, Dcm: c x m, ld ldc  (Z = C + D K)
+  int ldm, ldn, ldc, ld2n;
+  float *X23, *X5, *X4, *Bcm, *Zcm, *Dcm;
+  double *pb0, *kk0;
   ErrSlot* err;          // [batch]
 };
 

@@ -11,19 +11,29 @@ __device__ inline void bar_named(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-constexpr int gj_scratch_words(int NP) { return 4 * NP + 48; }
+// Scratch words: double-buffered per-warp candidate rows + keys, the displaced
+// row, the permutation and flags.
+constexpr int gj_scratch_words(int NP) { return 2 * (NP / 8) * NP + 2 * NP + 4 * (NP / 8) + 2 * NP + 8; }
 
-// In-place Gauss-Jordan with partial pivoting.  4 threads per row, each holding
-// NP/4 consecutive columns of its row in registers; threads [0, 4*NP) take part
-// and synchronize with named barrier 1.  Per pivot step: warp argmax of |a_ik|
-// over the column-k owners (first index on ties, as LAPACK i*amax), one smem
-// exchange of the pivot row and the displaced row, 2 barriers, NP/4 FMAs per
-// thread.  Reads a (smem, row-major, lds); writes the inverse row-major to inv
-// and transposed to invT (either may be null or alias a: a is only read before
-// the first barrier).
-// Returns (block-uniform) false when a pivot is zero / non-finite / below
-// rel_tol * max|a| (the ill-conditioned-combine rule, lqr.py:229-232).
-// Must be called by the whole CTA (blockDim.x >= 4*NP).
+// In-place Gauss-Jordan with partial pivoting, one CTA barrier per pivot step.
+// 4 threads per row, each holding NP/4 consecutive columns of its row in
+// registers; threads [0, 4*NP) take part and synchronize with named barrier 1.
+//
+// Step k: the column-k owners of rows >= k form keys (bits(|a_ik|) + 1, which
+// order like |a_ik|); each warp finds its max with one redux.sync and the
+// first lane holding it with a ballot (first index on ties, as LAPACK
+// i*amax).  The warp's candidate row is published in a per-warp slot together
+// with its key, and row k publishes itself (the row the pivot displaces).
+// After the single barrier every thread picks the winning warp (largest key,
+// lowest warp on ties = lowest row) and reads the pivot row from that slot.
+// Slots are double-buffered by step parity, so the next step's writes never
+// race the previous step's reads.
+//
+// Reads a (smem, row-major, lds); writes the inverse row-major to inv and
+// transposed to invT (either may be null or alias a: a is only read before
+// the first barrier).  Returns (block-uniform) false when a pivot is zero /
+// non-finite / below rel_tol * max|a| (the ill-conditioned-combine rule,
+// lqr.py:229-232).  Must be called by the whole CTA (blockDim.x >= 4*NP).
 template <int NP>
 __device__ bool gj_inverse_rows(const float* a, float* inv, float* invT, int lds, int n, float* scratch,
                                 float rel_tol) {
@@ -31,13 +41,13 @@ __device__ bool gj_inverse_rows(const float* a, float* inv, float* invT, int lds
   constexpr int NT = NP * 4;
   constexpr int NW = NT / 32;
   static_assert(SEG % 4 == 0, "segments are moved as float4");
-  float* prow = scratch;                           // NP
-  float* krow = prow + NP;                         // NP
-  int* perm = reinterpret_cast<int*>(krow + NP);   // NP
-  int* pos = perm + NP;                            // NP
-  float* wv = reinterpret_cast<float*>(pos + NP);  // 16
-  int* wi = reinterpret_cast<int*>(wv + 16);       // 16
-  float* misc = reinterpret_cast<float*>(wi + 16);  // [0] max|a|, [1] fail flag
+  float* cand = scratch;                                        // [2][NW][NP]
+  float* krow = cand + 2 * NW * NP;                             // [2][NP]
+  unsigned* wkey = reinterpret_cast<unsigned*>(krow + 2 * NP);  // [2][NW]
+  int* wrow = reinterpret_cast<int*>(wkey + 2 * NW);            // [2][NW]
+  int* perm = wrow + 2 * NW;                                    // NP
+  int* pos = perm + NP;                                         // NP
+  float* misc = reinterpret_cast<float*>(pos + NP);             // [0] max|a|, [1] fail flag
   const int tid = threadIdx.x;
   const bool part = tid < NT;
   const int row = tid >> 2, q = tid & 3, lane = tid & 31, warp = tid >> 5;
@@ -50,82 +60,95 @@ __device__ bool gj_inverse_rows(const float* a, float* inv, float* invT, int lds
     mx = fmaxf(mx, fabsf(r[c]));
   }
   mx = warp_max(mx);
-  if (part && lane == 0) wv[warp] = mx;
+  if (part && lane == 0) cand[warp] = mx;  // partial maxima (cand is free until the loop)
   __syncthreads();
   if (tid == 0) {
     float m2 = 0.f;
-    for (int w = 0; w < NW; ++w) m2 = fmaxf(m2, wv[w]);
+    for (int w = 0; w < NW; ++w) m2 = fmaxf(m2, cand[w]);
     misc[0] = m2;
     misc[1] = 0.f;
   }
   __syncthreads();
   if (part) {
     const float thresh = rel_tol * misc[0];
-    for (int k = 0; k < n; ++k) {
-      const int qk = k / SEG, ck = k - qk * SEG;
-      float mine = 0.f;  // my row's element in column k (valid in the owner lane)
+    bool fail = false;
+    // k = qk*SEG + ck with ck unrolled, so r[ck] is a static register and the
+    // buffer parity (k & 1 == ck & 1) is static too.
+    for (int qk = 0; qk < 4; ++qk) {
 #pragma unroll
-      for (int c = 0; c < SEG; ++c)
-        if (c == ck) mine = r[c];
-      float v = (q == qk && row >= k && row < n) ? fabsf(mine) : -1.f;
-      int vi = row;
+      for (int ck = 0; ck < SEG; ++ck) {
+        const int k = qk * SEG + ck;
+        if (k < n) {
+          const int b = ck & 1;
+          const bool own = (q == qk);
+          const float mine = r[ck];  // my row's element in column k when own
+          const unsigned key = (own && row >= k && row < n) ? __float_as_uint(fabsf(mine)) + 1u : 0u;
+          const unsigned wmax = __reduce_max_sync(0xffffffffu, key);
+          const unsigned hits = __ballot_sync(0xffffffffu, key == wmax);
+          const int wl = __ffs(hits) - 1;  // owner lane of the warp's candidate row
+          // f = a[row][k] before this step, from the column-k owner of my row
+          const float fk = __shfl_sync(0xffffffffu, mine, (lane & ~3) | qk);
+          float* cb = cand + (b * NW + warp) * NP;
+          if ((lane >> 2) == (wl >> 2)) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, v, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
-        if (ov > v || (ov == v && oi < vi)) { v = ov; vi = oi; }
-      }
-      if (lane == 0) { wv[warp] = v; wi[warp] = vi; }
-      // f = a[row][k] before this step, broadcast from the column-k owner of my row
-      const float fk = __shfl_sync(0xffffffffu, mine, (lane & ~3) | qk);
-      bar_named(1, NT);
-      float bv = -1.f;
-      int p = n;
+            for (int c = 0; c < SEG; c += 4)
+              *reinterpret_cast<float4*>(cb + q * SEG + c) = make_float4(r[c], r[c + 1], r[c + 2], r[c + 3]);
+            if (q == 0) {
+              wkey[b * NW + warp] = wmax;
+              wrow[b * NW + warp] = row;
+            }
+          }
+          if (row == k) {
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const float ov = wv[w];
-        const int oi = wi[w];
-        if (ov > bv || (ov == bv && oi < p)) { bv = ov; p = oi; }
-      }
-      if (row == p) {
+            for (int c = 0; c < SEG; c += 4)
+              *reinterpret_cast<float4*>(krow + b * NP + q * SEG + c) =
+                  make_float4(r[c], r[c + 1], r[c + 2], r[c + 3]);
+          }
+          bar_named(1, NT);
+          unsigned bk = 0;
+          int bw = 0;
 #pragma unroll
-        for (int c = 0; c < SEG; c += 4)
-          *reinterpret_cast<float4*>(prow + q * SEG + c) = make_float4(r[c], r[c + 1], r[c + 2], r[c + 3]);
-      }
-      if (row == k) {
-#pragma unroll
-        for (int c = 0; c < SEG; c += 4)
-          *reinterpret_cast<float4*>(krow + q * SEG + c) = make_float4(r[c], r[c + 1], r[c + 2], r[c + 3]);
-      }
-      if (tid == 0) perm[k] = p;
-      bar_named(1, NT);
-      const float piv = prow[k];
-      if (tid == 0 && (!(fabsf(piv) > thresh) || !isfinite(piv))) misc[1] = 1.f;
-      const float ip = 1.f / piv;
-      float pr[SEG];
-#pragma unroll
-      for (int c = 0; c < SEG; c += 4) {
-        const float4 t = *reinterpret_cast<const float4*>(prow + q * SEG + c);
-        pr[c] = t.x; pr[c + 1] = t.y; pr[c + 2] = t.z; pr[c + 3] = t.w;
-      }
-      if (row == k) {
-#pragma unroll
-        for (int c = 0; c < SEG; ++c) r[c] = (q * SEG + c == k) ? ip : pr[c] * ip;
-      } else {
-        float f = fk;
-        if (row == p) {  // the displaced row k lands here
+          for (int w = 0; w < NW; ++w) {
+            const unsigned kw = wkey[b * NW + w];
+            if (kw > bk) { bk = kw; bw = w; }
+          }
+          const int p = wrow[b * NW + bw];
+          const float* prow = cand + (b * NW + bw) * NP;
+          const float piv = prow[k];
+          const float ip = __frcp_rn(piv);
+          if (tid == 0) {
+            perm[k] = p;
+            if (!(fabsf(piv) > thresh) || !isfinite(piv)) fail = true;
+          }
+          float pr[SEG];
 #pragma unroll
           for (int c = 0; c < SEG; c += 4) {
-            const float4 t = *reinterpret_cast<const float4*>(krow + q * SEG + c);
-            r[c] = t.x; r[c + 1] = t.y; r[c + 2] = t.z; r[c + 3] = t.w;
+            const float4 t = *reinterpret_cast<const float4*>(prow + q * SEG + c);
+            pr[c] = t.x; pr[c + 1] = t.y; pr[c + 2] = t.z; pr[c + 3] = t.w;
           }
-          f = krow[k];
-        }
-        const float fi = f * ip;
+          if (row == k) {
 #pragma unroll
-        for (int c = 0; c < SEG; ++c) r[c] = (q * SEG + c == k) ? -fi : fmaf(-fi, pr[c], r[c]);
+            for (int c = 0; c < SEG; ++c) r[c] = pr[c] * ip;
+            if (own) r[ck] = ip;
+          } else {
+            float f = fk;
+            if (row == p) {  // the displaced row k lands here
+#pragma unroll
+              for (int c = 0; c < SEG; c += 4) {
+                const float4 t = *reinterpret_cast<const float4*>(krow + b * NP + q * SEG + c);
+                r[c] = t.x; r[c + 1] = t.y; r[c + 2] = t.z; r[c + 3] = t.w;
+              }
+              f = krow[b * NP + k];
+            }
+            const float fi = f * ip;
+#pragma unroll
+            for (int c = 0; c < SEG; ++c) r[c] = fmaf(-fi, pr[c], r[c]);
+            if (own) r[ck] = -fi;
+          }
+        }
       }
     }
+    if (fail && tid == 0) misc[1] = 1.f;
   }
   __syncthreads();
   if (tid == 0) {  // undo the row interchanges as a column permutation, last to first

@@ -218,6 +218,66 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) Shat[e] = (float)Sh[e];
   double* Shd = L.Shat64 + st * m * n;
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) Shd[e] = Sh[e];
+
+  // fused leaf operator of the ADMM iteration (ctx.h): with X1 = rho Rinv D',
+  // om0 = Rinv r:  pv = (q - Sh' om0) + (rho C' - Sh' X1) w,  bv = (b - B om0) - B X1 w.
+  double* X1 = wk + 2 * kMaxM * (kMaxM + 1) + 8;  // m x c
+  double* om0 = X1 + m * c;                        // m
+  const double* rg = qp.r + st * m;
+  for (int e = threadIdx.x; e < m * c + m; e += blockDim.x) {
+    if (e < m * c) {
+      const int l = e / c, r = e - l * c;
+      double s = 0.0;
+      for (int t = 0; t < m; ++t) s = fma(Ri[l * m + t], Dst[r * m + t], s);
+      X1[e] = rho * s;
+    } else {
+      const int l = e - m * c;
+      double s = 0.0;
+      for (int t = 0; t < m; ++t) s = fma(Ri[l * m + t], rg[t], s);
+      om0[l] = s;
+    }
+  }
+  __syncthreads();
+  const int ld2n = L.ld2n, ldn = L.ldn, ldc = L.ldc;
+  float* X23 = L.X23 + st * (size_t)c * ld2n;
+  for (int e = threadIdx.x; e < c * ld2n; e += blockDim.x) {
+    const int r = e / ld2n, i = e - r * ld2n;
+    double v = 0.0;
+    if (i < n) {
+      double s = 0.0;
+      for (int l = 0; l < m; ++l) s = fma(Sh[l * n + i], X1[l * c + r], s);
+      v = rho * Cst[r * n + i] - s;
+    } else if (i < 2 * n) {
+      const int ii = i - n;
+      double s = 0.0;
+      for (int l = 0; l < m; ++l) s = fma(Bst[ii * m + l], X1[l * c + r], s);
+      v = -s;
+    }
+    X23[e] = (float)v;
+  }
+  const double* qg = qp.q + st * n;
+  const double* bg = qp.b + st * n;
+  double* pb0 = L.pb0 + st * 2 * n;
+  for (int i = threadIdx.x; i < 2 * n; i += blockDim.x) {
+    double s = 0.0;
+    if (i < n) {
+      for (int l = 0; l < m; ++l) s = fma(Sh[l * n + i], om0[l], s);
+      pb0[i] = qg[i] - s;
+    } else {
+      for (int l = 0; l < m; ++l) s = fma(Bst[(i - n) * m + l], om0[l], s);
+      pb0[i] = bg[i - n] - s;
+    }
+  }
+  float* Bcm = L.Bcm + st * (size_t)m * ldn;
+  for (int e = threadIdx.x; e < m * ldn; e += blockDim.x) {
+    const int j = e / ldn, i = e - j * ldn;
+    Bcm[e] = (i < n) ? (float)Bst[i * m + j] : 0.f;
+  }
+  float* Dcm = L.Dcm + st * (size_t)m * ldc;
+  for (int e = threadIdx.x; e < m * ldc; e += blockDim.x) {
+    const int j = e / ldc, i = e - j * ldc;
+    Dcm[e] = (i < c) ? (float)Dst[i * m + j] : 0.f;
+  }
 }
 
 // Matrix half of the CVF combine (Eq. 28) for one op per CTA; optionally
@@ -304,11 +364,12 @@ int matmul_threads(int n) {
 }
 
 // Gains, closed loop and COT leaves per stage (lqr.py:398-404, :349-356), in float64.
-__global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const int* list) {
+__global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const double* rho_arr, const int* list) {
   const int inst = inst_of(list);
   const int k = blockIdx.x;
-  const int n = L.n, m = L.m, N = L.N, ldg = L.ldg;
+  const int n = L.n, m = L.m, N = L.N, ldg = L.ldg, c = L.c;
   const size_t MS = (size_t)n * ldg;
+  const double rho = rho_arr ? rho_arr[inst] : 0.0;
   extern __shared__ double smd[];
   double* Bst = smd;             // n x m
   double* BtP = Bst + n * m;     // m x n
@@ -317,7 +378,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const int
   double* Ga = Gm + m * n;       // m x m
   double* Ks = Ga + m * m;       // m x n
   double* wk = Ks + m * n;
-  float* Abar = reinterpret_cast<float*>(wk + 2 * kMaxM * (kMaxM + 1) + 8);  // n x ldg (float)
+  float* Abar = reinterpret_cast<float*>(wk + 2 * kMaxM * (kMaxM + 1) + 8 + L.c * m + m);  // n x ldg (float)
   const size_t st = (size_t)inst * N + k;
   const float* Pn = L.Ps + ((size_t)inst * L.cvf_nslots + L.cvf_out[k + 1]) * MS;
   const float* Bg = qp.B + st * n * m;
@@ -384,6 +445,58 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const int
     Ad[e] = (k == 0) ? 0.f : (float)v;
     if (j < n) ATd[j * ldg + i] = (k == 0) ? 0.f : (float)v;
   }
+  // fused feedforward / constraint operators (ctx.h):
+  //   kf = kk0 + X5 p+ + X4 w with X5 = -Gamma B', X4 = -rho Gamma D', kk0 = -Gamma (B' cvec + r)
+  //   G  = Z dx + D kf with Z = C + D K
+  {
+    double* Dst = wk + 2 * kMaxM * (kMaxM + 1) + 8;  // c x m (Abar follows tk)
+    double* tk = Dst + c * m;                         // m
+    const float* Dg = qp.D + st * c * m;
+    for (int e = threadIdx.x; e < c * m; e += blockDim.x) Dst[e] = Dg[e];
+    __syncthreads();
+    const double* rg = qp.r + st * m;
+    for (int l = threadIdx.x; l < m; l += blockDim.x) {
+      double s = rg[l];
+      for (int i = 0; i < n; ++i) s = fma(Bst[i * m + l], cv[i], s);
+      tk[l] = s;
+    }
+    __syncthreads();
+    const int ldm = L.ldm, ldc = L.ldc;
+    float* X5 = L.X5 + st * (size_t)n * ldm;
+    for (int e = threadIdx.x; e < n * ldm; e += blockDim.x) {
+      const int i = e / ldm, l = e - i * ldm;
+      double s = 0.0;
+      if (l < m)
+        for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Bst[i * m + t], s);
+      X5[e] = (float)(-s);
+    }
+    float* X4 = L.X4 + st * (size_t)c * ldm;
+    for (int e = threadIdx.x; e < c * ldm; e += blockDim.x) {
+      const int r = e / ldm, l = e - r * ldm;
+      double s = 0.0;
+      if (l < m)
+        for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Dst[r * m + t], s);
+      X4[e] = (float)(-rho * s);
+    }
+    double* kk0 = L.kk0 + st * m;
+    for (int l = threadIdx.x; l < m; l += blockDim.x) {
+      double s = 0.0;
+      for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], tk[t], s);
+      kk0[l] = -s;
+    }
+    const float* Cg = qp.C + st * c * n;
+    float* Zcm = L.Zcm + st * (size_t)n * ldc;
+    for (int e = threadIdx.x; e < n * ldc; e += blockDim.x) {
+      const int i = e / ldc, r = e - i * ldc;
+      double v = 0.0;
+      if (r < c) {
+        double s = (double)Cg[r * n + i];
+        for (int l = 0; l < m; ++l) s = fma(Dst[r * m + l], Ks[l * n + i], s);
+        v = s;
+      }
+      Zcm[e] = (float)v;
+    }
+  }
   if (k == 0) {
     __syncthreads();
     const double* dx0 = qp.dx0 + (size_t)inst * n;
@@ -420,11 +533,12 @@ __global__ void __launch_bounds__(512) k_cot_combine(DevLqr L, const int4* ops, 
 // host driver
 
 static size_t leaf_smem_bytes(int n, int m, int c) {
-  return (size_t)(c * n + c * m + n * m + m * n + 2 * m * m + m * n + n * m + 2 * kMaxM * (kMaxM + 1) + 8) *
+  return (size_t)(c * n + c * m + n * m + m * n + 2 * m * m + m * n + n * m + 2 * kMaxM * (kMaxM + 1) + 8 + m * c + m) *
          sizeof(double);
 }
-static size_t gains_smem_bytes(int n, int m) {
-  return (size_t)(n * m + m * n + m * m + m * n + m * m + m * n + 2 * kMaxM * (kMaxM + 1) + 8) * sizeof(double) +
+static size_t gains_smem_bytes(int n, int m, int c) {
+  return (size_t)(n * m + m * n + m * m + m * n + m * m + m * n + 2 * kMaxM * (kMaxM + 1) + 8 + c * m + m) *
+             sizeof(double) +
          (size_t)n * ldg_of(n) * sizeof(float);
 }
 
@@ -479,11 +593,11 @@ int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_l
   if (N == 0) return GSLS_OK;
   // gains / COT leaves
   {
-    const size_t sb = gains_smem_bytes(n, d.nu);
+    const size_t sb = gains_smem_bytes(n, d.nu, d.nc);
     int rc = set_smem((const void*)k_gains, sb);
     if (rc) return rc;
     ProfScope ps(P_GAINS, st, (double)N * count);
-    k_gains<<<dim3(N, count), 256, sb, st>>>(L, *qp, d_list);
+    k_gains<<<dim3(N, count), 256, sb, st>>>(L, *qp, d_rho, d_list);
     GSLS_CUDA_CHECK(cudaGetLastError());
   }
   // COT tree
@@ -582,13 +696,24 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
   L.last_k = (double*)dev_alloc(c, B * N * m * 8);
   L.last_p = (double*)dev_alloc(c, B * (N + 1) * n * 8);
   L.err = (ErrSlot*)dev_alloc(c, B * sizeof(ErrSlot));
+  const size_t cc = d.nc;
+  L.ldm = ldg_of(d.nu); L.ldn = ldg_of(d.nx); L.ldc = ldg_of(std::max(1, d.nc)); L.ld2n = ldg_of(2 * d.nx);
+  L.X23 = (float*)dev_alloc(c, std::max<size_t>(1, B * N * cc * L.ld2n) * 4);
+  L.pb0 = (double*)dev_alloc(c, std::max<size_t>(1, B * N * 2 * n) * 8);
+  L.X5 = (float*)dev_alloc(c, std::max<size_t>(1, B * N * n * L.ldm) * 4);
+  L.X4 = (float*)dev_alloc(c, std::max<size_t>(1, B * N * cc * L.ldm) * 4);
+  L.kk0 = (double*)dev_alloc(c, std::max<size_t>(1, B * N * m) * 8);
+  L.Bcm = (float*)dev_alloc(c, std::max<size_t>(1, B * N * m * L.ldn) * 4);
+  L.Zcm = (float*)dev_alloc(c, std::max<size_t>(1, B * N * n * L.ldc) * 4);
+  L.Dcm = (float*)dev_alloc(c, std::max<size_t>(1, B * N * m * L.ldc) * 4);
   c->d_inst_all = (int*)dev_alloc(c, B * sizeof(int));
   c->d_inst_list = (int*)dev_alloc(c, B * sizeof(int));
   c->d_status = (int32_t*)dev_alloc(c, B * sizeof(int32_t));
   c->scratch_floats = replay_smem_floats(c);  // doubles
   if (c->scratch_floats * 8 > kReplaySmemMax) c->d_scratch = (double*)dev_alloc(c, B * c->scratch_floats * 8);
   bool fail = !L.Ps || !L.As || !L.Cs || !L.ATs || !L.cotAT || !L.cvf_rec || !L.cotA || !L.cot_rec || !L.Rhat || !L.Shat || !L.Shat64 || !L.Rinv ||
-              !L.Gamma || !L.K || !L.cvec || !L.v0 || !L.last_k || !L.last_p || !L.err || !c->d_inst_all || !c->d_inst_list || !c->d_status ||
+              !L.Gamma || !L.K || !L.cvec || !L.v0 || !L.last_k || !L.last_p || !L.err || !L.X23 || !L.pb0 || !L.X5 || !L.X4 || !L.kk0 ||
+              !L.Bcm || !L.Zcm || !L.Dcm || !c->d_inst_all || !c->d_inst_list || !c->d_status ||
               (c->scratch_floats * 8 > kReplaySmemMax && !c->d_scratch);
   if (fail) {
     for (void* p : c->allocs) cudaFree(p);
