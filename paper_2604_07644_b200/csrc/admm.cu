@@ -18,10 +18,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "ctx.h"
 #include "prof.h"
+#include "cluster.cuh"
 
 namespace gsls {
 
@@ -151,57 +153,9 @@ __device__ inline void write_last(const DevLqr& L, int inst, const double* kf, c
   }
 }
 
-// ---- thread-block-cluster plumbing ---------------------------------------------
-// A replay instance runs on a cluster of CS CTAs (CS = 1 for large batches).
-// Every CTA holds a full replica of the replay vectors in its shared memory;
-// each phase's outputs are written to all replicas (DSMEM stores) and phases
-// are separated by cluster barriers, so every read is CTA-local.
-
-__device__ inline unsigned cluster_rank() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ inline unsigned cluster_size() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-  return r;
-}
-__device__ inline void st_remote(const double* local, unsigned rank, double v) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(local);
-  unsigned ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
-  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
-}
-
-struct Cl {
-  unsigned rank, cs;
-  __device__ void put(double* p, double v) const {  // write v to p in every replica
-    *p = v;
-    for (unsigned r = 0; r < cs; ++r)
-      if (r != rank) st_remote(p, r, v);
-  }
-  __device__ void put_mask(double* p, double v, unsigned mask) const {  // local + consumer replicas
-    *p = v;
-    mask &= ~(1u << rank);
-    while (mask) {
-      const unsigned r = __ffs(mask) - 1;
-      mask &= mask - 1;
-      st_remote(p, r, v);
-    }
-  }
-  __device__ void sync() const {
-    if (cs == 1) {
-      __syncthreads();
-    } else {
-      asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    }
-  }
-};
-
 // Partial column-major matvec over k in [k0, k1) for one 32-row block: lanes
 // with g == 0 return the sums of rows 32rb + 4rq .. +3 (see warp_cm_matvec).
-__device__ __noinline__ void warp_cm_partial(const float* __restrict__ Mcm, int ldg, int rb, const double* x, int k0,
+__device__ inline void warp_cm_partial(const float* __restrict__ Mcm, int ldg, int rb, const double* x, int k0,
                                        int k1, double (&acc)[4]) {
   const int lane = threadIdx.x & 31;
   const int rq = lane & 7, g = lane >> 3;
@@ -234,7 +188,7 @@ __device__ __noinline__ void warp_cm_partial(const float* __restrict__ Mcm, int 
 // (rq, g): rows 4rq..4rq+3 of the block as one 16-byte load per column, k =
 // g, g + 32/RQ, ...  Lanes with g == 0 return the sums.
 template <int RQ>
-__device__ __noinline__ void warp_stage_mv(const float* __restrict__ M, int ld, int rb, const double* x, int klen,
+__device__ inline void warp_stage_mv(const float* __restrict__ M, int ld, int rb, const double* x, int klen,
                                      const float* __restrict__ M2, const double* x2, int klen2, double (&acc)[4]) {
   constexpr int KG = 32 / RQ;
   const int lane = threadIdx.x & 31;
@@ -422,12 +376,10 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
   const double* dx0 = a.qp.dx0 + (size_t)inst * n;
   const float* X23 = L.X23 + sN * c * L.ld2n;
   const double* pb0 = L.pb0 + sN * 2 * n;
-  const float* X5 = L.X5 + sN * n * L.ldm;
-  const float* X4 = L.X4 + sN * c * L.ldm;
+  const float* XK = L.XK + sN * (n + c) * L.ldm;
   const double* kk0 = L.kk0 + sN * m;
   const float* Bcm = L.Bcm + sN * m * L.ldn;
-  const float* Zcm = L.Zcm + sN * n * L.ldc;
-  const float* Dcm = L.Dcm + sN * m * L.ldc;
+  const float* ZD = L.ZD + sN * (n + m) * L.ldc;
   const int warp = tid >> 5, lane = tid & 31, nwarp = nthr >> 5;
 
   double* w = vs + V.w;
@@ -601,8 +553,9 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
       for (int t = warp; t < nls * RBm; t += nwarp) {
         const int k = rank + (t / RBm) * cs, rb = t % RBm;
         double acc[4];
-        warp_stage_mv<4>(X5 + (size_t)k * n * L.ldm, L.ldm, rb, pv + (size_t)s_cvf_out[k + 1] * n, n,
-                         X4 + (size_t)k * c * L.ldm, w + k * c, c, acc);
+        const float* xk_ = XK + (size_t)k * (n + c) * L.ldm;
+        warp_stage_mv<4>(xk_, L.ldm, rb, pv + (size_t)s_cvf_out[k + 1] * n, n, xk_ + (size_t)n * L.ldm, w + k * c, c,
+                         acc);
         if (lane < 4) {
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
@@ -720,8 +673,8 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
       for (int t = warp; t < nls * RBc; t += nwarp) {
         const int k = rank + (t / RBc) * cs, rb = t % RBc;
         double acc[4];
-        warp_stage_mv<8>(Zcm + (size_t)k * n * L.ldc, L.ldc, rb, dxp(k), n, Dcm + (size_t)k * m * L.ldc,
-                         kf + k * m, m, acc);
+        const float* zd_ = ZD + (size_t)k * (n + m) * L.ldc;
+        warp_stage_mv<8>(zd_, L.ldc, rb, dxp(k), n, zd_ + (size_t)n * L.ldc, kf + k * m, m, acc);
         if (lane < 8) {
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
@@ -830,6 +783,551 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
   }
 }
 
+// ===========================================================================
+// Staged ADMM replay (TMA-fed).
+//
+// The per-iteration matrix stream of an instance is static: the fused stage
+// operators and the recorded scan matrices, in phase order.  Each CTA builds
+// its own ordered item list once (the items of the stages / ops it owns) and
+// streams the items through a ring of R shared-memory slots with 1-D bulk
+// copies (cp.async.bulk, mbarrier complete_tx), R items ahead of the
+// consumers, across phase and iteration boundaries.  Every matvec then reads
+// shared memory only; the loads of the next items overlap the current
+// phase's arithmetic, barriers and DSMEM exchanges.  All 16 warps work on one
+// item at a time (row blocks x k-slices, partial sums combined in a fixed
+// order), so an item costs two CTA barriers.
+//
+// Vectors are the replay vectors of k_replay with physical slot compression
+// (plan.h compress_slots); y is not stored (y = lambda / rho after every
+// ascent, admm.py:134).
+// ===========================================================================
+
+enum { IT_P1 = 0, IT_CVF1, IT_CVF2, IT_FF1, IT_FF2, IT_COT, IT_G };
+
+struct StagedLayout {
+  // byte offsets into dynamic shared memory
+  int ring, pv, bv, cb, t1, t2, z, lam, y, w, kf, dx0, part, red, redall, masks, ops, phys, items, phase, mbar, total;
+  int slot;  // bytes per ring slot
+  int R;     // ring slots
+  int max_items, nphase;
+};
+
+__host__ __device__ inline int stage_slot_bytes(int n, int m, int c, int ld2n, int ldm, int ldn, int ldc, int ldg) {
+  int b = n * ldg;                      // recorded n x n matrix
+  b = b > c * ld2n ? b : c * ld2n;      // X23
+  b = b > (n + c) * ldm ? b : (n + c) * ldm;
+  b = b > m * ldn ? b : m * ldn;
+  b = b > (n + m) * ldc ? b : (n + m) * ldc;
+  return ((b * 4 + 127) / 128) * 128;
+}
+
+__host__ __device__ inline StagedLayout staged_layout(const DevLqr& L, int max_layer, int R) {
+  StagedLayout S{};
+  const int n = L.n, m = L.m, N = L.N;
+  int o = 0;
+  auto take = [&](int bytes, int align) { o = (o + align - 1) / align * align; int r = o; o += bytes; return r; };
+  S.slot = stage_slot_bytes(n, m, L.c, L.ld2n, L.ldm, L.ldn, L.ldc, L.ldg);
+  S.R = R;
+  S.ring = take(S.slot * R, 128);
+  S.pv = take(L.cvf_nphys * n * 8, 16);
+  S.bv = take(L.cvf_nphys * n * 8, 16);
+  S.cb = take(L.cot_nphys * n * 8, 16);
+  S.t1 = take(max_layer * n * 8, 16);
+  S.t2 = take(max_layer * n * 8, 16);
+  S.z = take(L.mtot * 8, 16);
+  S.lam = take(L.mtot * 8, 16);
+  S.y = take(L.mtot * 8, 16);
+  S.w = take(L.mtot * 8, 16);
+  S.kf = take(N * m * 8, 16);
+  S.dx0 = take(n * 8, 16);
+  S.part = take(kReplayThreads * 8, 16);
+  S.red = take(64 * 8, 16);
+  S.redall = take(2 * kMaxCluster * 8, 16);
+  S.masks = take((L.cvf_nslots + L.cot_nslots) * 4, 16);
+  S.ops = take((L.cvf_nops + L.cot_nops) * 16 + (L.cvf_layers + L.cot_layers + 2 + 2 * N + 2) * 4, 16);
+  S.phys = take((L.cvf_nslots + L.cot_nslots) * 4, 16);
+  S.max_items = 4 * N + 4 * L.cvf_nops + L.cot_nops + 8;
+  S.items = take(S.max_items * 8, 16);
+  S.nphase = 2 * L.cvf_layers + L.cot_layers + 5;
+  S.phase = take((S.nphase + 1) * 4, 16);
+  S.mbar = take(R * 8, 8);
+  S.total = o;
+  return S;
+}
+
+__device__ inline void mbar_init(uint64_t* bar, unsigned count) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(count) : "memory");
+}
+__device__ inline void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(b),
+      "r"(parity)
+      : "memory");
+}
+__device__ inline void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+
+enum { E_SET = 0, E_PUT, E_P1, E_KF, E_CB, E_G };
+
+// Epilogue of one item: what thread i < rows does with its row sum s.
+struct ItemEpi {
+  int kind;
+  double* dst;         // output vector (E_P1: the p leaf)
+  double* dst2;        // E_P1: the b leaf
+  const double* add;   // shared-memory addend (E_SET, E_PUT)
+  const double* pre;   // global addend, loaded before the wait (E_P1, E_KF, E_CB, E_G: f)
+  const double* pre2;  // second global addend (E_CB at k = 0: Abar_0 dx0)
+  double sgn;
+  unsigned mask;       // consumer ranks (E_PUT, E_P1, E_CB)
+  int e0;              // E_G: first stacked constraint row of the stage
+};
+
+__global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a, int R) {
+  const DevLqr& L = a.L;
+  const int inst = a.list ? a.list[blockIdx.y] : (int)blockIdx.y;
+  const int n = L.n, m = L.m, c = L.c, nf = L.nf, N = L.N, ldg = L.ldg, mtot = L.mtot;
+  const size_t MS = (size_t)n * ldg;
+  const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31, nwarp = nthr >> 5;
+  Cl cl;
+  cl.rank = cluster_rank();
+  cl.cs = cluster_size();
+  const int rank = (int)cl.rank, cs = (int)cl.cs;
+  const StagedLayout SL = staged_layout(L, a.max_layer, R);
+  extern __shared__ __align__(128) unsigned char smb[];
+  unsigned char* ring = smb + SL.ring;
+  double* pv = reinterpret_cast<double*>(smb + SL.pv);
+  double* bv = reinterpret_cast<double*>(smb + SL.bv);
+  double* cb = reinterpret_cast<double*>(smb + SL.cb);
+  double* t1 = reinterpret_cast<double*>(smb + SL.t1);
+  double* t2 = reinterpret_cast<double*>(smb + SL.t2);
+  double* z = reinterpret_cast<double*>(smb + SL.z);
+  double* lam = reinterpret_cast<double*>(smb + SL.lam);
+  double* y = reinterpret_cast<double*>(smb + SL.y);
+  double* w = reinterpret_cast<double*>(smb + SL.w);
+  double* kf = reinterpret_cast<double*>(smb + SL.kf);
+  double* dx0s = reinterpret_cast<double*>(smb + SL.dx0);
+  double* part = reinterpret_cast<double*>(smb + SL.part);
+  double* red = reinterpret_cast<double*>(smb + SL.red);
+  double* redall = reinterpret_cast<double*>(smb + SL.redall);
+  unsigned* cvf_mask = reinterpret_cast<unsigned*>(smb + SL.masks);
+  unsigned* cot_mask = cvf_mask + L.cvf_nslots;
+  int4* s_cvf_ops = reinterpret_cast<int4*>(smb + SL.ops);
+  int4* s_cot_ops = s_cvf_ops + L.cvf_nops;
+  int* s_cvf_loff = reinterpret_cast<int*>(s_cot_ops + L.cot_nops);
+  int* s_cot_loff = s_cvf_loff + L.cvf_layers + 1;
+  int* s_cvf_out = s_cot_loff + L.cot_layers + 1;
+  int* s_cot_out = s_cvf_out + N + 1;
+  int* cvf_phys = reinterpret_cast<int*>(smb + SL.phys);
+  int* cot_phys = cvf_phys + L.cvf_nslots;
+  int2* items = reinterpret_cast<int2*>(smb + SL.items);  // (kind | which << 8, index)
+  int* phase_off = reinterpret_cast<int*>(smb + SL.phase);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smb + SL.mbar);
+  __shared__ int s_flag, s_nitems;
+  __shared__ double s_rho;
+
+  // ---- one-time setup: plan, physical slots, consumer masks, item list ------------
+  for (int i = tid; i < L.cvf_nops; i += nthr) s_cvf_ops[i] = L.cvf_ops[i];
+  for (int i = tid; i < L.cot_nops; i += nthr) s_cot_ops[i] = L.cot_ops[i];
+  for (int i = tid; i <= L.cvf_layers; i += nthr) s_cvf_loff[i] = L.cvf_loff[i];
+  for (int i = tid; i <= L.cot_layers; i += nthr) s_cot_loff[i] = (N > 0) ? L.cot_loff[i] : 0;
+  for (int i = tid; i <= N; i += nthr) s_cvf_out[i] = L.cvf_out[i];
+  for (int i = tid; i < N; i += nthr) s_cot_out[i] = L.cot_out[i];
+  for (int i = tid; i < L.cvf_nslots; i += nthr) cvf_phys[i] = L.cvf_phys[i];
+  for (int i = tid; i < L.cot_nslots; i += nthr) cot_phys[i] = L.cot_phys[i];
+  for (int i = tid; i < L.cvf_nslots + L.cot_nslots; i += nthr) cvf_mask[i] = 0u;
+  if (tid < R) mbar_init(full + tid, 1);
+  __syncthreads();
+  auto srank = [&](int k) { return k % cs; };
+  if (cs > 1) {
+    for (int lay = 0; lay < L.cvf_layers; ++lay) {
+      const int o0 = s_cvf_loff[lay], no = s_cvf_loff[lay + 1] - o0, per = (no + cs - 1) / cs;
+      for (int oi = tid; oi < no; oi += nthr) {
+        const int4 op = s_cvf_ops[o0 + oi];
+        atomicOr(cvf_mask + op.y, 1u << (oi / per));
+        atomicOr(cvf_mask + op.z, 1u << (oi / per));
+      }
+    }
+    for (int p = tid; p <= N; p += nthr) atomicOr(cvf_mask + s_cvf_out[p], 1u << srank(max(p - 1, 0)));
+    for (int lay = 0; lay < L.cot_layers; ++lay) {
+      const int o0 = s_cot_loff[lay], no = s_cot_loff[lay + 1] - o0, per = (no + cs - 1) / cs;
+      for (int oi = tid; oi < no; oi += nthr) {
+        const int4 op = s_cot_ops[o0 + oi];
+        atomicOr(cot_mask + op.y, 1u << (oi / per));
+        atomicOr(cot_mask + op.z, 1u << (oi / per));
+      }
+    }
+    for (int k = 1 + tid; k <= N; k += nthr) atomicOr(cot_mask + s_cot_out[k - 1], 1u << srank(k));
+  }
+  if (tid == 0) {  // this rank's items in consumption order, phase by phase
+    int ni = 0, ph = 0;
+    auto add = [&](int kind, int which, int idx, int loc = 0) {
+      items[ni++] = make_int2(kind | (which << 8) | (loc << 16), idx);
+    };
+    phase_off[ph++] = ni;
+    for (int k = rank; k < N; k += cs) add(IT_P1, 0, k);
+    for (int lay = 0; lay < L.cvf_layers; ++lay) {
+      const int o0 = s_cvf_loff[lay], no = s_cvf_loff[lay + 1] - o0, per = (no + cs - 1) / cs;
+      const int lo = min(no, rank * per), hi = min(no, lo + per);
+      phase_off[ph++] = ni;
+      for (int oi = lo; oi < hi; ++oi) { add(IT_CVF1, 0, o0 + oi, oi - lo); add(IT_CVF1, 1, o0 + oi, oi - lo); }
+      phase_off[ph++] = ni;
+      for (int oi = lo; oi < hi; ++oi) { add(IT_CVF2, 0, o0 + oi, oi - lo); add(IT_CVF2, 1, o0 + oi, oi - lo); }
+    }
+    phase_off[ph++] = ni;
+    for (int k = rank; k < N; k += cs) add(IT_FF1, 0, k);
+    phase_off[ph++] = ni;
+    for (int k = rank; k < N; k += cs) add(IT_FF2, 0, k);
+    for (int lay = 0; lay < L.cot_layers; ++lay) {
+      const int o0 = s_cot_loff[lay], no = s_cot_loff[lay + 1] - o0, per = (no + cs - 1) / cs;
+      const int lo = min(no, rank * per), hi = min(no, lo + per);
+      phase_off[ph++] = ni;
+      for (int oi = lo; oi < hi; ++oi) add(IT_COT, 0, o0 + oi);
+    }
+    phase_off[ph++] = ni;
+    for (int k = rank; k < N; k += cs) add(IT_G, 0, k);
+    phase_off[ph] = ni;
+    s_nitems = ni;
+  }
+  // fence: mbarrier inits visible to the async proxy before the first bulk copy
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const int P = s_nitems;
+
+  // ---- instance data --------------------------------------------------------------
+  const size_t sN = (size_t)inst * N;
+  const double* bq = a.qp.b + sN * n;
+  const float* CNq = a.qp.CN + (size_t)inst * nf * n;
+  const double* qN_lin = a.qp.qN + (size_t)inst * n;
+  const float* Kg = L.K + sN * m * n;
+  const double* v0 = L.v0 + (size_t)inst * n;
+  const float* cvf_rec = L.cvf_rec + (size_t)inst * L.cvf_nops * 4 * MS;
+  const float* cot_rec = L.cot_rec + (size_t)inst * L.cot_nops * MS;
+  const float* X23 = L.X23 + sN * c * L.ld2n;
+  const double* pb0 = L.pb0 + sN * 2 * n;
+  const float* XK = L.XK + sN * (n + c) * L.ldm;
+  const double* kk0 = L.kk0 + sN * m;
+  const float* Bcm = L.Bcm + sN * m * L.ldn;
+  const float* ZD = L.ZD + sN * (n + m) * L.ldc;
+  const double* fst = a.qp.f + sN * c;
+  const double* fN = a.qp.fN + (size_t)inst * nf;
+  auto PV = [&](int s) { return pv + (size_t)cvf_phys[s] * n; };
+  auto BV = [&](int s) { return bv + (size_t)cvf_phys[s] * n; };
+  auto CB = [&](int s) { return cb + (size_t)cot_phys[s] * n; };
+  auto dxp = [&](int k) -> const double* { return k == 0 ? dx0s : CB(s_cot_out[k - 1]); };
+
+  // ---- item stream ---------------------------------------------------------------------
+  int pi = 0, pslot = 0;  // producer (thread 0): next item (mod P), slot to fill
+  auto issue = [&]() {
+    if (tid != 0 || P == 0) return;
+    const int2 itm = items[pi];
+    const int kind = itm.x & 0xff, which = (itm.x >> 8) & 0xff, idx = itm.y;
+    const float* src;
+    unsigned bytes;
+    switch (kind) {
+      case IT_P1: bytes = c * L.ld2n * 4; src = X23 + (size_t)idx * c * L.ld2n; break;
+      case IT_CVF1: bytes = (unsigned)MS * 4; src = cvf_rec + ((size_t)idx * 4 + (which ? 3 : 1)) * MS; break;
+      case IT_CVF2: bytes = (unsigned)MS * 4; src = cvf_rec + ((size_t)idx * 4 + (which ? 2 : 0)) * MS; break;
+      case IT_FF1: bytes = (n + c) * L.ldm * 4; src = XK + (size_t)idx * (n + c) * L.ldm; break;
+      case IT_FF2: bytes = m * L.ldn * 4; src = Bcm + (size_t)idx * m * L.ldn; break;
+      case IT_COT: bytes = (unsigned)MS * 4; src = cot_rec + (size_t)idx * MS; break;
+      default: bytes = (n + m) * L.ldc * 4; src = ZD + (size_t)idx * (n + m) * L.ldc; break;
+    }
+    bulk_load(ring + (size_t)pslot * SL.slot, src, bytes, full + pslot);
+    if (++pi == P) pi = 0;
+    if (++pslot == R) pslot = 0;
+  };
+  for (int i = 0; i < R; ++i) issue();
+
+  double rho = a.state.rho[inst];
+  int it = a.stats.iterations[inst];
+  {
+    const double* zg = a.state.z + (size_t)inst * mtot;
+    const double* lg = a.state.lam + (size_t)inst * mtot;
+    const double* yg = a.state.y + (size_t)inst * mtot;
+    for (int e = tid; e < mtot; e += nthr) {
+      z[e] = zg[e];
+      lam[e] = lg[e];
+      y[e] = yg[e];
+      w[e] = yg[e] - zg[e];
+    }
+    for (int i = tid; i < n; i += nthr) dx0s[i] = a.qp.dx0[(size_t)inst * n + i];
+  }
+  cl.sync();  // every replica exists before the first remote store
+
+  int cslot = 0, cpar = 0, ph2 = 0;  // consumer: slot, mbarrier parity, partial-sum half
+  const int nph = 2 * L.cvf_layers + L.cot_layers + 4;  // P1, CVF rounds, FF1, FF2, COT layers, G
+  const int ph_ff1 = 2 * L.cvf_layers + 1, ph_g = nph - 1;
+
+  for (;;) {
+    double rp = 0.0, rdz = 0.0;
+    int j = 0;
+    for (int ph = 0; ph < nph; ++ph) {
+      // ---- the phase's items: one matvec each, read from the ring; the item code is
+      //      specialised per kind (compile-time) so each phase runs only its own path ----
+      auto run_item = [&](auto kind_c) {
+        constexpr int kind = decltype(kind_c)::value;
+        const int2 itm = items[j];
+        const int which = (itm.x >> 8) & 0xff, loc = itm.x >> 16, idx = itm.y;
+        // operands: rows x (K1 + K2) matrix (leading dimension ld), x = [x1; x2]
+        int rows = n, ld = ldg, K1 = n, K2 = 0, ek = E_SET;
+        const double *x1 = nullptr, *x2 = nullptr, *add = nullptr, *pre = nullptr, *pre2 = nullptr;
+        double *dst = nullptr, *dst2 = nullptr, sgn = 1.0;
+        unsigned mk = 0u;
+        if constexpr (kind == IT_P1) {  //   // [p; b]_k = pb0_k + X23_k w_k (fused leaves, admm.py:113-121, lqr.py:338-342)
+            rows = 2 * n; ld = L.ld2n; K1 = c; x1 = w + idx * c; ek = E_P1;
+            dst = PV(idx); dst2 = BV(idx); pre = pb0 + (size_t)idx * 2 * n; mk = cvf_mask[idx];
+        } else if constexpr (kind == IT_CVF1) {  // t1 = p_later + Pr b_earlier | t2 = b_earlier - Cl p_later (lqr.py:244-246)
+            const int4 op = s_cvf_ops[idx];
+            x1 = which ? PV(op.z) : BV(op.y);
+            add = which ? BV(op.y) : PV(op.z);
+            dst = (which ? t2 : t1) + loc * n;
+            sgn = which ? -1.0 : 1.0;
+        } else if constexpr (kind == IT_CVF2) {  // p = Ups t1 + p_earlier | b = Psi t2 + b_later
+            const int4 op = s_cvf_ops[idx];
+            x1 = (which ? t2 : t1) + loc * n;
+            add = which ? BV(op.z) : PV(op.y);
+            dst = which ? BV(op.x) : PV(op.x);
+            ek = E_PUT; mk = cvf_mask[op.x];
+        } else if constexpr (kind == IT_FF1) {  // kf = kk0 + [X5 X4] [p+; w] (lqr.py:345-346)
+            rows = m; ld = L.ldm; K1 = n; x1 = PV(s_cvf_out[idx + 1]); K2 = c; x2 = w + idx * c;
+            ek = E_KF; dst = kf + idx * m; pre = kk0 + (size_t)idx * m;
+        } else if constexpr (kind == IT_FF2) {  // COT leaf b = B kf + b (+ Abar_0 dx0) (lqr.py:349-356)
+            rows = n; ld = L.ldn; K1 = m; x1 = kf + idx * m;
+            ek = E_CB; dst = CB(idx); pre = bq + (size_t)idx * n; pre2 = (idx == 0) ? v0 : nullptr;
+            mk = cot_mask[idx];
+        } else if constexpr (kind == IT_COT) {  // b = A_later b_earlier + b_later (lqr.py:281-285)
+            const int4 op = s_cot_ops[idx];
+            x1 = CB(op.y); add = CB(op.z); dst = CB(op.x); ek = E_PUT; mk = cot_mask[op.x];
+        } else {  // G = [Z D] [dx; kf] = C dx + D du, then the projection (admm.py:91-97)
+            rows = c; ld = L.ldc; K1 = n; x1 = dxp(idx); K2 = m; x2 = kf + idx * m;
+            ek = E_G; pre = fst + (size_t)idx * c;
+        }
+        double pre_v = 0.0;
+        if (tid < rows && pre) pre_v = pre[tid] + (pre2 ? pre2[tid] : 0.0);
+        mbar_wait(full + cslot, (unsigned)cpar);
+        const float* M = reinterpret_cast<const float*>(ring + (size_t)cslot * SL.slot);
+        double* pt = part + ph2 * (kReplayThreads / 2);
+        const int RB = (rows + 31) >> 5, K = K1 + K2;
+        const int KS = max(1, (nwarp / 2) / RB);  // one partial half: <= 8 (row block, slice) tasks
+        const int kc = (((K + KS - 1) / KS) + 3) & ~3;
+        for (int t = warp; t < RB * KS; t += nwarp) {
+          const int rb = t / KS, ks = t - rb * KS;
+          const int rq = lane & 7, gq = lane >> 3;
+          const int row0 = rb * 32 + 4 * rq;
+          const int k0 = ks * kc, k1 = min(K, k0 + kc);
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          if (row0 < ld) {
+#pragma unroll 4
+            for (int k = k0 + gq; k < k1; k += 4) {
+              const float4 v = *reinterpret_cast<const float4*>(M + (size_t)k * ld + row0);
+              const double xk = (k < K1) ? x1[k] : x2[k - K1];
+              a0 = fma((double)v.x, xk, a0);
+              a1 = fma((double)v.y, xk, a1);
+              a2 = fma((double)v.z, xk, a2);
+              a3 = fma((double)v.w, xk, a3);
+            }
+          }
+#pragma unroll
+          for (int o = 8; o <= 16; o <<= 1) {
+            a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+            a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+            a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+            a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+          }
+          if (gq == 0) {
+            double* pp = pt + (rb * KS + ks) * 32 + 4 * rq;
+            pp[0] = a0; pp[1] = a1; pp[2] = a2; pp[3] = a3;
+          }
+        }
+        // One barrier per item: the slot is refilled right after it and the partial
+        // sums alternate halves, so this epilogue overlaps the next item.
+        __syncthreads();
+        issue();
+        if (++cslot == R) { cslot = 0; cpar ^= 1; }
+        ph2 ^= 1;
+        if (tid < rows) {
+          const int rb = tid >> 5, ro = tid & 31;
+          double sum = 0.0;
+          for (int ks = 0; ks < KS; ++ks) sum += pt[(rb * KS + ks) * 32 + ro];
+          const int i = tid;
+          if constexpr (kind == IT_CVF1) {
+            dst[i] = add[i] + sgn * sum;
+          } else if constexpr (kind == IT_CVF2 || kind == IT_COT) {
+            cl.put_mask(dst + i, add[i] + sum, mk);
+          } else if constexpr (kind == IT_P1) {
+            cl.put_mask(i < n ? dst + i : dst2 + (i - n), pre_v + sum, mk);
+          } else if constexpr (kind == IT_FF1) {
+            dst[i] = pre_v + sum;
+          } else if constexpr (kind == IT_FF2) {
+            cl.put_mask(dst + i, pre_v + sum, mk);
+          } else {  // z = min(G + y, f); lam += rho (G - z); y = lam / rho (admm.py:130-135)
+            {
+              const int e = idx * c + i;
+              const double zo = z[e];
+              const double zn = fmin(sum + y[e], pre_v);
+              const double ln = lam[e] + rho * (sum - zn);
+              const double yn = ln / rho;
+              lam[e] = ln;
+              y[e] = yn;
+              z[e] = zn;
+              w[e] = yn - zn;
+              rp = fmax(rp, fabs(sum - zn));
+              rdz = fmax(rdz, fabs(zn - zo));
+            }
+          }
+        }
+      };
+      const int kind_ph = (ph == 0) ? IT_P1 : (ph <= 2 * L.cvf_layers) ? ((ph & 1) ? IT_CVF1 : IT_CVF2)
+                        : (ph == ph_ff1) ? IT_FF1 : (ph == ph_ff1 + 1) ? IT_FF2 : (ph == ph_g) ? IT_G : IT_COT;
+      for (; j < phase_off[ph + 1]; ++j) {
+        switch (kind_ph) {
+          case IT_P1: run_item(std::integral_constant<int, IT_P1>{}); break;
+          case IT_CVF1: run_item(std::integral_constant<int, IT_CVF1>{}); break;
+          case IT_CVF2: run_item(std::integral_constant<int, IT_CVF2>{}); break;
+          case IT_FF1: run_item(std::integral_constant<int, IT_FF1>{}); break;
+          case IT_FF2: run_item(std::integral_constant<int, IT_FF2>{}); break;
+          case IT_COT: run_item(std::integral_constant<int, IT_COT>{}); break;
+          default: run_item(std::integral_constant<int, IT_G>{}); break;
+        }
+      }
+      // ---- phase boundary -----------------------------------------------------------
+      if (ph == 0) {  // terminal leaf (qN + rho CN' w_N, 0) on its owner
+        if (rank == srank(N))
+          for (int i = tid; i < n; i += nthr) {
+            double sum = 0.0;
+            for (int f = 0; f < nf; ++f) sum = fma((double)CNq[f * n + i], w[N * c + f], sum);
+            cl.put_mask(PV(N) + i, qN_lin[i] + rho * sum, cvf_mask[N]);
+            cl.put_mask(BV(N) + i, 0.0, cvf_mask[N]);
+          }
+        cl.sync();
+      } else if (ph == ph_g) {  // terminal constraint rows on their owner
+        if (rank == srank(N))
+          for (int f = tid; f < nf; f += nthr) {
+            const double* xN = dxp(N);
+            double sum = 0.0;
+            for (int i = 0; i < n; ++i) sum = fma((double)CNq[f * n + i], xN[i], sum);
+            const int e = N * c + f;
+            const double zo = z[e];
+            const double zn = fmin(sum + y[e], fN[f]);
+            const double ln = lam[e] + rho * (sum - zn);
+            const double yn = ln / rho;
+            lam[e] = ln;
+            y[e] = yn;
+            z[e] = zn;
+            w[e] = yn - zn;
+            rp = fmax(rp, fabs(sum - zn));
+            rdz = fmax(rdz, fabs(zn - zo));
+          }
+      } else if ((ph <= 2 * L.cvf_layers && (ph & 1)) || ph == ph_ff1) {
+        __syncthreads();  // t1 / t2 or kf complete (CTA-local)
+      } else {
+        cl.sync();  // CVF round 2, FF2, COT layers: remote consumers
+      }
+    }
+    const double rpb = block_max_d(rp, red);
+    const double rdb = block_max_d(rdz, red + 32);
+    if (tid == 0) {
+      cl.put(redall + 2 * rank, rpb);
+      cl.put(redall + 2 * rank + 1, rdb);
+    }
+    cl.sync();
+    if (tid == 0) {
+      double r_p = 0.0, r_dz = 0.0;
+      for (int r = 0; r < cs; ++r) {
+        r_p = fmax(r_p, redall[2 * r]);
+        r_dz = fmax(r_dz, redall[2 * r + 1]);
+      }
+      ++it;
+      const double r_d = rho * r_dz;
+      const bool lead = rank == 0;
+      if (lead) {
+        a.state.iteration[inst] += 1;
+        a.state.r_primal[inst] = r_p;
+        a.state.r_dual[inst] = r_d;
+      }
+      int flag = 0;
+      double rho_new = rho;
+      if (r_p <= a.set.tol_primal && r_d <= a.set.tol_dual) {
+        if (lead) a.stats.converged[inst] = 1;
+        flag = 1;
+      } else {
+        bool changed = false;
+        if (it % a.set.sigma == 0) {
+          const double ratio = sqrt(fmax(r_p, 1e-30) / fmax(r_d, 1e-30));
+          const double prop = fmin(fmax(rho * ratio, a.set.rho_min), a.set.rho_max);
+          if (prop > 5.0 * rho || prop < rho / 5.0) {
+            rho_new = prop;
+            if (lead) {
+              a.state.rho[inst] = prop;
+              a.state.generation[inst] += 1;
+              a.stats.rho_changes[inst] += 1;
+            }
+            changed = true;
+          }
+        }
+        if (it >= a.set.max_iter) flag = 1;
+        else if (changed) flag = 2;
+      }
+      if (lead) a.stats.iterations[inst] = it;
+      s_flag = flag;
+      s_rho = rho_new;
+    }
+    __syncthreads();
+    const int flag = s_flag;
+    if (flag == 0) continue;
+
+    // ---- exit: drain the in-flight bulk copies, write back what this rank owns -------
+    if (P > 0)  // the R in-flight copies land in slots cslot, cslot + 1, ... in order
+      for (int q = 0, sl = cslot, pa = cpar; q < R; ++q) {
+        mbar_wait(full + sl, (unsigned)pa);
+        if (++sl == R) { sl = 0; pa ^= 1; }
+      }
+    const double rho_new = s_rho;
+    auto owns_row = [&](int e) { return srank(e < N * c ? e / c : N) == rank; };
+    double* zg = a.state.z + (size_t)inst * mtot;
+    double* lg = a.state.lam + (size_t)inst * mtot;
+    double* yg = a.state.y + (size_t)inst * mtot;
+    for (int e = tid; e < mtot; e += nthr)
+      if (owns_row(e)) {
+        zg[e] = z[e];
+        lg[e] = lam[e];
+        yg[e] = (rho_new != rho) ? lam[e] / rho_new : y[e];  // a committed change rescales y (admm.py:149)
+      }
+    if (flag == 1) {
+      double* gdx = a.dx + (size_t)inst * (N + 1) * n;
+      double* gdu = a.du + (size_t)inst * N * m;
+      for (int e = tid; e < (N + 1) * n; e += nthr) {
+        const int p = e / n, i = e - p * n;
+        if ((p == 0 ? 0 : srank(p)) == rank) gdx[e] = dxp(p)[i];
+        if (srank(max(p - 1, 0)) == rank) L.last_p[(size_t)inst * (N + 1) * n + e] = PV(s_cvf_out[p])[i];
+      }
+      for (int e = tid; e < N * m; e += nthr) {  // du = K dx + k (lqr.py:359-363), once at exit
+        const int k = e / m;
+        if (srank(k) != rank) continue;
+        const double* xk = dxp(k);
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s = fma((double)Kg[(size_t)e * n + i], xk[i], s);
+        gdu[e] = s + kf[e];
+        L.last_k[(size_t)inst * N * m + e] = kf[e];
+      }
+    }
+    if (rank == 0 && tid == 0) a.status[inst] = (flag == 2) ? ST_REBUILD : ST_DONE;
+    cl.sync();
+    return;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 
@@ -837,7 +1335,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
 // while the whole batch still fits in one wave (small batches are latency-
 // bound on one SM's L2 bandwidth); 1 for large batches.  GSLS_REPLAY_CLUSTER
 // overrides (power of two <= 16).
-static int replay_cluster(Ctx* c, int count, size_t smem_bytes) {
+static int replay_cluster(Ctx* c, int count, size_t smem_bytes, const void* kern) {
   if (c->d_scratch) return 1;  // vectors in global memory: no DSMEM replicas
   static int sms = 0;
   if (!sms) {
@@ -861,7 +1359,7 @@ static int replay_cluster(Ctx* c, int count, size_t smem_bytes) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int ncl = 0;
-    if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)k_replay, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess) {
       cudaGetLastError();
       continue;
     }
@@ -890,7 +1388,7 @@ static int launch_replay(Ctx* c, ReplayArgs& a, int count, cudaStream_t st) {
     GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_replay, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attrs_set = true;
   }
-  const int cs = (a.mode == MODE_ADMM) ? replay_cluster(c, count, sb) : 1;  // LQR-mode phases broadcast
+  const int cs = (a.mode == MODE_ADMM) ? replay_cluster(c, count, sb, (const void*)k_replay) : 1;  // LQR-mode phases broadcast
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -924,6 +1422,53 @@ static int launch_replay(Ctx* c, ReplayArgs& a, int count, cudaStream_t st) {
     fprintf(stderr, " cycles");
     fprintf(stderr, "\n");
   }
+  return GSLS_OK;
+}
+
+// Staged ADMM launch: ring slots R chosen to fill shared memory (2..8); returns
+// GSLS_ERR_TOO_LARGE when even R = 2 does not fit (the caller falls back to k_replay).
+static int launch_admm_staged(Ctx* c, ReplayArgs& a, int count, cudaStream_t st) {
+  if (count == 0) return GSLS_OK;
+  a.L = c->dev;
+  a.max_layer = std::max(1, std::max(c->cvf_max_layer, c->cot_max_layer));
+  a.gscratch = nullptr;
+  a.scratch_floats = 0;
+  a.trace = nullptr;
+  const size_t limit = 227 * 1024 - 1024;
+  int R = 0;
+  size_t sb = 0;
+  for (int r = 8; r >= 2; --r) {
+    const StagedLayout SL = staged_layout(c->dev, a.max_layer, r);
+    if ((size_t)SL.total <= limit) { R = r; sb = SL.total; break; }
+  }
+  if (R == 0) return GSLS_ERR_TOO_LARGE;
+  static bool attrs_set = false;
+  if (!attrs_set) {
+    GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_admm_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)limit));
+    GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_admm_staged, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attrs_set = true;
+  }
+  const int cs = replay_cluster(c, count, sb, (const void*)k_admm_staged);
+  // One CTA per instance (large batches): k_replay's layer-parallel rounds keep more
+  // matrices in flight than the one-item-at-a-time stream; GSLS_REPLAY_STAGED=1 forces it.
+  const char* force = getenv("GSLS_REPLAY_STAGED");
+  if (cs == 1 && !(force && force[0] == '1')) return GSLS_ERR_TOO_LARGE;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(cs, count);
+  cfg.blockDim = dim3(kReplayThreads);
+  cfg.dynamicSmemBytes = sb;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ProfScope ps(P_REPLAY, st, (double)count);
+  GSLS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_admm_staged, a, R));
+  GSLS_CUDA_CHECK(cudaGetLastError());
   return GSLS_OK;
 }
 
@@ -1018,7 +1563,9 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
     a.status = c->d_status;
     a.dx = dx; a.du = du;
     a.list = c->d_inst_list;
-    rc = launch_replay(c, a, cnt, st);
+    const char* sg = getenv("GSLS_REPLAY_STAGED");
+    rc = (sg && sg[0] == '0') ? GSLS_ERR_TOO_LARGE : launch_admm_staged(c, a, cnt, st);
+    if (rc == GSLS_ERR_TOO_LARGE) rc = launch_replay(c, a, cnt, st);
     if (rc) return rc;
     rc = check_errors(c, st, "admm");  // synchronizes
     if (rc) return rc;

@@ -44,11 +44,15 @@ struct DevLqr {
   // the cache), float32 column-major with padded leading dimensions so every
   // per-iteration product is a coalesced 16-byte-load matvec (admm.cu):
   //   [pv; bv]_k = pb0_k + X23_k (y - z)_k          X23: rows 2n, cols c, ld ld2n
-  //   kf_k       = kk0_k + X5_k p+_k + X4_k w_k     X5: m x n, X4: m x c, ld ldm
+  //   kf_k       = kk0_k + [X5 X4]_k [p+; w]_k      XK: m x (n + c), ld ldm
   //   cb_k       = B_k kf_k + b_k                   Bcm: n x m, ld ldn
-  //   G_k        = Z_k dx_k + D_k kf_k              Zcm: c x n, Dcm: c x m, ld ldc  (Z = C + D K)
+  //   G_k        = [Z D]_k [dx; kf]_k               ZD: c x (n + m), ld ldc  (Z = C + D K)
   int ldm, ldn, ldc, ld2n;
-  float *X23, *X5, *X4, *Bcm, *Zcm, *Dcm;
+  float *X23, *XK, *Bcm, *ZD;
+  // physical storage of the replay vectors per scan slot (plan.h compress_slots)
+  const int* cvf_phys;
+  const int* cot_phys;
+  int cvf_nphys, cot_nphys;
   double *pb0, *kk0;
   ErrSlot* err;          // [batch]
 };
@@ -59,6 +63,7 @@ struct Ctx {
   ScanPlan cvf, cot;
   std::vector<int> cvf_layer_off, cot_layer_off;  // host copies
   int cvf_max_layer = 0, cot_max_layer = 0;
+  std::vector<int> cvf_phys, cot_phys;
   // device allocations
   std::vector<void*> allocs;
   int64_t bytes = 0;

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
     const int j = e / ldn, i = e - j * ldn;
     Bcm[e] = (i < n) ? (float)Bst[i * m + j] : 0.f;
   }
-  float* Dcm = L.Dcm + st * (size_t)m * ldc;
+  float* Dcm = L.ZD + st * (size_t)(n + m) * ldc + (size_t)n * ldc;  // D columns of [Z D]
   for (int e = threadIdx.x; e < m * ldc; e += blockDim.x) {
     const int j = e / ldc, i = e - j * ldc;
     Dcm[e] = (i < c) ? (float)Dst[i * m + j] : 0.f;
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
     }
     __syncthreads();
     const int ldm = L.ldm, ldc = L.ldc;
-    float* X5 = L.X5 + st * (size_t)n * ldm;
+    float* X5 = L.XK + st * (size_t)(n + c) * ldm;  // [X5 X4]
     for (int e = threadIdx.x; e < n * ldm; e += blockDim.x) {
       const int i = e / ldm, l = e - i * ldm;
       double s = 0.0;
@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
         for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Bst[i * m + t], s);
       X5[e] = (float)(-s);
     }
-    float* X4 = L.X4 + st * (size_t)c * ldm;
+    float* X4 = X5 + (size_t)n * ldm;
     for (int e = threadIdx.x; e < c * ldm; e += blockDim.x) {
       const int r = e / ldm, l = e - r * ldm;
       double s = 0.0;
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
       kk0[l] = -s;
     }
     const float* Cg = qp.C + st * c * n;
-    float* Zcm = L.Zcm + st * (size_t)n * ldc;
+    float* Zcm = L.ZD + st * (size_t)(n + m) * ldc;
     for (int e = threadIdx.x; e < n * ldc; e += blockDim.x) {
       const int i = e / ldc, r = e - i * ldc;
       double v = 0.0;
@@ -670,6 +670,18 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
   int rc = upload_plan(c, c->cvf, &L.cvf_ops, &L.cvf_out, &L.cvf_loff);
   if (!rc && d.N > 0) rc = upload_plan(c, c->cot, &L.cot_ops, &L.cot_out, &L.cot_loff);
   if (rc) { delete c; return rc; }
+  L.cvf_nphys = compress_slots(c->cvf, c->cvf_phys);
+  L.cot_nphys = d.N > 0 ? compress_slots(c->cot, c->cot_phys) : 0;
+  {
+    int* dp = (int*)dev_alloc(c, (c->cvf_phys.size() + c->cot_phys.size() + 1) * sizeof(int));
+    if (!dp) { delete c; return GSLS_ERR_CUDA; }
+    GSLS_CUDA_CHECK(cudaMemcpy(dp, c->cvf_phys.data(), c->cvf_phys.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (!c->cot_phys.empty())
+      GSLS_CUDA_CHECK(cudaMemcpy(dp + c->cvf_phys.size(), c->cot_phys.data(), c->cot_phys.size() * sizeof(int),
+                                 cudaMemcpyHostToDevice));
+    L.cvf_phys = dp;
+    L.cot_phys = dp + c->cvf_phys.size();
+  }
   L.cvf_nslots = c->cvf.nslots;
   L.cvf_nops = (int)c->cvf.ops.size();
   L.cvf_layers = c->cvf.layers;
@@ -700,20 +712,18 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
   L.ldm = ldg_of(d.nu); L.ldn = ldg_of(d.nx); L.ldc = ldg_of(std::max(1, d.nc)); L.ld2n = ldg_of(2 * d.nx);
   L.X23 = (float*)dev_alloc(c, std::max<size_t>(1, B * N * cc * L.ld2n) * 4);
   L.pb0 = (double*)dev_alloc(c, std::max<size_t>(1, B * N * 2 * n) * 8);
-  L.X5 = (float*)dev_alloc(c, std::max<size_t>(1, B * N * n * L.ldm) * 4);
-  L.X4 = (float*)dev_alloc(c, std::max<size_t>(1, B * N * cc * L.ldm) * 4);
+  L.XK = (float*)dev_alloc(c, std::max<size_t>(1, B * N * (n + cc) * L.ldm) * 4);
   L.kk0 = (double*)dev_alloc(c, std::max<size_t>(1, B * N * m) * 8);
   L.Bcm = (float*)dev_alloc(c, std::max<size_t>(1, B * N * m * L.ldn) * 4);
-  L.Zcm = (float*)dev_alloc(c, std::max<size_t>(1, B * N * n * L.ldc) * 4);
-  L.Dcm = (float*)dev_alloc(c, std::max<size_t>(1, B * N * m * L.ldc) * 4);
+  L.ZD = (float*)dev_alloc(c, std::max<size_t>(1, B * N * (n + m) * L.ldc) * 4);
   c->d_inst_all = (int*)dev_alloc(c, B * sizeof(int));
   c->d_inst_list = (int*)dev_alloc(c, B * sizeof(int));
   c->d_status = (int32_t*)dev_alloc(c, B * sizeof(int32_t));
   c->scratch_floats = replay_smem_floats(c);  // doubles
   if (c->scratch_floats * 8 > kReplaySmemMax) c->d_scratch = (double*)dev_alloc(c, B * c->scratch_floats * 8);
   bool fail = !L.Ps || !L.As || !L.Cs || !L.ATs || !L.cotAT || !L.cvf_rec || !L.cotA || !L.cot_rec || !L.Rhat || !L.Shat || !L.Shat64 || !L.Rinv ||
-              !L.Gamma || !L.K || !L.cvec || !L.v0 || !L.last_k || !L.last_p || !L.err || !L.X23 || !L.pb0 || !L.X5 || !L.X4 || !L.kk0 ||
-              !L.Bcm || !L.Zcm || !L.Dcm || !c->d_inst_all || !c->d_inst_list || !c->d_status ||
+              !L.Gamma || !L.K || !L.cvec || !L.v0 || !L.last_k || !L.last_p || !L.err || !L.X23 || !L.pb0 || !L.XK || !L.kk0 ||
+              !L.Bcm || !L.ZD || !c->d_inst_all || !c->d_inst_list || !c->d_status ||
               (c->scratch_floats * 8 > kReplaySmemMax && !c->d_scratch);
   if (fail) {
     for (void* p : c->allocs) cudaFree(p);

@@ -12,6 +12,7 @@
 // its reverse-scan operand swap (scan.py:169-173).
 #pragma once
 
+#include <algorithm>
 #include <vector>
 
 namespace gsls {
@@ -104,6 +105,43 @@ inline ScanPlan make_scan_plan(int length, bool reverse, const std::vector<char>
   for (int t = 0; t < length; ++t) pl.out[time_of(t)] = acc[t];
   pl.nslots = next_slot - first_slot;
   return pl;
+}
+
+// Physical slots for the replay vectors: interval colouring of slot lifetimes.
+// Leaves are defined at time 0; the ops of layer l read their operands and
+// define their result at time l + 1 (a result may not share storage with
+// anything read in the same layer); output slots stay live to the end.
+// Returns the number of physical slots; phys[s] is the storage of slot s.
+inline int compress_slots(const ScanPlan& p, std::vector<int>& phys) {
+  const int S = p.nslots;
+  const int INF = 1 << 30;
+  std::vector<int> def(S, 0), last(S, 0);
+  for (int l = 0; l < p.layers; ++l)
+    for (int o = p.layer_off[l]; o < p.layer_off[l + 1]; ++o) {
+      const ScanOp& op = p.ops[o];
+      def[op.dst] = l + 1;
+      last[op.dst] = std::max(last[op.dst], l + 1);
+      last[op.earlier] = std::max(last[op.earlier], l + 1);
+      last[op.later] = std::max(last[op.later], l + 1);
+    }
+  for (int t : p.out)
+    if (t >= 0) last[t] = INF;
+  std::vector<int> order(S);
+  for (int i = 0; i < S; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return def[a] < def[b]; });
+  phys.assign(S, -1);
+  std::vector<int> owner;  // phys id -> slot currently holding it (-1 free)
+  for (int s : order) {
+    int pick = -1;
+    for (int q = 0; q < (int)owner.size(); ++q) {
+      const int o = owner[q];
+      if (o < 0 || last[o] < def[s]) { pick = q; break; }
+    }
+    if (pick < 0) { pick = (int)owner.size(); owner.push_back(-1); }
+    owner[pick] = s;
+    phys[s] = pick;
+  }
+  return (int)owner.size();
 }
 
 }  // namespace gsls
