@@ -227,6 +227,19 @@ __device__ inline void warp_stage_mv(const float* __restrict__ M, int ld, int rb
   acc[0] = a0; acc[1] = a1; acc[2] = a2; acc[3] = a3;
 }
 
+// acc = M x (+ sgn2 M2 x2) over k in [k0, k1) for one 32-row block.
+__device__ inline void warp_cm_partial2(const float* __restrict__ M, const double* x, const float* __restrict__ M2,
+                                        const double* x2, double sgn2, int ldg, int rb, int k0, int k1,
+                                        double (&acc)[4]) {
+  warp_cm_partial(M, ldg, rb, x, k0, k1, acc);
+  if (M2) {
+    double b[4];
+    warp_cm_partial(M2, ldg, rb, x2, k0, k1, b);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) acc[r] = fma(sgn2, b[r], acc[r]);
+  }
+}
+
 // One matvec of a replay round: y = add + sgn * M x (M column-major, fp32).
 struct MvTask {
   const float* M;
@@ -234,7 +247,10 @@ struct MvTask {
   const double* add;
   double sgn;
   double* y;
-  unsigned mask;  // ranks (besides this one) whose replica of y consumes the result
+  unsigned mask;     // ranks (besides this one) whose replica of y consumes the result
+  const float* M2;   // optional second operator: y = add + sgn * (M x + sgn2 * M2 x2)
+  const double* x2;
+  double sgn2;
 };
 
 // Runs `ntask` independent matvecs (descriptors from desc(i)) with the CTA's
@@ -264,7 +280,7 @@ __device__ void mv_round(int ntask, int n, int ldg, double* part, const Cl& cl, 
       const int ti = t / RB, rb = t - ti * RB;
       const MvTask d = desc(ti);
       double acc[4];
-      warp_cm_partial(d.M, ldg, rb, d.x, 0, n, acc);
+      warp_cm_partial2(d.M, d.x, d.M2, d.x2, d.sgn2, ldg, rb, 0, n, acc);
       if ((lane >> 3) == 0) {
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
@@ -287,7 +303,7 @@ __device__ void mv_round(int ntask, int n, int ldg, double* part, const Cl& cl, 
     if (t == 0) D(1);
     double acc[4];
     const int k0 = ks * kc;
-    warp_cm_partial(d.M, ldg, rb, d.x, k0, min(n, k0 + kc), acc);
+    warp_cm_partial2(d.M, d.x, d.M2, d.x2, d.sgn2, ldg, rb, k0, min(n, k0 + kc), acc);
     if (t == 0) D(2);
     if ((lane >> 3) == 0) {
 #pragma unroll
@@ -522,25 +538,18 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
       const int per = (no + cs - 1) / cs;
       const int lo = min(no, rank * per), nl = min(no, lo + per) - lo;
       if (nl > 0) {
+        // p = p_earlier + Ups p_later + X b_earlier, b = b_later + Psi b_earlier - Y p_later
+        // (lqr.py:242-246 with the recorded X = Ups Pr, Y = Psi Cl): one round per layer
         mv_round(2 * nl, n, ldg, part, cl, [&](int ti) {
           const int oi = lo + (ti >> 1);
           const int4 op = s_cvf_ops[o0 + oi];
           const float* rec = cvf_rec + (size_t)(o0 + oi) * 4 * MS;
-          if ((ti & 1) == 0)  // t1 = p_later + Pr b_earlier
-            return MvTask{rec + 1 * MS, bv + op.y * n, pv + op.z * n, 1.0, t1 + (oi - lo) * n, 0u};
-          // t2 = b_earlier - Cl p_later
-          return MvTask{rec + 3 * MS, pv + op.z * n, bv + op.y * n, -1.0, t2 + (oi - lo) * n, 0u};
+          if ((ti & 1) == 0)
+            return MvTask{rec + 0 * MS, pv + op.z * n, pv + op.y * n, 1.0, pv + op.x * n, cvf_mask[op.x],
+                          rec + 1 * MS, bv + op.y * n, 1.0};
+          return MvTask{rec + 2 * MS, bv + op.y * n, bv + op.z * n, 1.0, bv + op.x * n, cvf_mask[op.x],
+                        rec + 3 * MS, pv + op.z * n, -1.0};
         }, (tr_on && lay == 3) ? a.trace + 200 : nullptr);
-        TR();
-        mv_round(2 * nl, n, ldg, part, cl, [&](int ti) {
-          const int oi = lo + (ti >> 1);
-          const int4 op = s_cvf_ops[o0 + oi];
-          const float* rec = cvf_rec + (size_t)(o0 + oi) * 4 * MS;
-          if ((ti & 1) == 0)  // p = Ups t1 + p_earlier
-            return MvTask{rec + 0 * MS, t1 + (oi - lo) * n, pv + op.y * n, 1.0, pv + op.x * n, cvf_mask[op.x]};
-          // b = Psi t2 + b_later
-          return MvTask{rec + 2 * MS, t2 + (oi - lo) * n, bv + op.z * n, 1.0, bv + op.x * n, cvf_mask[op.x]};
-        });
       }
       cl.sync();
       TR();
@@ -619,7 +628,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
           const int oi = lo + ti;
           const int4 op = s_cot_ops[o0 + oi];
           return MvTask{cot_rec + (size_t)(o0 + oi) * MS, cb + op.y * n, cb + op.z * n, 1.0, cb + op.x * n,
-                        cot_mask[op.x]};
+                        cot_mask[op.x], nullptr, nullptr, 0.0};
         });
       cl.sync();
       TR();
@@ -812,6 +821,20 @@ struct StagedLayout {
   int max_items, nphase;
 };
 
+// Precomputed item: everything the item loop needs, so the hot path does no
+// index arithmetic or integer division.  Vector operands are shared-memory
+// byte offsets from the dynamic shared base (-1: none).
+struct __align__(16) ItemDesc {
+  const float* src;   // bulk-copy source
+  const double* pre;  // global addend (leaf constants, kk0, b, f) or null
+  unsigned bytes;
+  int kind, rows, ld, K1, K2, kslog, kc;
+  int x1, x2, add, dst, dst2;
+  unsigned mask;
+  int e0, pre2;  // E_G first row; 1: add Abar_0 dx0 (FF2, k = 0)
+  double sgn;
+};
+
 __host__ __device__ inline int stage_slot_bytes(int n, int m, int c, int ld2n, int ldm, int ldn, int ldc, int ldg) {
   int b = n * ldg;                      // recorded n x n matrix
   b = b > c * ld2n ? b : c * ld2n;      // X23
@@ -821,7 +844,7 @@ __host__ __device__ inline int stage_slot_bytes(int n, int m, int c, int ld2n, i
   return ((b * 4 + 127) / 128) * 128;
 }
 
-__host__ __device__ inline StagedLayout staged_layout(const DevLqr& L, int max_layer, int R) {
+__host__ __device__ inline StagedLayout staged_layout(const DevLqr& L, int max_layer, int R, int max_items) {
   StagedLayout S{};
   const int n = L.n, m = L.m, N = L.N;
   int o = 0;
@@ -846,9 +869,9 @@ __host__ __device__ inline StagedLayout staged_layout(const DevLqr& L, int max_l
   S.masks = take((L.cvf_nslots + L.cot_nslots) * 4, 16);
   S.ops = take((L.cvf_nops + L.cot_nops) * 16 + (L.cvf_layers + L.cot_layers + 2 + 2 * N + 2) * 4, 16);
   S.phys = take((L.cvf_nslots + L.cot_nslots) * 4, 16);
-  S.max_items = 4 * N + 4 * L.cvf_nops + L.cot_nops + 8;
-  S.items = take(S.max_items * 8, 16);
-  S.nphase = 2 * L.cvf_layers + L.cot_layers + 5;
+  S.max_items = max_items;
+  S.items = take(S.max_items * (int)sizeof(ItemDesc), 16);
+  S.nphase = L.cvf_layers + L.cot_layers + 5;
   S.phase = take((S.nphase + 1) * 4, 16);
   S.mbar = take(R * 8, 8);
   S.total = o;
@@ -893,7 +916,7 @@ struct ItemEpi {
   int e0;              // E_G: first stacked constraint row of the stage
 };
 
-__global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a, int R) {
+__global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a, int R, int max_items) {
   const DevLqr& L = a.L;
   const int inst = a.list ? a.list[blockIdx.y] : (int)blockIdx.y;
   const int n = L.n, m = L.m, c = L.c, nf = L.nf, N = L.N, ldg = L.ldg, mtot = L.mtot;
@@ -903,7 +926,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   cl.rank = cluster_rank();
   cl.cs = cluster_size();
   const int rank = (int)cl.rank, cs = (int)cl.cs;
-  const StagedLayout SL = staged_layout(L, a.max_layer, R);
+  const StagedLayout SL = staged_layout(L, a.max_layer, R, max_items);
   extern __shared__ __align__(128) unsigned char smb[];
   unsigned char* ring = smb + SL.ring;
   double* pv = reinterpret_cast<double*>(smb + SL.pv);
@@ -930,7 +953,8 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   int* s_cot_out = s_cvf_out + N + 1;
   int* cvf_phys = reinterpret_cast<int*>(smb + SL.phys);
   int* cot_phys = cvf_phys + L.cvf_nslots;
-  int2* items = reinterpret_cast<int2*>(smb + SL.items);  // (kind | which << 8, index)
+  ItemDesc* desc = reinterpret_cast<ItemDesc*>(smb + SL.items);
+  int2* items = reinterpret_cast<int2*>(smb + SL.part);  // setup only: (kind | which << 8 | loc << 16, index)
   int* phase_off = reinterpret_cast<int*>(smb + SL.phase);
   uint64_t* full = reinterpret_cast<uint64_t*>(smb + SL.mbar);
   __shared__ int s_flag, s_nitems;
@@ -980,9 +1004,12 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
       const int o0 = s_cvf_loff[lay], no = s_cvf_loff[lay + 1] - o0, per = (no + cs - 1) / cs;
       const int lo = min(no, rank * per), hi = min(no, lo + per);
       phase_off[ph++] = ni;
-      for (int oi = lo; oi < hi; ++oi) { add(IT_CVF1, 0, o0 + oi, oi - lo); add(IT_CVF1, 1, o0 + oi, oi - lo); }
-      phase_off[ph++] = ni;
-      for (int oi = lo; oi < hi; ++oi) { add(IT_CVF2, 0, o0 + oi, oi - lo); add(IT_CVF2, 1, o0 + oi, oi - lo); }
+      for (int oi = lo; oi < hi; ++oi) {  // t1 = p_e + Ups p_l; p = t1 + X b_e; t2 = b_l + Psi b_e; b = t2 - Y p_l
+        add(IT_CVF1, 0, o0 + oi, oi - lo);
+        add(IT_CVF2, 1, o0 + oi, oi - lo);
+        add(IT_CVF1, 2, o0 + oi, oi - lo);
+        add(IT_CVF2, 3, o0 + oi, oi - lo);
+      }
     }
     phase_off[ph++] = ni;
     for (int k = rank; k < N; k += cs) add(IT_FF1, 0, k);
@@ -1026,24 +1053,76 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   auto CB = [&](int s) { return cb + (size_t)cot_phys[s] * n; };
   auto dxp = [&](int k) -> const double* { return k == 0 ? dx0s : CB(s_cot_out[k - 1]); };
 
-  // ---- item stream ---------------------------------------------------------------------
+  // ---- item descriptors (parallel over items) ------------------------------------------
+  {
+    auto off = [&](const void* p) { return p ? (int)((const unsigned char*)p - smb) : -1; };
+    for (int j = tid; j < P; j += nthr) {
+      const int2 itm = items[j];
+      const int kind = itm.x & 0xff, which = (itm.x >> 8) & 0xff, loc = itm.x >> 16, idx = itm.y;
+      ItemDesc d{};
+      d.kind = kind; d.rows = n; d.ld = ldg; d.K1 = n; d.K2 = 0; d.x2 = -1; d.add = -1; d.dst2 = -1;
+      d.sgn = 1.0; d.pre = nullptr; d.pre2 = 0; d.mask = 0u; d.e0 = 0;
+      d.bytes = (unsigned)MS * 4;
+      switch (kind) {
+        case IT_P1:  // [p; b]_k = pb0_k + X23_k w_k (fused leaves, admm.py:113-121, lqr.py:338-342)
+          d.src = X23 + (size_t)idx * c * L.ld2n; d.bytes = c * L.ld2n * 4;
+          d.rows = 2 * n; d.ld = L.ld2n; d.K1 = c; d.x1 = off(w + idx * c);
+          d.dst = off(PV(idx)); d.dst2 = off(BV(idx)); d.pre = pb0 + (size_t)idx * 2 * n; d.mask = cvf_mask[idx];
+          break;
+        case IT_CVF1: {  // t1 = p_earlier + Ups p_later | t2 = b_later + Psi b_earlier (lqr.py:242-246)
+          const int4 op = s_cvf_ops[idx];
+          d.src = cvf_rec + ((size_t)idx * 4 + which) * MS;  // which: 0 Ups, 2 Psi
+          d.x1 = off(which ? BV(op.y) : PV(op.z));
+          d.add = off(which ? BV(op.z) : PV(op.y));
+          d.dst = off((which ? t2 : t1) + loc * n);
+          break;
+        }
+        case IT_CVF2: {  // p = t1 + X b_earlier | b = t2 - Y p_later (X = Ups Pr, Y = Psi Cl)
+          const int4 op = s_cvf_ops[idx];
+          d.src = cvf_rec + ((size_t)idx * 4 + which) * MS;  // which: 1 X, 3 Y
+          d.x1 = off(which == 3 ? PV(op.z) : BV(op.y));
+          d.add = off((which == 3 ? t2 : t1) + loc * n);
+          d.dst = off(which == 3 ? BV(op.x) : PV(op.x));
+          d.sgn = (which == 3) ? -1.0 : 1.0;
+          d.mask = cvf_mask[op.x];
+          break;
+        }
+        case IT_FF1:  // kf = kk0 + [X5 X4] [p+; w] (lqr.py:345-346)
+          d.src = XK + (size_t)idx * (n + c) * L.ldm; d.bytes = (n + c) * L.ldm * 4;
+          d.rows = m; d.ld = L.ldm; d.K1 = n; d.x1 = off(PV(s_cvf_out[idx + 1])); d.K2 = c; d.x2 = off(w + idx * c);
+          d.dst = off(kf + idx * m); d.pre = kk0 + (size_t)idx * m;
+          break;
+        case IT_FF2:  // COT leaf b = B kf + b (+ Abar_0 dx0) (lqr.py:349-356)
+          d.src = Bcm + (size_t)idx * m * L.ldn; d.bytes = m * L.ldn * 4;
+          d.rows = n; d.ld = L.ldn; d.K1 = m; d.x1 = off(kf + idx * m);
+          d.dst = off(CB(idx)); d.pre = bq + (size_t)idx * n; d.pre2 = (idx == 0); d.mask = cot_mask[idx];
+          break;
+        case IT_COT: {  // b = A_later b_earlier + b_later (lqr.py:281-285)
+          const int4 op = s_cot_ops[idx];
+          d.src = cot_rec + (size_t)idx * MS;
+          d.x1 = off(CB(op.y)); d.add = off(CB(op.z)); d.dst = off(CB(op.x)); d.mask = cot_mask[op.x];
+          break;
+        }
+        default:  // G = [Z D] [dx; kf] = C dx + D du, then the projection (admm.py:91-97)
+          d.src = ZD + (size_t)idx * (n + m) * L.ldc; d.bytes = (n + m) * L.ldc * 4;
+          d.rows = c; d.ld = L.ldc; d.K1 = n; d.x1 = off(dxp(idx)); d.K2 = m; d.x2 = off(kf + idx * m);
+          d.pre = fst + (size_t)idx * c; d.e0 = idx * c;
+          break;
+      }
+      const int RB = (d.rows + 31) >> 5;
+      int kslog = 3;  // KS = 8 / RB (power of two): one partial half holds <= 8 (row block, slice) tasks
+      while (kslog > 0 && (RB << kslog) > 8) --kslog;
+      const int KS = 1 << kslog, K = d.K1 + d.K2;
+      d.kslog = kslog;
+      d.kc = (((K + KS - 1) / KS) + 3) & ~3;
+      desc[j] = d;
+    }
+  }
+  __syncthreads();
   int pi = 0, pslot = 0;  // producer (thread 0): next item (mod P), slot to fill
   auto issue = [&]() {
     if (tid != 0 || P == 0) return;
-    const int2 itm = items[pi];
-    const int kind = itm.x & 0xff, which = (itm.x >> 8) & 0xff, idx = itm.y;
-    const float* src;
-    unsigned bytes;
-    switch (kind) {
-      case IT_P1: bytes = c * L.ld2n * 4; src = X23 + (size_t)idx * c * L.ld2n; break;
-      case IT_CVF1: bytes = (unsigned)MS * 4; src = cvf_rec + ((size_t)idx * 4 + (which ? 3 : 1)) * MS; break;
-      case IT_CVF2: bytes = (unsigned)MS * 4; src = cvf_rec + ((size_t)idx * 4 + (which ? 2 : 0)) * MS; break;
-      case IT_FF1: bytes = (n + c) * L.ldm * 4; src = XK + (size_t)idx * (n + c) * L.ldm; break;
-      case IT_FF2: bytes = m * L.ldn * 4; src = Bcm + (size_t)idx * m * L.ldn; break;
-      case IT_COT: bytes = (unsigned)MS * 4; src = cot_rec + (size_t)idx * MS; break;
-      default: bytes = (n + m) * L.ldc * 4; src = ZD + (size_t)idx * (n + m) * L.ldc; break;
-    }
-    bulk_load(ring + (size_t)pslot * SL.slot, src, bytes, full + pslot);
+    bulk_load(ring + (size_t)pslot * SL.slot, desc[pi].src, desc[pi].bytes, full + pslot);
     if (++pi == P) pi = 0;
     if (++pslot == R) pslot = 0;
   };
@@ -1066,63 +1145,32 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   cl.sync();  // every replica exists before the first remote store
 
   int cslot = 0, cpar = 0, ph2 = 0;  // consumer: slot, mbarrier parity, partial-sum half
-  const int nph = 2 * L.cvf_layers + L.cot_layers + 4;  // P1, CVF rounds, FF1, FF2, COT layers, G
-  const int ph_ff1 = 2 * L.cvf_layers + 1, ph_g = nph - 1;
+  const int nph = L.cvf_layers + L.cot_layers + 4;  // P1, CVF layers, FF1, FF2, COT layers, G
+  const int ph_ff1 = L.cvf_layers + 1, ph_g = nph - 1;
 
+  int tr_it = 0;
   for (;;) {
     double rp = 0.0, rdz = 0.0;
     int j = 0;
+    if (a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == 0) a.trace[250] = clock64();
     for (int ph = 0; ph < nph; ++ph) {
-      // ---- the phase's items: one matvec each, read from the ring; the item code is
-      //      specialised per kind (compile-time) so each phase runs only its own path ----
-      auto run_item = [&](auto kind_c) {
-        constexpr int kind = decltype(kind_c)::value;
-        const int2 itm = items[j];
-        const int which = (itm.x >> 8) & 0xff, loc = itm.x >> 16, idx = itm.y;
-        // operands: rows x (K1 + K2) matrix (leading dimension ld), x = [x1; x2]
-        int rows = n, ld = ldg, K1 = n, K2 = 0, ek = E_SET;
-        const double *x1 = nullptr, *x2 = nullptr, *add = nullptr, *pre = nullptr, *pre2 = nullptr;
-        double *dst = nullptr, *dst2 = nullptr, sgn = 1.0;
-        unsigned mk = 0u;
-        if constexpr (kind == IT_P1) {  //   // [p; b]_k = pb0_k + X23_k w_k (fused leaves, admm.py:113-121, lqr.py:338-342)
-            rows = 2 * n; ld = L.ld2n; K1 = c; x1 = w + idx * c; ek = E_P1;
-            dst = PV(idx); dst2 = BV(idx); pre = pb0 + (size_t)idx * 2 * n; mk = cvf_mask[idx];
-        } else if constexpr (kind == IT_CVF1) {  // t1 = p_later + Pr b_earlier | t2 = b_earlier - Cl p_later (lqr.py:244-246)
-            const int4 op = s_cvf_ops[idx];
-            x1 = which ? PV(op.z) : BV(op.y);
-            add = which ? BV(op.y) : PV(op.z);
-            dst = (which ? t2 : t1) + loc * n;
-            sgn = which ? -1.0 : 1.0;
-        } else if constexpr (kind == IT_CVF2) {  // p = Ups t1 + p_earlier | b = Psi t2 + b_later
-            const int4 op = s_cvf_ops[idx];
-            x1 = (which ? t2 : t1) + loc * n;
-            add = which ? BV(op.z) : PV(op.y);
-            dst = which ? BV(op.x) : PV(op.x);
-            ek = E_PUT; mk = cvf_mask[op.x];
-        } else if constexpr (kind == IT_FF1) {  // kf = kk0 + [X5 X4] [p+; w] (lqr.py:345-346)
-            rows = m; ld = L.ldm; K1 = n; x1 = PV(s_cvf_out[idx + 1]); K2 = c; x2 = w + idx * c;
-            ek = E_KF; dst = kf + idx * m; pre = kk0 + (size_t)idx * m;
-        } else if constexpr (kind == IT_FF2) {  // COT leaf b = B kf + b (+ Abar_0 dx0) (lqr.py:349-356)
-            rows = n; ld = L.ldn; K1 = m; x1 = kf + idx * m;
-            ek = E_CB; dst = CB(idx); pre = bq + (size_t)idx * n; pre2 = (idx == 0) ? v0 : nullptr;
-            mk = cot_mask[idx];
-        } else if constexpr (kind == IT_COT) {  // b = A_later b_earlier + b_later (lqr.py:281-285)
-            const int4 op = s_cot_ops[idx];
-            x1 = CB(op.y); add = CB(op.z); dst = CB(op.x); ek = E_PUT; mk = cot_mask[op.x];
-        } else {  // G = [Z D] [dx; kf] = C dx + D du, then the projection (admm.py:91-97)
-            rows = c; ld = L.ldc; K1 = n; x1 = dxp(idx); K2 = m; x2 = kf + idx * m;
-            ek = E_G; pre = fst + (size_t)idx * c;
-        }
+      // ---- the phase's items: one matvec each, read from the ring ------------------------
+      for (; j < phase_off[ph + 1]; ++j) {
+        const bool tq = a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == 0 && j < 20;
+        long long q0 = tq ? clock64() : 0, q1 = 0, q2 = 0, q3 = 0, q4 = 0;
+        const ItemDesc& d = desc[j];
+        const int rows = d.rows, ld = d.ld, K1 = d.K1, kind = d.kind;
+        const double* x1 = reinterpret_cast<const double*>(smb + d.x1);
+        const double* x2 = reinterpret_cast<const double*>(smb + (d.x2 < 0 ? d.x1 : d.x2));
         double pre_v = 0.0;
-        if (tid < rows && pre) pre_v = pre[tid] + (pre2 ? pre2[tid] : 0.0);
+        if (tid < rows && d.pre) pre_v = d.pre[tid] + (d.pre2 ? v0[tid] : 0.0);
         mbar_wait(full + cslot, (unsigned)cpar);
+        if (tq) q1 = clock64();
         const float* M = reinterpret_cast<const float*>(ring + (size_t)cslot * SL.slot);
         double* pt = part + ph2 * (kReplayThreads / 2);
-        const int RB = (rows + 31) >> 5, K = K1 + K2;
-        const int KS = max(1, (nwarp / 2) / RB);  // one partial half: <= 8 (row block, slice) tasks
-        const int kc = (((K + KS - 1) / KS) + 3) & ~3;
-        for (int t = warp; t < RB * KS; t += nwarp) {
-          const int rb = t / KS, ks = t - rb * KS;
+        const int kslog = d.kslog, KS = 1 << kslog, kc = d.kc, K = K1 + d.K2;
+        if (warp < (((rows + 31) >> 5) << kslog)) {
+          const int rb = warp >> kslog, ks = warp & (KS - 1);
           const int rq = lane & 7, gq = lane >> 3;
           const int row0 = rb * 32 + 4 * rq;
           const int k0 = ks * kc, k1 = min(K, k0 + kc);
@@ -1130,7 +1178,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
           if (row0 < ld) {
 #pragma unroll 4
             for (int k = k0 + gq; k < k1; k += 4) {
-              const float4 v = *reinterpret_cast<const float4*>(M + (size_t)k * ld + row0);
+              const float4 v = *reinterpret_cast<const float4*>(M + k * ld + row0);
               const double xk = (k < K1) ? x1[k] : x2[k - K1];
               a0 = fma((double)v.x, xk, a0);
               a1 = fma((double)v.y, xk, a1);
@@ -1146,34 +1194,42 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
             a3 += __shfl_xor_sync(0xffffffffu, a3, o);
           }
           if (gq == 0) {
-            double* pp = pt + (rb * KS + ks) * 32 + 4 * rq;
+            double* pp = pt + (warp << 5) + 4 * rq;  // (rb * KS + ks) * 32
             pp[0] = a0; pp[1] = a1; pp[2] = a2; pp[3] = a3;
           }
         }
         // One barrier per item: the slot is refilled right after it and the partial
         // sums alternate halves, so this epilogue overlaps the next item.
+        if (tq) q2 = clock64();
         __syncthreads();
+        if (tq) q3 = clock64();
         issue();
+        if (tq) q4 = clock64();
         if (++cslot == R) { cslot = 0; cpar ^= 1; }
         ph2 ^= 1;
+        if (tq) {
+          a.trace[100 + 5 * j] = q1 - q0; a.trace[101 + 5 * j] = q2 - q1; a.trace[102 + 5 * j] = q3 - q2;
+          a.trace[103 + 5 * j] = q4 - q3;
+        }
         if (tid < rows) {
-          const int rb = tid >> 5, ro = tid & 31;
+          const double* pr = pt + (((tid >> 5) << kslog) << 5) + (tid & 31);
           double sum = 0.0;
-          for (int ks = 0; ks < KS; ++ks) sum += pt[(rb * KS + ks) * 32 + ro];
+          for (int ks = 0; ks < KS; ++ks) sum += pr[ks << 5];
           const int i = tid;
-          if constexpr (kind == IT_CVF1) {
-            dst[i] = add[i] + sgn * sum;
-          } else if constexpr (kind == IT_CVF2 || kind == IT_COT) {
-            cl.put_mask(dst + i, add[i] + sum, mk);
-          } else if constexpr (kind == IT_P1) {
-            cl.put_mask(i < n ? dst + i : dst2 + (i - n), pre_v + sum, mk);
-          } else if constexpr (kind == IT_FF1) {
-            dst[i] = pre_v + sum;
-          } else if constexpr (kind == IT_FF2) {
-            cl.put_mask(dst + i, pre_v + sum, mk);
-          } else {  // z = min(G + y, f); lam += rho (G - z); y = lam / rho (admm.py:130-135)
-            {
-              const int e = idx * c + i;
+          double* dst = reinterpret_cast<double*>(smb + d.dst);
+          switch (kind) {
+            case IT_CVF1: dst[i] = reinterpret_cast<const double*>(smb + d.add)[i] + sum; break;
+            case IT_CVF2:
+            case IT_COT:
+              cl.put_mask(dst + i, reinterpret_cast<const double*>(smb + d.add)[i] + d.sgn * sum, d.mask);
+              break;
+            case IT_P1:
+              cl.put_mask(i < n ? dst + i : reinterpret_cast<double*>(smb + d.dst2) + (i - n), pre_v + sum, d.mask);
+              break;
+            case IT_FF1: dst[i] = pre_v + sum; break;
+            case IT_FF2: cl.put_mask(dst + i, pre_v + sum, d.mask); break;
+            default: {  // z = min(G + y, f); lam += rho (G - z); y = lam / rho (admm.py:130-135)
+              const int e = d.e0 + i;
               const double zo = z[e];
               const double zn = fmin(sum + y[e], pre_v);
               const double ln = lam[e] + rho * (sum - zn);
@@ -1187,21 +1243,10 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
             }
           }
         }
-      };
-      const int kind_ph = (ph == 0) ? IT_P1 : (ph <= 2 * L.cvf_layers) ? ((ph & 1) ? IT_CVF1 : IT_CVF2)
-                        : (ph == ph_ff1) ? IT_FF1 : (ph == ph_ff1 + 1) ? IT_FF2 : (ph == ph_g) ? IT_G : IT_COT;
-      for (; j < phase_off[ph + 1]; ++j) {
-        switch (kind_ph) {
-          case IT_P1: run_item(std::integral_constant<int, IT_P1>{}); break;
-          case IT_CVF1: run_item(std::integral_constant<int, IT_CVF1>{}); break;
-          case IT_CVF2: run_item(std::integral_constant<int, IT_CVF2>{}); break;
-          case IT_FF1: run_item(std::integral_constant<int, IT_FF1>{}); break;
-          case IT_FF2: run_item(std::integral_constant<int, IT_FF2>{}); break;
-          case IT_COT: run_item(std::integral_constant<int, IT_COT>{}); break;
-          default: run_item(std::integral_constant<int, IT_G>{}); break;
-        }
       }
       // ---- phase boundary -----------------------------------------------------------
+      if (a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == 0 && 2 * ph + 1 < 250)
+        a.trace[2 * ph + 1] = clock64();
       if (ph == 0) {  // terminal leaf (qN + rho CN' w_N, 0) on its owner
         if (rank == srank(N))
           for (int i = tid; i < n; i += nthr) {
@@ -1229,12 +1274,16 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
             rp = fmax(rp, fabs(sum - zn));
             rdz = fmax(rdz, fabs(zn - zo));
           }
-      } else if ((ph <= 2 * L.cvf_layers && (ph & 1)) || ph == ph_ff1) {
-        __syncthreads();  // t1 / t2 or kf complete (CTA-local)
+      } else if (ph == ph_ff1) {
+        __syncthreads();  // kf complete (CTA-local)
       } else {
-        cl.sync();  // CVF round 2, FF2, COT layers: remote consumers
+        cl.sync();  // CVF layers, FF2, COT layers: remote consumers
       }
+      if (a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == 0 && 2 * ph + 2 < 250)
+        a.trace[2 * ph + 2] = clock64();
     }
+    if (a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == 0) a.trace[0] = nph;
+    ++tr_it;
     const double rpb = block_max_d(rp, red);
     const double rdb = block_max_d(rdz, red + 32);
     if (tid == 0) {
@@ -1435,13 +1484,6 @@ static int launch_admm_staged(Ctx* c, ReplayArgs& a, int count, cudaStream_t st)
   a.scratch_floats = 0;
   a.trace = nullptr;
   const size_t limit = 227 * 1024 - 1024;
-  int R = 0;
-  size_t sb = 0;
-  for (int r = 8; r >= 2; --r) {
-    const StagedLayout SL = staged_layout(c->dev, a.max_layer, r);
-    if ((size_t)SL.total <= limit) { R = r; sb = SL.total; break; }
-  }
-  if (R == 0) return GSLS_ERR_TOO_LARGE;
   static bool attrs_set = false;
   if (!attrs_set) {
     GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_admm_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1449,7 +1491,24 @@ static int launch_admm_staged(Ctx* c, ReplayArgs& a, int count, cudaStream_t st)
     GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_admm_staged, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attrs_set = true;
   }
-  const int cs = replay_cluster(c, count, sb, (const void*)k_admm_staged);
+  // items per rank bound for the largest cluster this batch can use (fewer ranks -> more items)
+  const int cs0 = replay_cluster(c, count, limit, (const void*)k_admm_staged);  // occupancy at the largest footprint
+  const int Nn = c->dims.N;
+  auto cdiv = [](int x, int y) { return (x + y - 1) / y; };
+  int max_items = 4 * cdiv(Nn, cs0) + 8;
+  for (int l = 0; l < c->cvf.layers; ++l) max_items += 4 * cdiv(c->cvf_layer_off[l + 1] - c->cvf_layer_off[l], cs0);
+  for (int l = 0; l < c->cot.layers; ++l) max_items += cdiv(c->cot_layer_off[l + 1] - c->cot_layer_off[l], cs0);
+  if (max_items > kReplayThreads) return GSLS_ERR_TOO_LARGE;  // setup list lives in the partial buffer
+  int R = 0;
+  size_t sb = 0;
+  for (int r = 8; r >= 2; --r) {
+    const StagedLayout SL = staged_layout(c->dev, a.max_layer, r, max_items);
+    if ((size_t)SL.total <= limit) { R = r; sb = SL.total; break; }
+  }
+  if (R == 0) return GSLS_ERR_TOO_LARGE;
+  const int cs = cs0;
+  if (getenv("GSLS_REPLAY_VERBOSE"))
+    fprintf(stderr, "staged replay: count=%d cs=%d R=%d max_items=%d smem=%zu\n", count, cs, R, max_items, sb);
   // One CTA per instance (large batches): k_replay's layer-parallel rounds keep more
   // matrices in flight than the one-item-at-a-time stream; GSLS_REPLAY_STAGED=1 forces it.
   const char* force = getenv("GSLS_REPLAY_STAGED");
@@ -1466,9 +1525,30 @@ static int launch_admm_staged(Ctx* c, ReplayArgs& a, int count, cudaStream_t st)
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  ProfScope ps(P_REPLAY, st, (double)count);
-  GSLS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_admm_staged, a, R));
-  GSLS_CUDA_CHECK(cudaGetLastError());
+  static unsigned long long* trace = nullptr;
+  const bool tracing = getenv("GSLS_REPLAY_TRACE") != nullptr;
+  if (tracing && !trace) GSLS_CUDA_CHECK(cudaMalloc(&trace, 256 * sizeof(unsigned long long)));
+  a.trace = tracing ? trace : nullptr;
+  if (tracing) GSLS_CUDA_CHECK(cudaMemsetAsync(trace, 0, 256 * sizeof(unsigned long long), st));
+  {
+    ProfScope ps(P_REPLAY, st, (double)count);
+    GSLS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_admm_staged, a, R, max_items));
+    GSLS_CUDA_CHECK(cudaGetLastError());
+  }
+  if (tracing) {
+    unsigned long long h[256];
+    GSLS_CUDA_CHECK(cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st));
+    GSLS_CUDA_CHECK(cudaStreamSynchronize(st));
+    fprintf(stderr, "staged R=%d cs=%d phases %llu (items | boundary) cycles:", R, cs, h[0]);
+    unsigned long long prev = h[250];
+    for (unsigned long long p = 0; p < h[0]; ++p) {
+      fprintf(stderr, " %llu|%llu", h[2 * p + 1] - prev, h[2 * p + 2] - h[2 * p + 1]);
+      prev = h[2 * p + 2];
+    }
+    fprintf(stderr, "\nitems (wait, matvec, sync, issue):");
+    for (int j = 0; j < 20; ++j) fprintf(stderr, " [%llu %llu %llu %llu]", h[100 + 5 * j], h[101 + 5 * j], h[102 + 5 * j], h[103 + 5 * j]);
+    fprintf(stderr, "\n");
+  }
   return GSLS_OK;
 }
 

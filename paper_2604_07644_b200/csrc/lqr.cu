@@ -281,13 +281,18 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
 }
 
 // Matrix half of the CVF combine (Eq. 28) for one op per CTA; optionally
-// records (Ups, Pr, Psi, Cl) column-major for the replay.  Shared with the SLS
-// grid scan (no record).
+// records the replay operators column-major: Ups, X = Ups Pr, Psi, Y = Psi Cl,
+// so the cached replay p = Ups (p_r + Pr b_l) + p_l, b = Psi (b_l - Cl p_r) + b_r
+// (lqr.py:242-246) becomes p = p_l + Ups p_r + X b_l, b = b_r + Psi b_l - Y p_r:
+// four independent matvecs per combine, one round per tree layer.  Shared with
+// the SLS grid scan (no record).
 //
 // P and C are symmetric in exact arithmetic (value-function Hessians and
 // controllability Gramians, lqr.py:236-238), so Pr and Cl serve as their own
 // transposes; A is kept in both orientations (As, ATs) so every operand
-// arrives by a plain cp.async copy.  Six n x lds smem buffers:
+// arrives by a plain cp.async copy.  With Minv = (I + Pr Cl)^-1, the products
+// Minv Pr and Minv' Cl are symmetric, so X' = Minv Pr Al = V (the product P
+// needs anyway) and Y' = Minv' Cl Ar' = Minv' W2.  Six n x lds smem buffers:
 //   b0 Pr -> W2 | b1 Cl -> Minv -> V | b2 M1 -> Minv^T | b3 Al | b4 Ar^T | b5 W1 -> Psi^T
 template <int NP>
 __global__ void __launch_bounds__(NP == 64 ? 256 : 416, NP == 64 ? 2 : 1) k_cvf_combine(CombineArgs a) {
@@ -318,10 +323,6 @@ __global__ void __launch_bounds__(NP == 64 ? 256 : 416, NP == 64 ? 2 : 1) k_cvf_
   cp_async_wait<1>();
   __syncthreads();
   gemm_tn(n, b0, b1, lds, EpiSmem{b2, lds, n, true});   // M1 = I + Pr Cl
-  if (rec) {
-    cta_store(rec + 1 * MS, b0, lds, n);                 // Pr record
-    cta_store(rec + 3 * MS, b1, lds, n);                 // Cl record
-  }
   cp_async_wait<0>();
   __syncthreads();
   gemm_tn(n, b0, b3, lds, EpiSmem{b5, lds, n, false});  // W1 = Pr Al
@@ -333,11 +334,13 @@ __global__ void __launch_bounds__(NP == 64 ? 256 : 416, NP == 64 ? 2 : 1) k_cvf_
   if (!ok && threadIdx.x == 0)
     raise_err(a.err ? a.err + inst : nullptr, GSLS_ERR_ILL_CONDITIONED, a.op_base + blockIdx.x);
   if (rec) {
-    gemm_tn(n, b1, b3, lds, EpiGlobal{rec, nullptr, ldg, n, nullptr});  // Ups^T = Minv^T Al -> record
+    gemm_tn(n, b1, b3, lds, EpiGlobal{rec + 0 * MS, nullptr, ldg, n, nullptr});  // Ups^T = Minv^T Al
+    gemm_tn(n, b1, b0, lds, EpiGlobal{rec + 3 * MS, nullptr, ldg, n, nullptr});  // Y^T = Minv^T W2
     __syncthreads();
   }
-  gemm_tn(n, b2, b5, lds, EpiSmem{b1, lds, n, false});  // V = Minv W1 (over Minv)
+  gemm_tn(n, b2, b5, lds, EpiSmem{b1, lds, n, false});  // V = Minv W1 = X^T (over Minv)
   __syncthreads();
+  if (rec) cta_store(rec + 1 * MS, b1, lds, n);          // X record
   gemm_tn(n, b3, b1, lds, EpiGlobal{a.Ps + ib + od, a.Ps + ib + oe, ldg, n, nullptr});  // P = Al^T V + Pl
   gemm_tn(n, b2, b4, lds, EpiSmem{b5, lds, n, false});  // Psi^T = Minv Ar^T (over W1)
   __syncthreads();
