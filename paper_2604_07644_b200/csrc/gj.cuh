@@ -177,4 +177,195 @@ __device__ bool gj_inverse_rows(const float* a, float* inv, float* invT, int lds
   return ok;
 }
 
+
+// Scratch words of gj_inverse_panel: panel values (NP x 8), pivot rows / steps.
+constexpr int gjp_scratch_words(int NP) { return NP * 8 + 2 * NP + 16; }
+
+// Blocked in-place Gauss-Jordan inverse with partial pivoting and no row
+// interchanges: panels of 8 pivot columns.  Per panel, one warp eliminates the
+// n x 8 panel in its registers (warp-shuffle argmax over the rows not yet
+// pivoted, first index on ties as LAPACK i*amax; the in-place rule turns the
+// panel into [D; -A_op D] with D the inverse of the pivot block), then every
+// thread applies the panel to its columns as one rank-8 update
+//     new[i][c] = (i pivot ? 0 : old[i][c]) + sum_s panel[i][s] old[p_s][c],
+// so a panel costs two CTA barriers instead of sixteen.  Without interchanges
+// the result is the inverse with rows and columns permuted by the pivot order:
+// inv[q(i)][p(c)] = W[i][c] (p(k) = pivot row of step k, q = p^-1).
+//
+// a: input (smem, row-major, lds), read into registers first; work: an NP x lds
+// smem buffer (may alias a); inv / invT outputs (may alias a / work: written
+// after the last read).  4 threads per row, threads [0, 4*NP) take part;
+// named barrier 1.  Returns false when a pivot is zero / non-finite / below
+// rel_tol * max|a| (the ill-conditioned-combine rule, lqr.py:229-232).
+template <int NP>
+__device__ bool gj_inverse_panel(const float* a, float* work, float* inv, float* invT, int lds, int n,
+                                 float* scratch, float rel_tol) {
+  constexpr int SEG = NP / 4;
+  constexpr int NT = NP * 4;
+  constexpr int NW = NT / 32;
+  constexpr int PW = 8;                                   // panel width
+  constexpr int RPL = NP / 32;                            // rows per lane in the panel warp (2 for 64)
+  static_assert(NP % 32 == 0 || NP == 80, "panel warp covers NP rows");
+  float* pan = scratch;                                   // [NP][PW] eliminated panel
+  int* prow = reinterpret_cast<int*>(pan + NP * PW);      // [NP] pivot row of step k
+  int* pstep = prow + NP;                                 // [NP] step at which row i pivoted (-1)
+  float* misc = reinterpret_cast<float*>(pstep + NP);     // [0] max|a|, [1] fail
+  const int tid = threadIdx.x;
+  const bool part = tid < NT;
+  const int row = tid >> 2, q = tid & 3, lane = tid & 31, warp = tid >> 5;
+  float r[SEG];
+  float mx = 0.f;
+#pragma unroll
+  for (int c = 0; c < SEG; ++c) {
+    const int col = q * SEG + c;
+    r[c] = (part && row < n && col < n) ? a[row * lds + col] : 0.f;
+    mx = fmaxf(mx, fabsf(r[c]));
+  }
+  mx = warp_max(mx);
+  if (part && lane == 0) pan[warp] = mx;
+  for (int i = tid; i < NP; i += blockDim.x) pstep[i] = -1;
+  __syncthreads();  // a fully read (work / inv may alias it from here on)
+  if (tid == 0) {
+    float m2 = 0.f;
+    for (int w = 0; w < NW; ++w) m2 = fmaxf(m2, pan[w]);
+    misc[0] = m2;
+    misc[1] = 0.f;
+  }
+  __syncthreads();
+  const float thresh = rel_tol * misc[0];
+  constexpr int PROWS = (NP + 31) / 32;  // panel rows per lane
+  // threads >= NT (CTAs wider than 4*NP) sit out: the named barriers count NT threads
+  for (int k0 = 0; part && k0 < n; k0 += PW) {
+    const int pw = min(PW, n - k0);
+    // ---- publish the rows ----------------------------------------------------------
+    if (part && row < n) {
+#pragma unroll
+      for (int c = 0; c < SEG; c += 4)
+        if (q * SEG + c < n)  // 4-column chunks inside the padded row (ld >= round_up(n, 4))
+          *reinterpret_cast<float4*>(work + row * lds + q * SEG + c) = make_float4(r[c], r[c + 1], r[c + 2], r[c + 3]);
+    }
+    bar_named(1, NT);
+    // ---- panel elimination by warp 0 (registers + shuffles) --------------------------
+    if (warp == 0) {
+      float pv[PROWS][PW];
+      bool used[PROWS];
+#pragma unroll
+      for (int h = 0; h < PROWS; ++h) {
+        const int i = lane + 32 * h;
+        used[h] = !(i < n) || pstep[i] >= 0;
+#pragma unroll
+        for (int s = 0; s < PW; ++s) pv[h][s] = (i < n && s < pw) ? work[i * lds + k0 + s] : 0.f;
+      }
+      bool fail = false;
+#pragma unroll
+      for (int s = 0; s < PW; ++s) {
+        if (s < pw) {
+          // argmax |pv[i][s]| over unused rows (key = bits(|x|) + 1 orders like |x|)
+          unsigned best = 0u;
+          int bi = NP;
+#pragma unroll
+          for (int h = 0; h < PROWS; ++h) {
+            const unsigned key = used[h] ? 0u : __float_as_uint(fabsf(pv[h][s])) + 1u;
+            if (key > best) { best = key; bi = lane + 32 * h; }
+          }
+          const unsigned wbest = __reduce_max_sync(0xffffffffu, best);
+          const int pr = __reduce_min_sync(0xffffffffu, (best == wbest && best != 0u) ? bi : NP);
+          const int ph = pr >> 5, pl = pr & 31;
+          // pivot row values of the panel, broadcast from its lane
+          float prv[PW];
+#pragma unroll
+          for (int t = 0; t < PW; ++t) {
+            float v = 0.f;
+#pragma unroll
+            for (int h = 0; h < PROWS; ++h) if (h == ph) v = pv[h][t];
+            prv[t] = __shfl_sync(0xffffffffu, v, pl);
+          }
+          const float piv = prv[s];
+          if (!(fabsf(piv) > thresh) || !isfinite(piv)) fail = true;
+          const float ip = 1.f / piv;
+#pragma unroll
+          for (int h = 0; h < PROWS; ++h) {
+            const int i = lane + 32 * h;
+            if (i == pr) {  // pivot row: scaled, inverse entry in column s
+#pragma unroll
+              for (int t = 0; t < PW; ++t) pv[h][t] = (t == s) ? ip : pv[h][t] * ip;
+              used[h] = true;
+            } else {
+              const float fi = pv[h][s] * ip;
+#pragma unroll
+              for (int t = 0; t < PW; ++t) pv[h][t] = (t == s) ? -fi : fmaf(-fi, prv[t], pv[h][t]);
+            }
+          }
+          if (lane == 0) {
+            prow[k0 + s] = pr;
+            pstep[pr] = k0 + s;
+          }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < PROWS; ++h) {
+        const int i = lane + 32 * h;
+        if (i < NP) {
+          *reinterpret_cast<float4*>(pan + i * PW) = make_float4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
+          *reinterpret_cast<float4*>(pan + i * PW + 4) = make_float4(pv[h][4], pv[h][5], pv[h][6], pv[h][7]);
+        }
+      }
+      if (lane == 0 && fail) misc[1] = 1.f;
+    }
+    bar_named(1, NT);
+    // ---- rank-pw update of every row, panel columns replaced -------------------------
+    if (part) {
+      float cf[PW];
+      {
+        const float4 u = *reinterpret_cast<const float4*>(pan + row * PW);
+        const float4 v = *reinterpret_cast<const float4*>(pan + row * PW + 4);
+        cf[0] = u.x; cf[1] = u.y; cf[2] = u.z; cf[3] = u.w; cf[4] = v.x; cf[5] = v.y; cf[6] = v.z; cf[7] = v.w;
+      }
+      const int st = pstep[row];
+      const bool mine = (st >= k0 && st < k0 + pw);  // this row pivoted in this panel
+      float v[SEG];
+#pragma unroll
+      for (int c = 0; c < SEG; ++c) v[c] = mine ? 0.f : r[c];
+#pragma unroll
+      for (int s = 0; s < PW; ++s) {
+        if (s < pw) {
+          const float* pr = work + prow[k0 + s] * lds + q * SEG;
+          const float f = cf[s];
+#pragma unroll
+          for (int c = 0; c < SEG; c += 4) {
+            if (q * SEG + c >= n) break;
+            const float4 t = *reinterpret_cast<const float4*>(pr + c);
+            v[c] = fmaf(f, t.x, v[c]);
+            v[c + 1] = fmaf(f, t.y, v[c + 1]);
+            v[c + 2] = fmaf(f, t.z, v[c + 2]);
+            v[c + 3] = fmaf(f, t.w, v[c + 3]);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < SEG; ++c) {
+        const int col = q * SEG + c;
+        r[c] = (col >= k0 && col < k0 + pw) ? cf[col - k0] : v[c];
+      }
+    }
+    bar_named(1, NT);  // work is rewritten by the next panel
+  }
+  __syncthreads();
+  const bool ok = misc[1] == 0.f;
+  if (part && row < n) {
+    const int qi = pstep[row];
+#pragma unroll
+    for (int c = 0; c < SEG; ++c) {
+      const int col = q * SEG + c;
+      if (col < n) {
+        const int d = prow[col];
+        if (inv) inv[qi * lds + d] = r[c];
+        if (invT) invT[d * lds + qi] = r[c];
+      }
+    }
+  }
+  __syncthreads();
+  return ok;
+}
+
 }  // namespace gsls

@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(NP == 64 ? 256 : 416, NP == 64 ? 2 : 1) k_cvf_
   gemm_tn(n, b1, b4, lds, EpiSmem{b0, lds, n, false});  // W2 = Cl Ar^T (over Pr)
   __syncthreads();
   // Minv = M1^{-1} -> b1 (row-major, over Cl), Minv^T -> b2 (over M1, read first)
-  const bool ok = gj_inverse_rows<NP>(b2, b1, b2, lds, n, gjbuf, a.rel_tol);
+  const bool ok = gj_inverse_panel<NP>(b2, b1, b1, b2, lds, n, gjbuf, a.rel_tol);  // work: b1 (Cl is dead)
   if (!ok && threadIdx.x == 0)
     raise_err(a.err ? a.err + inst : nullptr, GSLS_ERR_ILL_CONDITIONED, a.op_base + blockIdx.x);
   if (rec) {
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(NP == 64 ? 256 : 416, NP == 64 ? 2 : 1) k_cvf_
 }
 
 size_t combine_smem_bytes(int n) {
-  return (6 * (size_t)n * lds_of(n) + gj_scratch_words(n <= 64 ? 64 : 80)) * sizeof(float);
+  return (6 * (size_t)n * lds_of(n) + gjp_scratch_words(n <= 64 ? 64 : 80)) * sizeof(float);
 }
 
 int combine_threads(int n) {  // k_cvf_combine needs >= 4*NP threads for the inverse

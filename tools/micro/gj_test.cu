@@ -1,0 +1,58 @@
+// Unit test of the shared-memory Gauss-Jordan inverses (gj.cuh) on random matrices.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cmath>
+#include "../../paper_2604_07644_b200/csrc/gj.cuh"
+using namespace gsls;
+namespace gsls { void set_last_error(const char*, const char*, int) {} }
+
+template <int NP>
+__global__ void k(const float* A, float* out, int n, int* ok, int which) {
+  extern __shared__ float sm[];
+  const int lds = lds_of(n);
+  float* a = sm;
+  float* work = a + NP * lds;
+  float* invT = work + NP * lds;
+  float* scr = invT + NP * lds;
+  for (int e = threadIdx.x; e < n * lds; e += blockDim.x) a[e] = (e % lds < n) ? A[(e / lds) * n + e % lds] : 0.f;
+  __syncthreads();
+  bool r;
+  if (which == 0) r = gj_inverse_rows<NP>(a, work, invT, lds, n, scr, 1e-10f);
+  else r = gj_inverse_panel<NP>(a, work, work, invT, lds, n, scr, 1e-10f);
+  if (threadIdx.x == 0) *ok = r;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    out[e] = work[(e / n) * lds + e % n];
+    out[n * n + e] = invT[(e % n) * lds + e / n];
+  }
+}
+
+int main() {
+  for (int n : {6, 8, 13, 61, 64, 75}) {
+    std::vector<float> h(n * n);
+    srand(n);
+    for (int i = 0; i < n * n; ++i) h[i] = (rand() / (float)RAND_MAX - 0.5f) + ((i / n == i % n) ? 2.f : 0.f);
+    float *dA, *dO; int* dok;
+    cudaMalloc(&dA, n * n * 4); cudaMalloc(&dO, 2 * n * n * 4); cudaMalloc(&dok, 4);
+    cudaMemcpy(dA, h.data(), n * n * 4, cudaMemcpyHostToDevice);
+    const int sb = (3 * 80 * lds_of(n) + 4096) * 4;
+    cudaFuncSetAttribute(k<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb); cudaFuncSetAttribute(k<80>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
+    for (int which : {0, 1}) {
+      if (n <= 64) k<64><<<1, 256, sb>>>(dA, dO, n, dok, which); else k<80><<<1, 416, sb>>>(dA, dO, n, dok, which);
+      cudaError_t e = cudaDeviceSynchronize();
+      std::vector<float> o(2 * n * n); int ok;
+      cudaMemcpy(o.data(), dO, 2 * n * n * 4, cudaMemcpyDeviceToHost);
+      cudaMemcpy(&ok, dok, 4, cudaMemcpyDeviceToHost);
+      double err = 0, errT = 0;
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+          double s = 0, sT = 0;
+          for (int t = 0; t < n; ++t) { s += (double)o[i * n + t] * h[t * n + j]; sT += (double)o[n * n + i * n + t] * h[t * n + j]; }
+          err = fmax(err, fabs(s - (i == j)));
+          errT = fmax(errT, fabs(sT - (i == j)));
+        }
+      printf("n=%d %s ok=%d |inv*A-I|=%.3g |invT'*A-I|=%.3g (%s)\n", n, which ? "panel" : "rows", ok, err, errT,
+             cudaGetErrorString(e));
+    }
+  }
+}
