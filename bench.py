@@ -106,6 +106,14 @@ def measured_peaks():
         return {}
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of the roofline kernels from the committed ncu capture."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic.json")))
+    except Exception:
+        return {}
+
+
 def W(L):
     return 2 * (L - 1)
 
@@ -378,17 +386,20 @@ def run_ours(args):
               if v[2]}
     total_iters = float(its_all.sum())
     rl = {}
+    tr = ncu_traffic()
     for k in ("sls_cvf", "cvf_lqr"):
         t_ms, units, nl = fam[k]
         if nl:
             ach = units * flops_cvf(n) / (t_ms / 1e3) / 1e12
             rl[k] = {"bound": "fp32-simt", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
-                     "frac": ach / fp32_peak, "traffic": None}
+                     "frac": ach / fp32_peak, "traffic": (tr.get(k) or {}).get("dram_bytes"),
+                     "traffic_launch": (tr.get(k) or {}).get("launch")}
     t_ms, units, nl = fam["replay"]
     if nl:
         ach = total_iters * bytes_replay_iter(n, mu, c, nf, N) / (t_ms / 1e3) / 1e9
         rl["replay"] = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-                        "traffic": None}
+                        "traffic": (tr.get("replay") or {}).get("dram_bytes"),
+                        "traffic_launch": (tr.get("replay") or {}).get("launch")}
     dom = max(fam, key=lambda k: fam[k][0])
     roof = dict(rl.get(dom, {}), kernel=dom,
                 peak_source=("derived: 148 SMs x 128 FP32 FMA/clk x 2 x max SM clock (no FP32-SIMT figure in "
