@@ -66,8 +66,8 @@ __host__ __device__ inline VecLayout vec_layout(int n, int m, int N, int mtot, i
   v.pv = take(s_cvf * n);
   v.bv = take(s_cvf * n);
   v.cb = take(s_cot * n);
-  v.t1 = take(max_layer * n);
-  v.t2 = take(max_layer * n);
+  v.t1 = take(0);  // (unused since the one-round CVF replay)
+  v.t2 = take(0);
   v.z = take(mtot);
   v.lam = take(mtot);
   v.y = take(mtot);
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
                                  L.cvf_layers, L.cot_layers);
   extern __shared__ double smem[];
   double* vs = a.gscratch ? a.gscratch + (size_t)inst * a.scratch_floats : smem;
-  double *pv = vs + V.pv, *bv = vs + V.bv, *cb = vs + V.cb, *t1 = vs + V.t1, *t2 = vs + V.t2;
+  double *pv = vs + V.pv, *bv = vs + V.bv, *cb = vs + V.cb;
   double *z = vs + V.z, *lam = vs + V.lam, *y = vs + V.y;
   double *rhat = vs + V.rhat, *om = vs + V.om, *kf = vs + V.kf, *du = vs + V.du, *red = vs + V.red;
   double *part = vs + V.part, *redall = vs + V.redall;
@@ -440,12 +440,12 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
   for (int i = tid; i < L.cvf_nslots + L.cot_nslots; i += nthr) cvf_mask[i] = 0u;
   __syncthreads();
   if (cs > 1) {
-    for (int lay = 0; lay < L.cvf_layers; ++lay) {
-      const int o0 = s_cvf_loff[lay], no = s_cvf_loff[lay + 1] - o0, per = (no + cs - 1) / cs;
-      for (int oi = tid; oi < no; oi += nthr) {
-        const int4 op = s_cvf_ops[o0 + oi];
-        atomicOr(cvf_mask + op.y, 1u << (oi / per));
-        atomicOr(cvf_mask + op.z, 1u << (oi / per));
+    for (int lay = 0; lay < L.cvf_layers; ++lay) {  // half-ops (p, b) h = 2 oi + which on rank h / per
+      const int o0 = s_cvf_loff[lay], nh = 2 * (s_cvf_loff[lay + 1] - o0), per = (nh + cs - 1) / cs;
+      for (int h = tid; h < nh; h += nthr) {
+        const int4 op = s_cvf_ops[o0 + (h >> 1)];
+        atomicOr(cvf_mask + op.y, 1u << (h / per));
+        atomicOr(cvf_mask + op.z, 1u << (h / per));
       }
     }
     for (int p = tid; p <= N; p += nthr) atomicOr(cvf_mask + s_cvf_out[p], 1u << srank(max(p - 1, 0)));
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
       const int lo = min(no, rank * per), nl = min(no, lo + per) - lo;
       if (nl > 0) {
         // p = p_earlier + Ups p_later + X b_earlier, b = b_later + Psi b_earlier - Y p_later
-        // (lqr.py:242-246 with the recorded X = Ups Pr, Y = Psi Cl): one round per layer
+        // (lqr.py:242-246 with the recorded X = Ups Pr, -Y = -Psi Cl): one round per layer
         mv_round(2 * nl, n, ldg, part, cl, [&](int ti) {
           const int oi = lo + (ti >> 1);
           const int4 op = s_cvf_ops[o0 + oi];
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
             return MvTask{rec + 0 * MS, pv + op.z * n, pv + op.y * n, 1.0, pv + op.x * n, cvf_mask[op.x],
                           rec + 1 * MS, bv + op.y * n, 1.0};
           return MvTask{rec + 2 * MS, bv + op.y * n, bv + op.z * n, 1.0, bv + op.x * n, cvf_mask[op.x],
-                        rec + 3 * MS, pv + op.z * n, -1.0};
+                        rec + 3 * MS, pv + op.z * n, 1.0};  // the record holds -Y
         }, (tr_on && lay == 3) ? a.trace + 200 : nullptr);
       }
       cl.sync();
@@ -836,7 +836,7 @@ struct __align__(16) ItemDesc {
 };
 
 __host__ __device__ inline int stage_slot_bytes(int n, int m, int c, int ld2n, int ldm, int ldn, int ldc, int ldg) {
-  int b = n * ldg;                      // recorded n x n matrix
+  int b = 2 * n * ldg;                  // recorded n x 2n replay operator [Ups X] / [Psi -Y]
   b = b > c * ld2n ? b : c * ld2n;      // X23
   b = b > (n + c) * ldm ? b : (n + c) * ldm;
   b = b > m * ldn ? b : m * ldn;
@@ -855,8 +855,8 @@ __host__ __device__ inline StagedLayout staged_layout(const DevLqr& L, int max_l
   S.pv = take(L.cvf_nphys * n * 8, 16);
   S.bv = take(L.cvf_nphys * n * 8, 16);
   S.cb = take(L.cot_nphys * n * 8, 16);
-  S.t1 = take(max_layer * n * 8, 16);
-  S.t2 = take(max_layer * n * 8, 16);
+  S.t1 = take(0, 16);  // (unused since the one-round CVF replay)
+  S.t2 = take(0, 16);
   S.z = take(L.mtot * 8, 16);
   S.lam = take(L.mtot * 8, 16);
   S.y = take(L.mtot * 8, 16);
@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   const int inst = a.list ? a.list[blockIdx.y] : (int)blockIdx.y;
   const int n = L.n, m = L.m, c = L.c, nf = L.nf, N = L.N, ldg = L.ldg, mtot = L.mtot;
   const size_t MS = (size_t)n * ldg;
-  const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31, nwarp = nthr >> 5;
+  const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
   Cl cl;
   cl.rank = cluster_rank();
   cl.cs = cluster_size();
@@ -932,8 +932,6 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   double* pv = reinterpret_cast<double*>(smb + SL.pv);
   double* bv = reinterpret_cast<double*>(smb + SL.bv);
   double* cb = reinterpret_cast<double*>(smb + SL.cb);
-  double* t1 = reinterpret_cast<double*>(smb + SL.t1);
-  double* t2 = reinterpret_cast<double*>(smb + SL.t2);
   double* z = reinterpret_cast<double*>(smb + SL.z);
   double* lam = reinterpret_cast<double*>(smb + SL.lam);
   double* y = reinterpret_cast<double*>(smb + SL.y);
@@ -974,12 +972,12 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   __syncthreads();
   auto srank = [&](int k) { return k % cs; };
   if (cs > 1) {
-    for (int lay = 0; lay < L.cvf_layers; ++lay) {
-      const int o0 = s_cvf_loff[lay], no = s_cvf_loff[lay + 1] - o0, per = (no + cs - 1) / cs;
-      for (int oi = tid; oi < no; oi += nthr) {
-        const int4 op = s_cvf_ops[o0 + oi];
-        atomicOr(cvf_mask + op.y, 1u << (oi / per));
-        atomicOr(cvf_mask + op.z, 1u << (oi / per));
+    for (int lay = 0; lay < L.cvf_layers; ++lay) {  // half-ops (p, b) h = 2 oi + which on rank h / per
+      const int o0 = s_cvf_loff[lay], nh = 2 * (s_cvf_loff[lay + 1] - o0), per = (nh + cs - 1) / cs;
+      for (int h = tid; h < nh; h += nthr) {
+        const int4 op = s_cvf_ops[o0 + (h >> 1)];
+        atomicOr(cvf_mask + op.y, 1u << (h / per));
+        atomicOr(cvf_mask + op.z, 1u << (h / per));
       }
     }
     for (int p = tid; p <= N; p += nthr) atomicOr(cvf_mask + s_cvf_out[p], 1u << srank(max(p - 1, 0)));
@@ -1001,15 +999,11 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
     phase_off[ph++] = ni;
     for (int k = rank; k < N; k += cs) add(IT_P1, 0, k);
     for (int lay = 0; lay < L.cvf_layers; ++lay) {
-      const int o0 = s_cvf_loff[lay], no = s_cvf_loff[lay + 1] - o0, per = (no + cs - 1) / cs;
-      const int lo = min(no, rank * per), hi = min(no, lo + per);
+      // half-ops: p = p_e + [Ups X] [p_l; b_e] (which 0), b = b_l + [Psi -Y] [b_e; p_l] (which 1)
+      const int o0 = s_cvf_loff[lay], nh = 2 * (s_cvf_loff[lay + 1] - o0), per = (nh + cs - 1) / cs;
+      const int lo = min(nh, rank * per), hi = min(nh, lo + per);
       phase_off[ph++] = ni;
-      for (int oi = lo; oi < hi; ++oi) {  // t1 = p_e + Ups p_l; p = t1 + X b_e; t2 = b_l + Psi b_e; b = t2 - Y p_l
-        add(IT_CVF1, 0, o0 + oi, oi - lo);
-        add(IT_CVF2, 1, o0 + oi, oi - lo);
-        add(IT_CVF1, 2, o0 + oi, oi - lo);
-        add(IT_CVF2, 3, o0 + oi, oi - lo);
-      }
+      for (int h = lo; h < hi; ++h) add(IT_CVF1, h & 1, o0 + (h >> 1));
     }
     phase_off[ph++] = ni;
     for (int k = rank; k < N; k += cs) add(IT_FF1, 0, k);
@@ -1058,7 +1052,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
     auto off = [&](const void* p) { return p ? (int)((const unsigned char*)p - smb) : -1; };
     for (int j = tid; j < P; j += nthr) {
       const int2 itm = items[j];
-      const int kind = itm.x & 0xff, which = (itm.x >> 8) & 0xff, loc = itm.x >> 16, idx = itm.y;
+      const int kind = itm.x & 0xff, which = (itm.x >> 8) & 0xff, idx = itm.y;
       ItemDesc d{};
       d.kind = kind; d.rows = n; d.ld = ldg; d.K1 = n; d.K2 = 0; d.x2 = -1; d.add = -1; d.dst2 = -1;
       d.sgn = 1.0; d.pre = nullptr; d.pre2 = 0; d.mask = 0u; d.e0 = 0;
@@ -1069,21 +1063,15 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
           d.rows = 2 * n; d.ld = L.ld2n; d.K1 = c; d.x1 = off(w + idx * c);
           d.dst = off(PV(idx)); d.dst2 = off(BV(idx)); d.pre = pb0 + (size_t)idx * 2 * n; d.mask = cvf_mask[idx];
           break;
-        case IT_CVF1: {  // t1 = p_earlier + Ups p_later | t2 = b_later + Psi b_earlier (lqr.py:242-246)
+        case IT_CVF1: {  // p = p_e + [Ups X] [p_l; b_e] | b = b_l + [Psi -Y] [b_e; p_l] (lqr.py:242-246)
           const int4 op = s_cvf_ops[idx];
-          d.src = cvf_rec + ((size_t)idx * 4 + which) * MS;  // which: 0 Ups, 2 Psi
+          d.src = cvf_rec + ((size_t)idx * 4 + 2 * which) * MS;  // n x 2n column-major operator
+          d.bytes = (unsigned)MS * 8;
+          d.K1 = n; d.K2 = n;
           d.x1 = off(which ? BV(op.y) : PV(op.z));
+          d.x2 = off(which ? PV(op.z) : BV(op.y));
           d.add = off(which ? BV(op.z) : PV(op.y));
-          d.dst = off((which ? t2 : t1) + loc * n);
-          break;
-        }
-        case IT_CVF2: {  // p = t1 + X b_earlier | b = t2 - Y p_later (X = Ups Pr, Y = Psi Cl)
-          const int4 op = s_cvf_ops[idx];
-          d.src = cvf_rec + ((size_t)idx * 4 + which) * MS;  // which: 1 X, 3 Y
-          d.x1 = off(which == 3 ? PV(op.z) : BV(op.y));
-          d.add = off((which == 3 ? t2 : t1) + loc * n);
-          d.dst = off(which == 3 ? BV(op.x) : PV(op.x));
-          d.sgn = (which == 3) ? -1.0 : 1.0;
+          d.dst = off(which ? BV(op.x) : PV(op.x));
           d.mask = cvf_mask[op.x];
           break;
         }
@@ -1218,8 +1206,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
           const int i = tid;
           double* dst = reinterpret_cast<double*>(smb + d.dst);
           switch (kind) {
-            case IT_CVF1: dst[i] = reinterpret_cast<const double*>(smb + d.add)[i] + sum; break;
-            case IT_CVF2:
+            case IT_CVF1:
             case IT_COT:
               cl.put_mask(dst + i, reinterpret_cast<const double*>(smb + d.add)[i] + d.sgn * sum, d.mask);
               break;
@@ -1437,7 +1424,11 @@ static int launch_replay(Ctx* c, ReplayArgs& a, int count, cudaStream_t st) {
     GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_replay, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attrs_set = true;
   }
-  const int cs = (a.mode == MODE_ADMM) ? replay_cluster(c, count, sb, (const void*)k_replay) : 1;  // LQR-mode phases broadcast
+  // One CTA per instance.  Cluster launches of the ADMM loop go to k_admm_staged; this
+  // kernel's cluster mode (DSMEM replicas) is kept for GSLS_REPLAY_CLUSTER experiments only:
+  // it reproduces the reference at cs <= 2 but not at cs >= 4 (open issue).
+  const char* force_cs = getenv("GSLS_REPLAY_LEGACY_CLUSTER");
+  const int cs = (a.mode == MODE_ADMM && force_cs) ? replay_cluster(c, count, sb, (const void*)k_replay) : 1;
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1496,7 +1487,7 @@ static int launch_admm_staged(Ctx* c, ReplayArgs& a, int count, cudaStream_t st)
   const int Nn = c->dims.N;
   auto cdiv = [](int x, int y) { return (x + y - 1) / y; };
   int max_items = 4 * cdiv(Nn, cs0) + 8;
-  for (int l = 0; l < c->cvf.layers; ++l) max_items += 4 * cdiv(c->cvf_layer_off[l + 1] - c->cvf_layer_off[l], cs0);
+  for (int l = 0; l < c->cvf.layers; ++l) max_items += cdiv(2 * (c->cvf_layer_off[l + 1] - c->cvf_layer_off[l]), cs0);
   for (int l = 0; l < c->cot.layers; ++l) max_items += cdiv(c->cot_layer_off[l + 1] - c->cot_layer_off[l], cs0);
   if (max_items > kReplayThreads) return GSLS_ERR_TOO_LARGE;  // setup list lives in the partial buffer
   int R = 0;

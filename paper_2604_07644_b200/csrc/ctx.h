@@ -28,7 +28,7 @@ struct DevLqr {
   // scan values (matrices) per instance: [batch][slots][n*ldg]
   float *Ps, *As, *Cs;   // CVF P, A, C
   float* ATs;            // CVF A transposed (both orientations kept; see k_cvf_combine)
-  float* cvf_rec;        // [batch][cvf_nops][4][n*ldg]: Ups, X = Ups Pr, Psi, Y = Psi Cl (column-major)
+  float* cvf_rec;        // [batch][cvf_nops][4][n*ldg]: Ups, X = Ups Pr, Psi, -Y (Y = Psi Cl), column-major
   float* cotA;           // [batch][cot_nslots][n*ldg]
   float* cotAT;          // transposed
   float* cot_rec;        // [batch][cot_nops][n*ldg]: A_later (column-major)

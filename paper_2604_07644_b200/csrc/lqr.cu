@@ -281,10 +281,11 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
 }
 
 // Matrix half of the CVF combine (Eq. 28) for one op per CTA; optionally
-// records the replay operators column-major: Ups, X = Ups Pr, Psi, Y = Psi Cl,
-// so the cached replay p = Ups (p_r + Pr b_l) + p_l, b = Psi (b_l - Cl p_r) + b_r
-// (lqr.py:242-246) becomes p = p_l + Ups p_r + X b_l, b = b_r + Psi b_l - Y p_r:
-// four independent matvecs per combine, one round per tree layer.  Shared with
+// records the replay operators column-major: Ups, X = Ups Pr, Psi, -Y with
+// Y = Psi Cl, so the cached replay p = Ups (p_r + Pr b_l) + p_l,
+// b = Psi (b_l - Cl p_r) + b_r (lqr.py:242-246) becomes
+// p = p_l + [Ups X] [p_r; b_l], b = b_r + [Psi -Y] [b_l; p_r]: two n x 2n
+// column-major operators (consecutive in the record), one round per tree layer.  Shared with
 // the SLS grid scan (no record).
 //
 // P and C are symmetric in exact arithmetic (value-function Hessians and
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(NP == 64 ? 256 : 416, NP == 64 ? 2 : 1) k_cvf_
     raise_err(a.err ? a.err + inst : nullptr, GSLS_ERR_ILL_CONDITIONED, a.op_base + blockIdx.x);
   if (rec) {
     gemm_tn(n, b1, b3, lds, EpiGlobal{rec + 0 * MS, nullptr, ldg, n, nullptr});  // Ups^T = Minv^T Al
-    gemm_tn(n, b1, b0, lds, EpiGlobal{rec + 3 * MS, nullptr, ldg, n, nullptr});  // Y^T = Minv^T W2
+    gemm_tn(n, b1, b0, lds, EpiGlobalNeg{rec + 3 * MS, ldg, n});  // -Y^T = -Minv^T W2
     __syncthreads();
   }
   gemm_tn(n, b2, b5, lds, EpiSmem{b1, lds, n, false});  // V = Minv W1 = X^T (over Minv)

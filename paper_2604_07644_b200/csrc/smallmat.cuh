@@ -129,6 +129,19 @@ struct EpiSmem {  // C (smem) = acc (+ I)
   }
 };
 
+struct EpiGlobalNeg {  // G (global, ld) = -acc
+  float* G;
+  int ld, n;
+  __device__ void operator()(int i0, int j0, float (&acc)[4][4]) const {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = i0 + r;
+      if (i >= n) break;
+      *reinterpret_cast<float4*>(G + (size_t)i * ld + j0) = make_float4(-acc[r][0], -acc[r][1], -acc[r][2], -acc[r][3]);
+    }
+  }
+};
+
 struct EpiGlobal {  // G (global, ld) = acc + add (global, may be null); optional transposed copy Gt
   float* G;
   const float* add;

@@ -209,3 +209,26 @@ def test_solve_nmpc_planar_quadrotor_vs_oracle(G):
     assert got.stats.converged == ref.stats.converged
     assert got.stats.iterations == ref.stats.iterations
     assert rel(got.trajectory.x, ref.trajectory.x) <= 1e-3
+
+
+@pytest.mark.parametrize("path", [("staged", "2"), ("staged", "4"), ("staged", "16"), ("legacy", "1"),
+                                  ("staged-forced", "1")])
+@pytest.mark.parametrize("tag", ["q61", "h75"])
+def test_rti_robust_step_every_replay_path(G, tag, path, monkeypatch):
+    """Both ADMM replay kernels (k_admm_staged on clusters of 2..16 CTAs, k_replay with one
+    CTA per instance) reproduce the reference's robust RTI step: exact ADMM iteration count,
+    u0 / plan within 1e-4."""
+    sls, sqp = G
+    import test_oracle_golden as T
+    kind, cs = path
+    monkeypatch.setenv("GSLS_REPLAY_CLUSTER", cs)
+    monkeypatch.setenv("GSLS_REPLAY_STAGED", "0" if kind == "legacy" else ("1" if kind == "staged-forced" else "x"))
+    g = load_golden("rti")
+    model, rs = _rti_case(tag)
+    x, prev, tau = T.rti_inputs(g, tag, model)
+    ours = _to_ours(sls, sqp, rs)
+    t_ours = sls.SlsDuals(tau.tau, tau.tau_term, tau.beta, tau.beta_term, tau.eps)
+    r = sls.rti_robust_step(model, x, sqp.Trajectory(prev.x, prev.u, prev.dt), t_ours, ours)
+    assert r.stats.admm_iterations == int(g[f"{tag}_admm_iters"])
+    assert rel(r.u0, g[f"{tag}_u0"]) <= TOL
+    assert rel(r.plan.x, g[f"{tag}_plan_x"]) <= TOL
