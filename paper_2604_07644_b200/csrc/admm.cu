@@ -227,14 +227,42 @@ __device__ inline void warp_stage_mv(const float* __restrict__ M, int ld, int rb
   acc[0] = a0; acc[1] = a1; acc[2] = a2; acc[3] = a3;
 }
 
+// 64-row variant: lane (rq, g) = (lane & 15, lane >> 4) covers rows 64rb + 4rq .. +3, k = g, g + 2, ...;
+// 16 lanes of equal g read one full 256-byte column segment per k (better DRAM locality
+// for the batched replay, where the recorded operators stream from HBM).
+__device__ inline void warp_cm_partial64(const float* __restrict__ Mcm, int ldg, int rb, const double* x, int k0,
+                                         int k1, double (&acc)[4]) {
+  const int lane = threadIdx.x & 31;
+  const int rq = lane & 15, g = lane >> 4;
+  const int row0 = rb * 64 + 4 * rq;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (row0 < ldg) {
+    const float* p = Mcm + row0;
+#pragma unroll 8
+    for (int k = k0 + g; k < k1; k += 2) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(p + (size_t)k * ldg));
+      const double xk = x[k];
+      a0 = fma((double)v.x, xk, a0);
+      a1 = fma((double)v.y, xk, a1);
+      a2 = fma((double)v.z, xk, a2);
+      a3 = fma((double)v.w, xk, a3);
+    }
+  }
+  a0 += __shfl_xor_sync(0xffffffffu, a0, 16);
+  a1 += __shfl_xor_sync(0xffffffffu, a1, 16);
+  a2 += __shfl_xor_sync(0xffffffffu, a2, 16);
+  a3 += __shfl_xor_sync(0xffffffffu, a3, 16);
+  acc[0] = a0; acc[1] = a1; acc[2] = a2; acc[3] = a3;
+}
+
 // acc = M x (+ sgn2 M2 x2) over k in [k0, k1) for one 32-row block.
 __device__ inline void warp_cm_partial2(const float* __restrict__ M, const double* x, const float* __restrict__ M2,
                                         const double* x2, double sgn2, int ldg, int rb, int k0, int k1,
                                         double (&acc)[4]) {
-  warp_cm_partial(M, ldg, rb, x, k0, k1, acc);
+  warp_cm_partial64(M, ldg, rb, x, k0, k1, acc);
   if (M2) {
     double b[4];
-    warp_cm_partial(M2, ldg, rb, x2, k0, k1, b);
+    warp_cm_partial64(M2, ldg, rb, x2, k0, k1, b);
 #pragma unroll
     for (int r = 0; r < 4; ++r) acc[r] = fma(sgn2, b[r], acc[r]);
   }
@@ -271,20 +299,20 @@ __device__ void mv_round(int ntask, int n, int ldg, double* part, const Cl& cl, 
   auto D = [&](int j) { if (dbg && threadIdx.x == 0) dbg[j] = clock64(); };
   D(0);
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, nwarp = nthr >> 5, lane = tid & 31;
-  const int RB = (n + 31) >> 5;
+  const int RB = (n + 63) >> 6;  // 64-row blocks
   const int base = ntask * RB;
   int KS = 1;
-  while (KS < 4 && base * KS * 2 <= nwarp) KS <<= 1;
+  while (KS < 4 && base * KS * 2 <= nwarp / 2) KS <<= 1;  // partials: base * KS * 64 <= 512
   if (KS == 1) {
     for (int t = warp; t < base; t += nwarp) {
       const int ti = t / RB, rb = t - ti * RB;
       const MvTask d = desc(ti);
       double acc[4];
       warp_cm_partial2(d.M, d.x, d.M2, d.x2, d.sgn2, ldg, rb, 0, n, acc);
-      if ((lane >> 3) == 0) {
+      if ((lane >> 4) == 0) {
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const int row = rb * 32 + 4 * (lane & 7) + r;
+          const int row = rb * 64 + 4 * (lane & 15) + r;
           if (row < n) {
             const double v = d.add[row] + d.sgn * acc[r];
             cl.put_mask(d.y + row, v, d.mask);
@@ -295,7 +323,7 @@ __device__ void mv_round(int ntask, int n, int ldg, double* part, const Cl& cl, 
     __syncthreads();
     return;
   }
-  const int kc = ((n + KS - 1) / KS + 3) & ~3;  // slice length, multiple of 4 (keeps the lane interleave)
+  const int kc = ((n + KS - 1) / KS + 1) & ~1;  // slice length, even (keeps the 2-way lane interleave)
   for (int t = warp; t < base * KS; t += nwarp) {
     const int tb = t / KS, ks = t - tb * KS;
     const int ti = tb / RB, rb = tb - ti * RB;
@@ -305,20 +333,20 @@ __device__ void mv_round(int ntask, int n, int ldg, double* part, const Cl& cl, 
     const int k0 = ks * kc;
     warp_cm_partial2(d.M, d.x, d.M2, d.x2, d.sgn2, ldg, rb, k0, min(n, k0 + kc), acc);
     if (t == 0) D(2);
-    if ((lane >> 3) == 0) {
+    if ((lane >> 4) == 0) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r) part[(tb * KS + ks) * 32 + 4 * (lane & 7) + r] = acc[r];
+      for (int r = 0; r < 4; ++r) part[(tb * KS + ks) * 64 + 4 * (lane & 15) + r] = acc[r];
     }
   }
   __syncthreads();
   D(3);
-  for (int e = tid; e < base * 32; e += nthr) {
-    const int tb = e >> 5, ro = e & 31;
+  for (int e = tid; e < base * 64; e += nthr) {
+    const int tb = e >> 6, ro = e & 63;
     const int ti = tb / RB, rb = tb - ti * RB;
-    const int row = rb * 32 + ro;
+    const int row = rb * 64 + ro;
     if (row >= n) continue;
     double s = 0.0;
-    for (int ks = 0; ks < KS; ++ks) s += part[(tb * KS + ks) * 32 + ro];
+    for (int ks = 0; ks < KS; ++ks) s += part[(tb * KS + ks) * 64 + ro];
     const MvTask d = desc(ti);
     const double v = d.add[row] + d.sgn * s;
     cl.put_mask(d.y + row, v, d.mask);
@@ -1109,7 +1137,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   __syncthreads();
   int pi = 0, pslot = 0;  // producer (thread 0): next item (mod P), slot to fill
   auto issue = [&]() {
-    if (tid != 0 || P == 0) return;
+    if (tid != nthr - 32 || P == 0) return;  // last warp: off the epilogue rows (tid < rows)
     bulk_load(ring + (size_t)pslot * SL.slot, desc[pi].src, desc[pi].bytes, full + pslot);
     if (++pi == P) pi = 0;
     if (++pslot == R) pslot = 0;
