@@ -259,13 +259,42 @@ __device__ inline void warp_cm_partial64(const float* __restrict__ Mcm, int ldg,
 __device__ inline void warp_cm_partial2(const float* __restrict__ M, const double* x, const float* __restrict__ M2,
                                         const double* x2, double sgn2, int ldg, int rb, int k0, int k1,
                                         double (&acc)[4]) {
-  warp_cm_partial64(M, ldg, rb, x, k0, k1, acc);
-  if (M2) {
-    double b[4];
-    warp_cm_partial64(M2, ldg, rb, x2, k0, k1, b);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) acc[r] = fma(sgn2, b[r], acc[r]);
+  if (!M2) {
+    warp_cm_partial64(M, ldg, rb, x, k0, k1, acc);
+    return;
   }
+  // both operators in one loop: twice the loads in flight per lane
+  const int lane = threadIdx.x & 31;
+  const int rq = lane & 15, g = lane >> 4;
+  const int row0 = rb * 64 + 4 * rq;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+  if (row0 < ldg) {
+    const float* p = M + row0;
+    const float* q = M2 + row0;
+#pragma unroll 4
+    for (int k = k0 + g; k < k1; k += 2) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(p + (size_t)k * ldg));
+      const float4 u = __ldg(reinterpret_cast<const float4*>(q + (size_t)k * ldg));
+      const double xk = x[k], yk = x2[k];
+      a0 = fma((double)v.x, xk, a0);
+      a1 = fma((double)v.y, xk, a1);
+      a2 = fma((double)v.z, xk, a2);
+      a3 = fma((double)v.w, xk, a3);
+      b0 = fma((double)u.x, yk, b0);
+      b1 = fma((double)u.y, yk, b1);
+      b2 = fma((double)u.z, yk, b2);
+      b3 = fma((double)u.w, yk, b3);
+    }
+  }
+  a0 = fma(sgn2, b0, a0);
+  a1 = fma(sgn2, b1, a1);
+  a2 = fma(sgn2, b2, a2);
+  a3 = fma(sgn2, b3, a3);
+  a0 += __shfl_xor_sync(0xffffffffu, a0, 16);
+  a1 += __shfl_xor_sync(0xffffffffu, a1, 16);
+  a2 += __shfl_xor_sync(0xffffffffu, a2, 16);
+  a3 += __shfl_xor_sync(0xffffffffu, a3, 16);
+  acc[0] = a0; acc[1] = a1; acc[2] = a2; acc[3] = a3;
 }
 
 // One matvec of a replay round: y = add + sgn * M x (M column-major, fp32).
