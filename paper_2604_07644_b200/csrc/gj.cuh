@@ -206,6 +206,7 @@ __device__ bool gj_inverse_panel(const float* a, float* work, float* inv, float*
   constexpr int PW = 8;                                   // panel width
   constexpr int RPL = NP / 32;                            // rows per lane in the panel warp (2 for 64)
   static_assert(NP % 32 == 0 || NP == 80, "panel warp covers NP rows");
+  static_assert(NP <= 128, "row index packed in 7 key bits");
   float* pan = scratch;                                   // [NP][PW] eliminated panel
   int* prow = reinterpret_cast<int*>(pan + NP * PW);      // [NP] pivot row of step k
   int* pstep = prow + NP;                                 // [NP] step at which row i pivoted (-1)
@@ -260,16 +261,19 @@ __device__ bool gj_inverse_panel(const float* a, float* work, float* inv, float*
 #pragma unroll
       for (int s = 0; s < PW; ++s) {
         if (s < pw) {
-          // argmax |pv[i][s]| over unused rows (key = bits(|x|) + 1 orders like |x|)
+          // argmax |pv[i][s]| over unused rows with one redux: key = the bits of |x| with
+          // the low 7 mantissa bits replaced by (127 - row), so the lowest row wins ties
+          // (as LAPACK i*amax) and near-ties closer than 2^-16 relative
           unsigned best = 0u;
-          int bi = NP;
 #pragma unroll
           for (int h = 0; h < PROWS; ++h) {
-            const unsigned key = used[h] ? 0u : __float_as_uint(fabsf(pv[h][s])) + 1u;
-            if (key > best) { best = key; bi = lane + 32 * h; }
+            const int i = lane + 32 * h;
+            const unsigned key =
+                used[h] ? 0u : ((__float_as_uint(fabsf(pv[h][s])) & ~127u) | (unsigned)(127 - i));
+            best = max(best, key);
           }
           const unsigned wbest = __reduce_max_sync(0xffffffffu, best);
-          const int pr = __reduce_min_sync(0xffffffffu, (best == wbest && best != 0u) ? bi : NP);
+          const int pr = 127 - (int)(wbest & 127u);
           const int ph = pr >> 5, pl = pr & 31;
           // pivot row values of the panel, broadcast from its lane
           float prv[PW];
@@ -282,7 +286,7 @@ __device__ bool gj_inverse_panel(const float* a, float* work, float* inv, float*
           }
           const float piv = prv[s];
           if (!(fabsf(piv) > thresh) || !isfinite(piv)) fail = true;
-          const float ip = 1.f / piv;
+          const float ip = __frcp_rn(piv);
 #pragma unroll
           for (int h = 0; h < PROWS; ++h) {
             const int i = lane + 32 * h;
