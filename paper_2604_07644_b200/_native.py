@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgsls.so")
+LIB_PATH = os.environ.get("GSLS_LIB") or os.path.join(_HERE, "libgsls.so")  # GSLS_LIB: A/B builds
 
 c_int32_p = ctypes.POINTER(ctypes.c_int32)
 c_void_p = ctypes.c_void_p
