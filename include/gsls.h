@@ -151,6 +151,14 @@ int gsls_admm_solve_qp(gsls_ctx* ctx, const gsls_qp_t* qp, const gsls_admm_setti
                        gsls_admm_state_t* state, gsls_admm_stats_t* stats, double* dx, double* du,
                        void* stream);
 
+/* The first ADMM cache build (LQR factorization at the augmented costs, all
+ * instances, at rho (B) float64) issued ahead of gsls_admm_solve_qp, which then
+ * skips it.  Lets the caller overlap the build with independent work on another
+ * stream (the robust RTI step overlaps it with the SLS synthesis: the
+ * factorization of admm.py:171-178 does not depend on the tightened offsets f);
+ * the caller orders the streams.  Same result as the solve's own first build. */
+int gsls_admm_build_cache(gsls_ctx* ctx, const gsls_qp_t* qp, const double* rho, void* stream);
+
 /* Exports the last solve held by ctx: K (B,N,nu,nx) and P (B,N+1,nx,nx) of
  * the current factorization, k (B,N,nu) and p (B,N+1,nx) of the last replay
  * (the LqrSolution the reference returns in AdmmResult.solution, admm.py:203).

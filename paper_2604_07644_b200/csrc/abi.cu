@@ -17,6 +17,7 @@ int lqr_solve(Ctx* c, const gsls_qp_t* qp, int generation, double* dx, double* d
               double* p, cudaStream_t st);
 int lqr_solve_cached(Ctx* c, const gsls_qp_t* qp, const double* q, const double* r, const double* qN,
                      int generation, double* dx, double* du, double* k, double* p, cudaStream_t st);
+int admm_build(Ctx* c, const gsls_qp_t* qp, const double* rho, cudaStream_t st);
 int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_admm_state_t* state,
                gsls_admm_stats_t* stats, double* dx, double* du, cudaStream_t st);
 int ctx_export(Ctx* c, float* K, double* k, float* P, double* p, cudaStream_t st);
@@ -132,6 +133,13 @@ int gsls_admm_solve_qp(gsls_ctx* ctx, const gsls_qp_t* qp, const gsls_admm_setti
   int rc = check_qp(qp, ctx->impl->dims);
   if (rc) return rc;
   return admm_solve(ctx->impl, qp, settings, state, stats, dx, du, (cudaStream_t)stream);
+}
+
+int gsls_admm_build_cache(gsls_ctx* ctx, const gsls_qp_t* qp, const double* rho, void* stream) {
+  if (!ctx || !rho) return fail_null("argument");
+  int rc = check_qp(qp, ctx->impl->dims);
+  if (rc) return rc;
+  return admm_build(ctx->impl, qp, rho, (cudaStream_t)stream);
 }
 
 int gsls_ctx_export_solution(gsls_ctx* ctx, float* K, double* k, float* P, double* p, void* stream) {

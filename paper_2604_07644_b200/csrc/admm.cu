@@ -1676,10 +1676,13 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
   std::vector<int> builds(B, 0), list(B), status(B);
   for (int i = 0; i < B; ++i) list[i] = i;
   c->cache_valid = false;  // the ADMM rebuilds the cache at augmented costs
+  bool prebuilt = c->admm_prebuilt;  // first build already issued by admm_build (possibly on another stream)
+  c->admm_prebuilt = false;
   while (!list.empty()) {
     const int cnt = (int)list.size();
     GSLS_CUDA_CHECK(cudaMemcpyAsync(c->d_inst_list, list.data(), sizeof(int) * cnt, cudaMemcpyHostToDevice, st));
-    int rc = build_cache(c, qp, state->rho, c->d_inst_list, cnt, st);
+    int rc = prebuilt ? GSLS_OK : build_cache(c, qp, state->rho, c->d_inst_list, cnt, st);
+    prebuilt = false;
     if (rc) return rc;
     for (int i : list) builds[i]++;
     ReplayArgs a{};
@@ -1706,6 +1709,18 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
   }
   GSLS_CUDA_CHECK(cudaMemcpyAsync(stats->cache_builds, builds.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice, st));
   GSLS_CUDA_CHECK(cudaStreamSynchronize(st));
+  return GSLS_OK;
+}
+
+// The ADMM's first cache build (all instances, at state rho) ahead of the solve, so a
+// caller can overlap it with independent work on another stream (the robust RTI step
+// builds it while the SLS synthesis runs: the factorization does not depend on the
+// tightened offsets f).  The next admm_solve on this context skips that build; the
+// caller orders the two streams.
+int admm_build(Ctx* c, const gsls_qp_t* qp, const double* rho, cudaStream_t st) {
+  int rc = build_cache(c, qp, rho, nullptr, c->dims.batch, st);
+  if (rc) return rc;
+  c->admm_prebuilt = true;
   return GSLS_OK;
 }
 

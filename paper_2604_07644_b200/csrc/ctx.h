@@ -76,6 +76,7 @@ struct Ctx {
   int generation = -1;         // cache stamp (single-generation API); -1 = none
   std::vector<int> gen_host;   // per-instance stamp for the batched API
   bool cache_valid = false;
+  bool admm_prebuilt = false;  // gsls_admm_build_cache ran: the next ADMM solve skips its first build
   void* sls = nullptr;         // SLS workspace (sls.cu), allocated on first use
 };
 

@@ -127,6 +127,10 @@ class RtiEngine:
         self.cost = d(batch)
         self._weights_written = False
         self.launches_per_step = 0
+        # side stream for the ADMM's first cache build, overlapped with the SLS synthesis
+        import os
+        self.overlap = robust and os.environ.get("GSLS_OVERLAP", "1") != "0"
+        self.side = torch.cuda.Stream(device=dev) if self.overlap else None
 
     # -- pieces ------------------------------------------------------------------
     def _reset_admm(self, warm: DeviceAdmmState | None = None):
@@ -149,6 +153,18 @@ class RtiEngine:
         self._weights_written = True
         if E is not None:
             self.E.copy_(E)
+        if not warm_admm:
+            self._reset_admm()
+        prebuilt = False
+        if self.robust and self.overlap:
+            # The ADMM's first factorization depends on A, B, Q, R, S, C, D and rho only, not on
+            # the tightened offsets f: build it on a side stream while the SLS synthesis runs.
+            main = torch.cuda.current_stream()
+            self.side.wait_stream(main)
+            with torch.cuda.stream(self.side):
+                nat.check(lib.gsls_admm_build_cache(ctx.handle, ctypes.byref(qs), self.state.rho.data_ptr(),
+                                                    self.side.cuda_stream), "admm build")
+            prebuilt = True
         if self.robust:
             if tau is not None:
                 self.tau.copy_(tau)
@@ -163,8 +179,8 @@ class RtiEngine:
             nat.check(lib.gsls_sls_tighten(ctx.handle, ctypes.byref(qs), _p(self.h), _p(self.hf), S), "tighten")
             nat.check(lib.gsls_apply_tightening(ctx.handle, _p(qp.f), _p(qp.fN), _p(self.h), _p(self.hf), S),
                       "apply_tightening")
-        if not warm_admm:
-            self._reset_admm()
+        if prebuilt:
+            torch.cuda.current_stream().wait_stream(self.side)
         sa, ss, st = self.state.cstruct(), self.stats.cstruct(), self.admm_settings.cstruct()
         nat.check(lib.gsls_admm_solve_qp(ctx.handle, ctypes.byref(qs), ctypes.byref(st), ctypes.byref(sa),
                                          ctypes.byref(ss), self.dx.data_ptr(), _p(self.du), S), "admm.solve_qp")
