@@ -232,3 +232,34 @@ def test_rti_robust_step_every_replay_path(G, tag, path, monkeypatch):
     assert r.stats.admm_iterations == int(g[f"{tag}_admm_iters"])
     assert rel(r.u0, g[f"{tag}_u0"]) <= TOL
     assert rel(r.plan.x, g[f"{tag}_plan_x"]) <= TOL
+
+
+def test_large_batch_one_cta_per_instance_matches_single(G):
+    """B = 160 > 148 / 2 runs k_replay with one CTA per instance (the batched-throughput
+    path); sampled instances equal the same instances solved alone (cluster path)."""
+    sls, sqp = G
+    import torch
+    import test_oracle_golden as T
+    from paper_2604_07644_b200.engine import RtiEngine
+    from paper_2604_07644_b200.sls import ragged_to_cells
+    g = load_golden("rti")
+    model, rs = _rti_case("q61")
+    x, prev, tau = T.rti_inputs(g, "q61", model)
+    ours = _to_ours(sls, sqp, rs)
+    B = 160
+    rng = np.random.default_rng(7)
+    xs = x[None] + 0.002 * rng.standard_normal((B, model.nx)) * (np.arange(B)[:, None] > 0)
+    eng = RtiEngine(model, prev.N, B, ours)
+    d = lambda a: torch.as_tensor(a, dtype=torch.float64, device="cuda").contiguous()  # noqa: E731
+    tc = np.stack([ragged_to_cells(tau.tau, prev.N, (model.nc,))] * B)
+    tt = np.stack([tau.tau_term] * B)
+    eng.step(d(xs), d(np.stack([prev.x] * B)), d(np.stack([prev.u] * B)), tau=d(tc), tau_term=d(tt))
+    its = eng.stats.iterations.cpu().numpy()
+    u0 = eng.u0.cpu().numpy()
+    assert its[0] == int(g["q61_admm_iters"])
+    assert rel(u0[0], g["q61_u0"]) <= TOL
+    for i in (1, 77, 159):
+        r = sls.rti_robust_step(model, xs[i], sqp.Trajectory(prev.x, prev.u, prev.dt),
+                                sls.SlsDuals(tau.tau, tau.tau_term, tau.beta, tau.beta_term, tau.eps), ours)
+        assert r.stats.admm_iterations == its[i]
+        assert np.abs(r.u0 - u0[i]).max() <= 1e-9
