@@ -372,4 +372,247 @@ __device__ bool gj_inverse_panel(const float* a, float* work, float* inv, float*
   return ok;
 }
 
+
+// Look-ahead variant of gj_inverse_panel: a dedicated panel warp (warp NT/32,
+// so blockDim >= 4*NP + 32) factors panel t+1 while the row threads apply panel
+// t's rank-8 update to their registers.  The panel warp first brings panel
+// t+1's columns up to date itself (from the published rows and panel t), so
+// the two overlap completely; two barriers per panel.  Same arithmetic and
+// pivot choices as gj_inverse_panel.  Scratch: gjl_scratch_words(NP).
+constexpr int gjl_scratch_words(int NP) { return 2 * NP * 8 + 2 * NP + 16; }
+
+template <int NP>
+__device__ bool gj_inverse_lookahead(const float* a, float* work, float* inv, float* invT, int lds, int n,
+                                     float* scratch, float rel_tol) {
+  constexpr int SEG = NP / 4;
+  constexpr int NT = NP * 4;  // row threads
+  constexpr int NW = NT / 32;
+  constexpr int PW = 8;
+  constexpr int PROWS = (NP + 31) / 32;
+  static_assert(NP <= 128, "row index packed in 7 key bits");
+  float* pan0 = scratch;                                   // [2][NP][PW] eliminated panels (double buffer)
+  int* prow = reinterpret_cast<int*>(pan0 + 2 * NP * PW);  // [NP] pivot row of step k
+  int* pstep = prow + NP;                                  // [NP] step at which row i pivoted (-1)
+  float* misc = reinterpret_cast<float*>(pstep + NP);      // [0] max|a|, [1] fail
+  const int tid = threadIdx.x;
+  const bool part = tid < NT;
+  const bool pwarp = (tid >> 5) == NW;  // the panel warp
+  const int row = tid >> 2, q = tid & 3, lane = tid & 31, warp = tid >> 5;
+  float r[SEG];
+  float mx = 0.f;
+#pragma unroll
+  for (int c = 0; c < SEG; ++c) {
+    const int col = q * SEG + c;
+    r[c] = (part && row < n && col < n) ? a[row * lds + col] : 0.f;
+    mx = fmaxf(mx, fabsf(r[c]));
+  }
+  mx = warp_max(mx);
+  if (part && lane == 0) pan0[warp] = mx;
+  for (int i = tid; i < NP; i += blockDim.x) pstep[i] = -1;
+  __syncthreads();  // a fully read (work / inv may alias it from here on)
+  if (tid == 0) {
+    float m2 = 0.f;
+    for (int w = 0; w < NW; ++w) m2 = fmaxf(m2, pan0[w]);
+    misc[0] = m2;
+    misc[1] = 0.f;
+  }
+  // zero the columns past round_up(n, 4) the 8-wide panel loads may touch (never published)
+  for (int e = tid; e < n * 8; e += blockDim.x) {
+    const int i = e >> 3, cc = ((n + 3) & ~3) + (e & 7);
+    if (cc < lds) work[i * lds + cc] = 0.f;
+  }
+  // publish the rows (pre-panel-0 state)
+  if (part && row < n) {
+#pragma unroll
+    for (int c = 0; c < SEG; c += 4)
+      if (q * SEG + c < n)
+        *reinterpret_cast<float4*>(work + row * lds + q * SEG + c) = make_float4(r[c], r[c + 1], r[c + 2], r[c + 3]);
+  }
+  __syncthreads();
+  const float thresh = rel_tol * misc[0];
+  const int npan = (n + PW - 1) / PW;
+  // Panel warp: eliminate panel t (columns k0..k0+pw) from its values pv (post panels < t).
+  auto factor = [&](float (&pv)[PROWS][PW], int k0, float* pan) {
+    const int pw = min(PW, n - k0);
+    bool used[PROWS];
+#pragma unroll
+    for (int h = 0; h < PROWS; ++h) {
+      const int i = lane + 32 * h;
+      used[h] = !(i < n) || pstep[i] >= 0;
+    }
+    bool fail = false;
+#pragma unroll
+    for (int s = 0; s < PW; ++s) {
+      if (s < pw) {
+        unsigned best = 0u;
+#pragma unroll
+        for (int h = 0; h < PROWS; ++h) {
+          const int i = lane + 32 * h;
+          const unsigned key = used[h] ? 0u : ((__float_as_uint(fabsf(pv[h][s])) & ~127u) | (unsigned)(127 - i));
+          best = max(best, key);
+        }
+        const unsigned wbest = __reduce_max_sync(0xffffffffu, best);
+        const int pr = 127 - (int)(wbest & 127u);
+        const int ph = pr >> 5, pl = pr & 31;
+        float prv[PW];
+#pragma unroll
+        for (int t = 0; t < PW; ++t) {
+          float v = 0.f;
+#pragma unroll
+          for (int h = 0; h < PROWS; ++h) if (h == ph) v = pv[h][t];
+          prv[t] = __shfl_sync(0xffffffffu, v, pl);
+        }
+        const float piv = prv[s];
+        if (!(fabsf(piv) > thresh) || !isfinite(piv)) fail = true;
+        const float ip = __frcp_rn(piv);
+#pragma unroll
+        for (int h = 0; h < PROWS; ++h) {
+          const int i = lane + 32 * h;
+          if (i == pr) {
+#pragma unroll
+            for (int t = 0; t < PW; ++t) pv[h][t] = (t == s) ? ip : pv[h][t] * ip;
+            used[h] = true;
+          } else {
+            const float fi = pv[h][s] * ip;
+#pragma unroll
+            for (int t = 0; t < PW; ++t) pv[h][t] = (t == s) ? -fi : fmaf(-fi, prv[t], pv[h][t]);
+          }
+        }
+        if (lane == 0) {
+          prow[k0 + s] = pr;
+          pstep[pr] = k0 + s;
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < PROWS; ++h) {
+      const int i = lane + 32 * h;
+      if (i < NP) {
+        *reinterpret_cast<float4*>(pan + i * PW) = make_float4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
+        *reinterpret_cast<float4*>(pan + i * PW + 4) = make_float4(pv[h][4], pv[h][5], pv[h][6], pv[h][7]);
+      }
+    }
+    if (lane == 0 && fail) misc[1] = 1.f;
+  };
+  if (pwarp) {  // panel 0 from the published rows
+    float pv[PROWS][PW];
+#pragma unroll
+    for (int h = 0; h < PROWS; ++h) {
+      const int i = lane + 32 * h;
+#pragma unroll
+      for (int t = 0; t < PW; ++t) pv[h][t] = (i < n && t < min(PW, n)) ? work[i * lds + t] : 0.f;
+    }
+    factor(pv, 0, pan0);
+  }
+  __syncthreads();
+  for (int t = 0; t < npan; ++t) {
+    const int k0 = t * PW, pw = min(PW, n - k0);
+    const float* pan = pan0 + (t & 1) * NP * PW;
+    if (pwarp) {
+      if (t + 1 < npan) {  // panel t+1's columns after panel t, for every row, then eliminate them
+        const int k1 = k0 + PW, pw1 = min(PW, n - k1);
+        // pivot rows' panel-(t+1) segments: lane-uniform, loaded once as float4 pairs
+        float prs[PW][PW];
+#pragma unroll
+        for (int s = 0; s < PW; ++s) {
+          const float* pr = work + prow[k0 + min(s, pw - 1)] * lds + k1;
+          const float4 u = *reinterpret_cast<const float4*>(pr);
+          const float4 w = *reinterpret_cast<const float4*>(pr + 4);
+          const bool live = s < pw;
+          prs[s][0] = live ? u.x : 0.f; prs[s][1] = live ? u.y : 0.f; prs[s][2] = live ? u.z : 0.f;
+          prs[s][3] = live ? u.w : 0.f; prs[s][4] = live ? w.x : 0.f; prs[s][5] = live ? w.y : 0.f;
+          prs[s][6] = live ? w.z : 0.f; prs[s][7] = live ? w.w : 0.f;
+        }
+        float pv[PROWS][PW];
+#pragma unroll
+        for (int h = 0; h < PROWS; ++h) {
+          const int i = lane + 32 * h;
+          const bool valid = i < n;
+          const int st = valid ? pstep[i] : -1;
+          const bool mine = st >= k0 && st < k0 + pw;
+          float cf[PW], v[PW];
+          if (valid) {
+            const float4 c0 = *reinterpret_cast<const float4*>(pan + i * PW);
+            const float4 c1 = *reinterpret_cast<const float4*>(pan + i * PW + 4);
+            cf[0] = c0.x; cf[1] = c0.y; cf[2] = c0.z; cf[3] = c0.w; cf[4] = c1.x; cf[5] = c1.y; cf[6] = c1.z; cf[7] = c1.w;
+            const float4 o0 = *reinterpret_cast<const float4*>(work + i * lds + k1);
+            const float4 o1 = *reinterpret_cast<const float4*>(work + i * lds + k1 + 4);
+            v[0] = o0.x; v[1] = o0.y; v[2] = o0.z; v[3] = o0.w; v[4] = o1.x; v[5] = o1.y; v[6] = o1.z; v[7] = o1.w;
+          } else {
+#pragma unroll
+            for (int c = 0; c < PW; ++c) { cf[c] = 0.f; v[c] = 0.f; }
+          }
+#pragma unroll
+          for (int c = 0; c < PW; ++c) v[c] = mine ? 0.f : v[c];
+#pragma unroll
+          for (int s = 0; s < PW; ++s)
+#pragma unroll
+            for (int c = 0; c < PW; ++c) v[c] = fmaf(cf[s], prs[s][c], v[c]);
+#pragma unroll
+          for (int c = 0; c < PW; ++c) pv[h][c] = (valid && c < pw1) ? v[c] : 0.f;
+        }
+        factor(pv, k1, pan0 + ((t + 1) & 1) * NP * PW);
+      }
+    } else if (part) {  // rank-pw update of this thread's columns, panel columns replaced
+      float cf[PW];
+      {
+        const float4 u = *reinterpret_cast<const float4*>(pan + row * PW);
+        const float4 v = *reinterpret_cast<const float4*>(pan + row * PW + 4);
+        cf[0] = u.x; cf[1] = u.y; cf[2] = u.z; cf[3] = u.w; cf[4] = v.x; cf[5] = v.y; cf[6] = v.z; cf[7] = v.w;
+      }
+      const int st = pstep[row];  // entries of panel t+1 may land concurrently: never in [k0, k0 + pw)
+      const bool mine = (st >= k0 && st < k0 + pw);
+      float v[SEG];
+#pragma unroll
+      for (int c = 0; c < SEG; ++c) v[c] = mine ? 0.f : r[c];
+#pragma unroll
+      for (int s = 0; s < PW; ++s) {
+        if (s < pw) {
+          const float* pr = work + prow[k0 + s] * lds + q * SEG;
+          const float f = cf[s];
+#pragma unroll
+          for (int c = 0; c < SEG; c += 4) {
+            if (q * SEG + c >= n) break;
+            const float4 tt = *reinterpret_cast<const float4*>(pr + c);
+            v[c] = fmaf(f, tt.x, v[c]);
+            v[c + 1] = fmaf(f, tt.y, v[c + 1]);
+            v[c + 2] = fmaf(f, tt.z, v[c + 2]);
+            v[c + 3] = fmaf(f, tt.w, v[c + 3]);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < SEG; ++c) {
+        const int col = q * SEG + c;
+        r[c] = (col >= k0 && col < k0 + pw) ? cf[col - k0] : v[c];
+      }
+    }
+    __syncthreads();  // panel t consumed, panel t+1 factored
+    if (t + 1 < npan) {  // publish the rows after panel t
+      if (part && row < n) {
+#pragma unroll
+        for (int c = 0; c < SEG; c += 4)
+          if (q * SEG + c < n)
+            *reinterpret_cast<float4*>(work + row * lds + q * SEG + c) = make_float4(r[c], r[c + 1], r[c + 2], r[c + 3]);
+      }
+      __syncthreads();
+    }
+  }
+  const bool ok = misc[1] == 0.f;
+  if (part && row < n) {
+    const int qi = pstep[row];
+#pragma unroll
+    for (int c = 0; c < SEG; ++c) {
+      const int col = q * SEG + c;
+      if (col < n) {
+        const int d = prow[col];
+        if (inv) inv[qi * lds + d] = r[c];
+        if (invT) invT[d * lds + qi] = r[c];
+      }
+    }
+  }
+  __syncthreads();
+  return ok;
+}
+
 }  // namespace gsls

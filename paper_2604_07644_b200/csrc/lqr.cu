@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
 // needs anyway) and Y' = Minv' Cl Ar' = Minv' W2.  Six n x lds smem buffers:
 //   b0 Pr -> W2 | b1 Cl -> Minv -> V | b2 M1 -> Minv^T | b3 Al | b4 Ar^T | b5 W1 -> Psi^T
 template <int NP>
-__global__ void __launch_bounds__(NP == 64 ? 256 : 416, NP == 64 ? 2 : 1) k_cvf_combine(CombineArgs a) {
+__global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_combine(CombineArgs a) {
   const int inst = inst_of(a.list);
   const int4 op = a.ops[blockIdx.x];
   const int n = a.n, ldg = ldg_of(n), lds = lds_of(n);
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(NP == 64 ? 256 : 416, NP == 64 ? 2 : 1) k_cvf_
   gemm_tn(n, b1, b4, lds, EpiSmem{b0, lds, n, false});  // W2 = Cl Ar^T (over Pr)
   __syncthreads();
   // Minv = M1^{-1} -> b1 (row-major, over Cl), Minv^T -> b2 (over M1, read first)
-  const bool ok = gj_inverse_panel<NP>(b2, b1, b1, b2, lds, n, gjbuf, a.rel_tol);  // work: b1 (Cl is dead)
+  const bool ok = gj_inverse_lookahead<NP>(b2, b1, b1, b2, lds, n, gjbuf, a.rel_tol);  // work: b1 (Cl is dead)
   if (!ok && threadIdx.x == 0)
     raise_err(a.err ? a.err + inst : nullptr, GSLS_ERR_ILL_CONDITIONED, a.op_base + blockIdx.x);
   if (rec) {
@@ -351,11 +351,11 @@ __global__ void __launch_bounds__(NP == 64 ? 256 : 416, NP == 64 ? 2 : 1) k_cvf_
 }
 
 size_t combine_smem_bytes(int n) {
-  return (6 * (size_t)n * lds_of(n) + gjp_scratch_words(n <= 64 ? 64 : 80)) * sizeof(float);
+  return (6 * (size_t)n * lds_of(n) + gjl_scratch_words(n <= 64 ? 64 : 80)) * sizeof(float);
 }
 
-int combine_threads(int n) {  // k_cvf_combine needs >= 4*NP threads for the inverse
-  if (n <= 64) return 256;
+int combine_threads(int n) {  // k_cvf_combine: 4*NP row threads + the inverse's panel warp, >= GEMM tiles
+  if (n <= 64) return 288;
   return 416;
 }
 

@@ -8,7 +8,7 @@ using namespace gsls;
 namespace gsls { void set_last_error(const char*, const char*, int) {} }
 
 template <int NP>
-__global__ void k(const float* A, float* out, int n, int* ok, int which) {
+__global__ void __launch_bounds__(NP == 64 ? 288 : 416) k(const float* A, float* out, int n, int* ok, int which) {
   extern __shared__ float sm[];
   const int lds = lds_of(n);
   float* a = sm;
@@ -18,7 +18,7 @@ __global__ void k(const float* A, float* out, int n, int* ok, int which) {
   for (int e = threadIdx.x; e < n * lds; e += blockDim.x) a[e] = (e % lds < n) ? A[(e / lds) * n + e % lds] : 0.f;
   __syncthreads();
   bool r;
-  if (which == 0) r = gj_inverse_rows<NP>(a, work, invT, lds, n, scr, 1e-10f);
+  if (which == 0) r = gj_inverse_lookahead<NP>(a, work, work, invT, lds, n, scr, 1e-10f);
   else r = gj_inverse_panel<NP>(a, work, work, invT, lds, n, scr, 1e-10f);
   if (threadIdx.x == 0) *ok = r;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
@@ -38,8 +38,9 @@ int main() {
     const int sb = (3 * 80 * lds_of(n) + 4096) * 4;
     cudaFuncSetAttribute(k<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb); cudaFuncSetAttribute(k<80>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
     for (int which : {0, 1}) {
-      if (n <= 64) k<64><<<1, 256, sb>>>(dA, dO, n, dok, which); else k<80><<<1, 416, sb>>>(dA, dO, n, dok, which);
-      cudaError_t e = cudaDeviceSynchronize();
+      if (n <= 64) k<64><<<1, 288, sb>>>(dA, dO, n, dok, which); else k<80><<<1, 416, sb>>>(dA, dO, n, dok, which);
+      cudaError_t e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
       std::vector<float> o(2 * n * n); int ok;
       cudaMemcpy(o.data(), dO, 2 * n * n * 4, cudaMemcpyDeviceToHost);
       cudaMemcpy(&ok, dok, 4, cudaMemcpyDeviceToHost);
@@ -51,7 +52,7 @@ int main() {
           err = fmax(err, fabs(s - (i == j)));
           errT = fmax(errT, fabs(sT - (i == j)));
         }
-      printf("n=%d %s ok=%d |inv*A-I|=%.3g |invT'*A-I|=%.3g (%s)\n", n, which ? "panel" : "rows", ok, err, errT,
+      printf("n=%d %s ok=%d |inv*A-I|=%.3g |invT'*A-I|=%.3g (%s)\n", n, which ? "panel" : "lookahead", ok, err, errT,
              cudaGetErrorString(e));
     }
   }
