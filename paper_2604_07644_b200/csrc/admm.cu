@@ -870,6 +870,17 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
 
 enum { IT_P1 = 0, IT_CVF1, IT_CVF2, IT_FF1, IT_FF2, IT_COT, IT_G };
 
+// f32 -> f64 widening off the conversion pipe (F2F.F64.F32 issues at 16 / clk / SM on
+// B200, tools/micro/cvt.cu): shifting the f32 exponent+mantissa down 3 bits into an f64
+// gives exactly f * 2^-896 for every finite f, denormals included.  Accumulate in that
+// scale and multiply the sum by 2^896; products stay normal unless |M x| < 2^-126.
+__device__ __forceinline__ double widen_scaled(uint32_t u) {
+  const uint32_t hi = ((u >> 3) & 0x0FFFFFFFu) | (u & 0x80000000u);
+  return __hiloint2double((int)hi, (int)(u << 29));
+}
+constexpr double kWidenUnscale = 0x1p896;
+constexpr int kTraceIter = 5;  // GSLS_REPLAY_TRACE samples this ADMM iteration (warm caches)
+
 struct StagedLayout {
   // byte offsets into dynamic shared memory
   int ring, pv, bv, cb, t1, t2, z, lam, y, w, kf, dx0, part, red, redall, masks, ops, phys, items, phase, mbar, total;
@@ -920,7 +931,7 @@ __host__ __device__ inline StagedLayout staged_layout(const DevLqr& L, int max_l
   S.w = take(L.mtot * 8, 16);
   S.kf = take(N * m * 8, 16);
   S.dx0 = take(n * 8, 16);
-  S.part = take(kReplayThreads * 8, 16);
+  S.part = take(2 * kReplayThreads * 8, 16);  // two halves x 16 (row block, slice) tasks x 32 rows
   S.red = take(64 * 8, 16);
   S.redall = take(2 * kMaxCluster * 8, 16);
   S.masks = take((L.cvf_nslots + L.cot_nslots) * 4, 16);
@@ -1155,8 +1166,8 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
           break;
       }
       const int RB = (d.rows + 31) >> 5;
-      int kslog = 3;  // KS = 8 / RB (power of two): one partial half holds <= 8 (row block, slice) tasks
-      while (kslog > 0 && (RB << kslog) > 8) --kslog;
+      int kslog = 4;  // KS = 16 / RB (power of two): one partial half holds <= 16 (row block, slice) tasks
+      while (kslog > 0 && (RB << kslog) > 16) --kslog;
       const int KS = 1 << kslog, K = d.K1 + d.K2;
       d.kslog = kslog;
       d.kc = (((K + KS - 1) / KS) + 3) & ~3;
@@ -1197,11 +1208,11 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   for (;;) {
     double rp = 0.0, rdz = 0.0;
     int j = 0;
-    if (a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == 0) a.trace[250] = clock64();
+    if (a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == kTraceIter) a.trace[250] = clock64();
     for (int ph = 0; ph < nph; ++ph) {
       // ---- the phase's items: one matvec each, read from the ring ------------------------
       for (; j < phase_off[ph + 1]; ++j) {
-        const bool tq = a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == 0 && j < 20;
+        const bool tq = a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == kTraceIter && j < 20;
         long long q0 = tq ? clock64() : 0, q1 = 0, q2 = 0, q3 = 0, q4 = 0;
         const ItemDesc& d = desc[j];
         const int rows = d.rows, ld = d.ld, K1 = d.K1, kind = d.kind;
@@ -1212,7 +1223,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
         mbar_wait(full + cslot, (unsigned)cpar);
         if (tq) q1 = clock64();
         const float* M = reinterpret_cast<const float*>(ring + (size_t)cslot * SL.slot);
-        double* pt = part + ph2 * (kReplayThreads / 2);
+        double* pt = part + ph2 * kReplayThreads;
         const int kslog = d.kslog, KS = 1 << kslog, kc = d.kc, K = K1 + d.K2;
         if (warp < (((rows + 31) >> 5) << kslog)) {
           const int rb = warp >> kslog, ks = warp & (KS - 1);
@@ -1223,13 +1234,16 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
           if (row0 < ld) {
 #pragma unroll 4
             for (int k = k0 + gq; k < k1; k += 4) {
-              const float4 v = *reinterpret_cast<const float4*>(M + k * ld + row0);
+              const uint4 v = *reinterpret_cast<const uint4*>(M + k * ld + row0);
               const double xk = (k < K1) ? x1[k] : x2[k - K1];
-              a0 = fma((double)v.x, xk, a0);
-              a1 = fma((double)v.y, xk, a1);
-              a2 = fma((double)v.z, xk, a2);
-              a3 = fma((double)v.w, xk, a3);
+              // rows 0-1 widen on the conversion pipe, rows 2-3 on the integer pipe (scaled)
+              a0 = fma((double)__uint_as_float(v.x), xk, a0);
+              a1 = fma((double)__uint_as_float(v.y), xk, a1);
+              a2 = fma(widen_scaled(v.z), xk, a2);
+              a3 = fma(widen_scaled(v.w), xk, a3);
             }
+            a2 *= kWidenUnscale;
+            a3 *= kWidenUnscale;
           }
 #pragma unroll
           for (int o = 8; o <= 16; o <<= 1) {
@@ -1289,7 +1303,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
         }
       }
       // ---- phase boundary -----------------------------------------------------------
-      if (a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == 0 && 2 * ph + 1 < 250)
+      if (a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == kTraceIter && 2 * ph + 1 < 250)
         a.trace[2 * ph + 1] = clock64();
       if (ph == 0) {  // terminal leaf (qN + rho CN' w_N, 0) on its owner
         if (rank == srank(N))
@@ -1323,10 +1337,10 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
       } else {
         cl.sync();  // CVF layers, FF2, COT layers: remote consumers
       }
-      if (a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == 0 && 2 * ph + 2 < 250)
+      if (a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == kTraceIter && 2 * ph + 2 < 250)
         a.trace[2 * ph + 2] = clock64();
     }
-    if (a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == 0) a.trace[0] = nph;
+    if (a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == kTraceIter) a.trace[0] = nph;
     ++tr_it;
     const double rpb = block_max_d(rp, red);
     const double rdb = block_max_d(rdz, red + 32);
