@@ -183,6 +183,16 @@ __device__ inline void warp_cm_partial(const float* __restrict__ Mcm, int ldg, i
   acc[0] = a0; acc[1] = a1; acc[2] = a2; acc[3] = a3;
 }
 
+// f32 -> f64 widening off the conversion pipe (F2F.F64.F32 issues at 16 / clk / SM on
+// B200, tools/micro/cvt.cu): shifting the f32 exponent+mantissa down 3 bits into an f64
+// gives exactly f * 2^-896 for every finite f, denormals included.  Accumulate in that
+// scale and multiply the sum by 2^896; products stay normal unless |M x| < 2^-126.
+__device__ __forceinline__ double widen_scaled(uint32_t u) {
+  const uint32_t hi = ((u >> 3) & 0x0FFFFFFFu) | (u & 0x80000000u);
+  return __hiloint2double((int)hi, (int)(u << 29));
+}
+constexpr double kWidenUnscale = 0x1p896;
+
 // Stage operator product for one (4*RQ)-row block: acc = M x (+ M2 x2), both
 // column-major with leading dimension ld (rows padded with zeros).  Lane
 // (rq, g): rows 4rq..4rq+3 of the block as one 16-byte load per column, k =
@@ -870,15 +880,6 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
 
 enum { IT_P1 = 0, IT_CVF1, IT_CVF2, IT_FF1, IT_FF2, IT_COT, IT_G };
 
-// f32 -> f64 widening off the conversion pipe (F2F.F64.F32 issues at 16 / clk / SM on
-// B200, tools/micro/cvt.cu): shifting the f32 exponent+mantissa down 3 bits into an f64
-// gives exactly f * 2^-896 for every finite f, denormals included.  Accumulate in that
-// scale and multiply the sum by 2^896; products stay normal unless |M x| < 2^-126.
-__device__ __forceinline__ double widen_scaled(uint32_t u) {
-  const uint32_t hi = ((u >> 3) & 0x0FFFFFFFu) | (u & 0x80000000u);
-  return __hiloint2double((int)hi, (int)(u << 29));
-}
-constexpr double kWidenUnscale = 0x1p896;
 constexpr int kTraceIter = 5;  // GSLS_REPLAY_TRACE samples this ADMM iteration (warm caches)
 
 struct StagedLayout {

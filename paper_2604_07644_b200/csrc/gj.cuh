@@ -381,6 +381,15 @@ __device__ bool gj_inverse_panel(const float* a, float* work, float* inv, float*
 // pivot choices as gj_inverse_panel.  Scratch: gjl_scratch_words(NP).
 constexpr int gjl_scratch_words(int NP) { return 2 * NP * 8 + 2 * NP + 16; }
 
+#ifdef GJ_TRACE  // tools/micro/gj_test.cu: clock64 probes of thread 0 and the panel warp
+__device__ long long g_gj_trace[256];
+#define GJT(i) do { if (threadIdx.x == 0 || threadIdx.x == NT) g_gj_trace[(threadIdx.x == NT ? 128 : 0) + (i)] = clock64(); } while (0)
+#define GJS(i) do { if (threadIdx.x == NT) g_gj_trace[200 + (i)] = clock64(); } while (0)
+#else
+#define GJT(i) do { } while (0)
+#define GJS(i) do { } while (0)
+#endif
+
 template <int NP>
 __device__ bool gj_inverse_lookahead(const float* a, float* work, float* inv, float* invT, int lds, int n,
                                      float* scratch, float rel_tol) {
@@ -400,6 +409,7 @@ __device__ bool gj_inverse_lookahead(const float* a, float* work, float* inv, fl
   const int row = tid >> 2, q = tid & 3, lane = tid & 31, warp = tid >> 5;
   float r[SEG];
   float mx = 0.f;
+  GJT(0);
 #pragma unroll
   for (int c = 0; c < SEG; ++c) {
     const int col = q * SEG + c;
@@ -410,6 +420,7 @@ __device__ bool gj_inverse_lookahead(const float* a, float* work, float* inv, fl
   if (part && lane == 0) pan0[warp] = mx;
   for (int i = tid; i < NP; i += blockDim.x) pstep[i] = -1;
   __syncthreads();  // a fully read (work / inv may alias it from here on)
+  GJT(1);
   if (tid == 0) {
     float m2 = 0.f;
     for (int w = 0; w < NW; ++w) m2 = fmaxf(m2, pan0[w]);
@@ -430,6 +441,7 @@ __device__ bool gj_inverse_lookahead(const float* a, float* work, float* inv, fl
   }
   __syncthreads();
   const float thresh = rel_tol * misc[0];
+  GJT(2);
   const int npan = (n + PW - 1) / PW;
   // Panel warp: eliminate panel t (columns k0..k0+pw) from its values pv (post panels < t).
   auto factor = [&](float (&pv)[PROWS][PW], int k0, float* pan) {
@@ -440,6 +452,7 @@ __device__ bool gj_inverse_lookahead(const float* a, float* work, float* inv, fl
       const int i = lane + 32 * h;
       used[h] = !(i < n) || pstep[i] >= 0;
     }
+    if (k0 == 0) GJS(0);
     bool fail = false;
 #pragma unroll
     for (int s = 0; s < PW; ++s) {
@@ -482,6 +495,7 @@ __device__ bool gj_inverse_lookahead(const float* a, float* work, float* inv, fl
           prow[k0 + s] = pr;
           pstep[pr] = k0 + s;
         }
+        if (k0 == 0) GJS(1 + s);
       }
     }
 #pragma unroll
@@ -505,8 +519,10 @@ __device__ bool gj_inverse_lookahead(const float* a, float* work, float* inv, fl
     factor(pv, 0, pan0);
   }
   __syncthreads();
+  GJT(3);
   for (int t = 0; t < npan; ++t) {
     const int k0 = t * PW, pw = min(PW, n - k0);
+    if (t < 8) GJT(8 + 4 * t);
     const float* pan = pan0 + (t & 1) * NP * PW;
     if (pwarp) {
       if (t + 1 < npan) {  // panel t+1's columns after panel t, for every row, then eliminate them
@@ -552,6 +568,7 @@ __device__ bool gj_inverse_lookahead(const float* a, float* work, float* inv, fl
           for (int c = 0; c < PW; ++c) pv[h][c] = (valid && c < pw1) ? v[c] : 0.f;
         }
         factor(pv, k1, pan0 + ((t + 1) & 1) * NP * PW);
+        if (t < 8) GJT(9 + 4 * t);
       }
     } else if (part) {  // rank-pw update of this thread's columns, panel columns replaced
       float cf[PW];
@@ -582,12 +599,17 @@ __device__ bool gj_inverse_lookahead(const float* a, float* work, float* inv, fl
         }
       }
 #pragma unroll
-      for (int c = 0; c < SEG; ++c) {
-        const int col = q * SEG + c;
-        r[c] = (col >= k0 && col < k0 + pw) ? cf[col - k0] : v[c];
+      for (int c = 0; c < SEG; ++c) {  // panel columns take their eliminated entries (static selects:
+        const int rel = q * SEG + c - k0;  // a runtime cf index would put cf in local memory)
+        float x = v[c];
+#pragma unroll
+        for (int s = 0; s < PW; ++s) x = (rel == s && s < pw) ? cf[s] : x;
+        r[c] = x;
       }
+      if (t < 8) GJT(9 + 4 * t);
     }
     __syncthreads();  // panel t consumed, panel t+1 factored
+    if (t < 8) GJT(10 + 4 * t);
     if (t + 1 < npan) {  // publish the rows after panel t
       if (part && row < n) {
 #pragma unroll
@@ -597,7 +619,9 @@ __device__ bool gj_inverse_lookahead(const float* a, float* work, float* inv, fl
       }
       __syncthreads();
     }
+    if (t < 8) GJT(11 + 4 * t);
   }
+  GJT(4);
   const bool ok = misc[1] == 0.f;
   if (part && row < n) {
     const int qi = pstep[row];

@@ -295,8 +295,14 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
 // Minv Pr and Minv' Cl are symmetric, so X' = Minv Pr Al = V (the product P
 // needs anyway) and Y' = Minv' Cl Ar' = Minv' W2.  Six n x lds smem buffers:
 //   b0 Pr -> W2 | b1 Cl -> Minv -> V | b2 M1 -> Minv^T | b3 Al | b4 Ar^T | b5 W1 -> Psi^T
+// GSLS_COMBINE_TRACE: clock64 at the phase points of one CTA mid-grid (diagnostics only).
+__device__ long long* g_comb_trace = nullptr;
+
 template <int NP>
 __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_combine(CombineArgs a) {
+  long long* trc = (g_comb_trace && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == gridDim.y / 2) ? g_comb_trace : nullptr;
+#define CTRACE(i) do { if (trc) trc[i] = clock64(); } while (0)
+  CTRACE(0);
   const int inst = inst_of(a.list);
   const int4 op = a.ops[blockIdx.x];
   const int n = a.n, ldg = ldg_of(n), lds = lds_of(n);
@@ -323,17 +329,21 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   cp_async_commit();
   cp_async_wait<1>();
   __syncthreads();
+  CTRACE(1);
   gemm_tn(n, b0, b1, lds, EpiSmem{b2, lds, n, true});   // M1 = I + Pr Cl
   cp_async_wait<0>();
   __syncthreads();
+  CTRACE(2);
   gemm_tn(n, b0, b3, lds, EpiSmem{b5, lds, n, false});  // W1 = Pr Al
   __syncthreads();
   gemm_tn(n, b1, b4, lds, EpiSmem{b0, lds, n, false});  // W2 = Cl Ar^T (over Pr)
   __syncthreads();
+  CTRACE(3);
   // Minv = M1^{-1} -> b1 (row-major, over Cl), Minv^T -> b2 (over M1, read first)
   const bool ok = gj_inverse_lookahead<NP>(b2, b1, b1, b2, lds, n, gjbuf, a.rel_tol);  // work: b1 (Cl is dead)
   if (!ok && threadIdx.x == 0)
     raise_err(a.err ? a.err + inst : nullptr, GSLS_ERR_ILL_CONDITIONED, a.op_base + blockIdx.x);
+  CTRACE(4);
   if (rec) {
     gemm_tn(n, b1, b3, lds, EpiGlobal{rec + 0 * MS, nullptr, ldg, n, nullptr});  // Ups^T = Minv^T Al
     gemm_tn(n, b1, b0, lds, EpiGlobalNeg{rec + 3 * MS, ldg, n});  // -Y^T = -Minv^T W2
@@ -348,6 +358,9 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   if (rec) cta_store(rec + 2 * MS, b5, lds, n);          // Psi record
   gemm_tn(n, b5, b3, lds, EpiGlobal{a.As + ib + od, nullptr, ldg, n, a.ATs + ib + od});  // A = Psi Al (+ A^T)
   gemm_tn(n, b5, b0, lds, EpiGlobal{a.Cs + ib + od, a.Cs + ib + ol, ldg, n, nullptr});   // C = Psi W2 + Cr
+  __syncthreads();
+  CTRACE(5);
+#undef CTRACE
 }
 
 size_t combine_smem_bytes(int n) {
@@ -555,7 +568,14 @@ static int set_smem(const void* fn, size_t bytes) {
 
 int launch_combine(const CombineArgs& a, int nops, int count, cudaStream_t st) {
   if (nops == 0 || count == 0) return GSLS_OK;
-  const size_t sb = combine_smem_bytes(a.n);
+  size_t sb = combine_smem_bytes(a.n);
+  if (getenv("GSLS_COMBINE_1CTA")) sb = 200 * 1024;  // diagnostics: one CTA per SM
+  static long long* trace = nullptr;
+  const bool tracing = getenv("GSLS_COMBINE_TRACE") != nullptr;
+  if (tracing && !trace) {
+    GSLS_CUDA_CHECK(cudaMalloc(&trace, 16 * sizeof(long long)));
+    GSLS_CUDA_CHECK(cudaMemcpyToSymbol(g_comb_trace, &trace, sizeof(trace)));
+  }
   if (a.n <= 64) {
     int rc = set_smem((const void*)k_cvf_combine<64>, sb);
     if (rc) return rc;
@@ -566,6 +586,13 @@ int launch_combine(const CombineArgs& a, int nops, int count, cudaStream_t st) {
     k_cvf_combine<80><<<dim3(nops, count), combine_threads(a.n), sb, st>>>(a);
   }
   GSLS_CUDA_CHECK(cudaGetLastError());
+  if (tracing) {
+    long long h[16];
+    GSLS_CUDA_CHECK(cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st));
+    GSLS_CUDA_CHECK(cudaStreamSynchronize(st));
+    fprintf(stderr, "combine n=%d ops=%d count=%d rec=%d cycles: load %lld gemm1 %lld gemm2+3 %lld gj %lld rest %lld total %lld\n",
+            a.n, nops, count, a.rec != nullptr, h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4], h[5] - h[0]);
+  }
   return GSLS_OK;
 }
 
