@@ -380,7 +380,14 @@ def run_ours(args):
     fam = dict(zip(nat.PROF_FAMILIES, zip(pm, pu_, pl)))
     clk = clocks.summary()
     sm_max = clk["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
-    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    # FP32-SIMT peak: measured on a B200 of this pool (tools/micro/fp32peak.cu, committed result);
+    # MEASURED_PEAKS.json carries no FP32-SIMT figure.  Fallback: 148 SMs x 128 FMA/clk x 2 x clock.
+    fp32_src = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "fp32_peak.json")
+    try:
+        with open(fp32_src) as fh:
+            fp32_peak, fp32_how = float(json.load(fh)["fp32_ffma_tflops"]), "measured: profiles/r01/fp32_peak.json (tools/micro/fp32peak.cu)"
+    except (OSError, ValueError, KeyError):
+        fp32_peak, fp32_how = 148 * 128 * 2 * sm_max * 1e6 / 1e12, "derived: 148 SMs x 128 FP32 FMA/clk x 2 x max SM clock"
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     phases = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[2] / args.steps} for k, v in fam.items()
               if v[2]}
@@ -402,8 +409,7 @@ def run_ours(args):
                         "traffic_launch": (tr.get("replay") or {}).get("launch")}
     dom = max(fam, key=lambda k: fam[k][0])
     roof = dict(rl.get(dom, {}), kernel=dom,
-                peak_source=("derived: 148 SMs x 128 FP32 FMA/clk x 2 x max SM clock (no FP32-SIMT figure in "
-                             "MEASURED_PEAKS.json)") if dom in ("sls_cvf", "cvf_lqr") else
+                peak_source=fp32_how if dom in ("sls_cvf", "cvf_lqr") else
                 "MEASURED_PEAKS.json hbm_gbs",
                 work=("units = combines per launch x batch; 16 2/3 n^3 flop per combine (SURVEY §8d)"
                       if dom in ("sls_cvf", "cvf_lqr") else "B_iter x ADMM iterations (SURVEY §8d)"))
