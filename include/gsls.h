@@ -243,6 +243,39 @@ int gsls_linearize(gsls_ctx* ctx, const gsls_linearize_args_t* args, const gsls_
  * max(g + h) (unclamped), sum max(g + h, 0), sum|x0 - xbar0|, max|x0 - xbar0|, n_obs}. */
 int gsls_traj_eval(gsls_ctx* ctx, const gsls_linearize_args_t* args, double* out, void* stream);
 
+/* ---- closed-loop verification (rollout.py:47-93) ------------------------------
+ * Replaces rollout.closed_loop (rollout.py:47) for `rollouts` disturbance
+ * sequences per instance of the context's batch: u_k = v_k + sum_{j<k}
+ * Phi^u_{k,j} w_hat_j, x_{k+1} = f(x_k, u_k) + E d_k, w_hat_k = E^+ (x_{k+1} - f),
+ * stage/terminal constraint values, tube slack min(g_nom + h_k + tol_lin - g)
+ * (+inf without h), flags.  E must be state-independent (true for every
+ * device model); E_pinv is its range-restricted pseudo-inverse (rollout.py:41-44). */
+typedef struct {
+  int32_t model_id;             /* GSLS_MODEL_*                                        */
+  const double* params;         /* model parameters + constraint block (device)        */
+  int32_t cons_offset;          /* index of the constraint block in params             */
+  const double *x, *u;          /* nominal trajectory (B,N+1,nx), (B,N,nu)             */
+  const float* phi_u;           /* (B, N(N+1)/2, nu, nx) cell layout, or NULL           */
+  const double *E, *E_pinv;     /* (nx,nx) disturbance map and its pseudo-inverse       */
+  const double* disturbances;   /* true injected w (B, rollouts, N, nx)                 */
+  const double* h;              /* stage tightening (B,N,nc) or NULL (no tube check)    */
+  double tol_lin;               /* rollout.py:48 default 1e-2                           */
+  int32_t rollouts;             /* disturbance sequences per instance                   */
+} gsls_rollout_args_t;
+
+typedef struct {                /* all device buffers, float64 unless noted             */
+  double* x;                    /* (B, R, N+1, nx) realized states                      */
+  double* u;                    /* (B, R, N, nu) applied controls                       */
+  double* w;                    /* (B, R, N, nx) reconstructed disturbances             */
+  double* stage_g;              /* (B, R, N, nc)                                        */
+  double* terminal_g;           /* (B, R, nf)                                           */
+  double* tube_margin;          /* (B, R, N), +inf where unchecked                      */
+  double* max_w_norm;           /* (B, R)                                               */
+  int32_t* flags;               /* (B, R, 3) int32: safe, tube_ok, disturbance_model_violated */
+} gsls_rollout_out_t;
+
+int gsls_rollout(gsls_ctx* ctx, const gsls_rollout_args_t* args, const gsls_rollout_out_t* out, void* stream);
+
 /* f -= h, fN -= hf in place (the tightened re-linearization, sqp.py:136/:140). */
 int gsls_apply_tightening(gsls_ctx* ctx, double* f, double* fN, const double* h, const double* hf, void* stream);
 /* RTI update (sqp.py:293-301, :40-43): plan = prev + (dx, du); warm start =

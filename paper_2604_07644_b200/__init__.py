@@ -6,4 +6,4 @@ Modules mirror the reference package: ``scan``, ``lqr``, ``admm``, ``sqp``,
 sm_100a CUDA kernels (``csrc/``) behind the C ABI in ``include/gsls.h``.
 """
 
-__all__ = ["scan", "lqr", "admm", "sqp", "sls", "models", "engine", "device", "dist", "scenarios"]
+__all__ = ["scan", "lqr", "admm", "sqp", "sls", "models", "rollout", "engine", "device", "dist", "scenarios"]

@@ -56,6 +56,18 @@ class LinArgs(ctypes.Structure):
                 ("E_const", c_void_p), ("write_weights", ctypes.c_int32)]
 
 
+class RolloutArgs(ctypes.Structure):
+    _fields_ = [("model_id", ctypes.c_int32), ("params", c_void_p), ("cons_offset", ctypes.c_int32),
+                ("x", c_void_p), ("u", c_void_p), ("phi_u", c_void_p), ("E", c_void_p), ("E_pinv", c_void_p),
+                ("disturbances", c_void_p), ("h", c_void_p), ("tol_lin", ctypes.c_double),
+                ("rollouts", ctypes.c_int32)]
+
+
+class RolloutOut(ctypes.Structure):
+    _fields_ = [(k, c_void_p) for k in ("x", "u", "w", "stage_g", "terminal_g", "tube_margin", "max_w_norm",
+                                        "flags")]
+
+
 class Error(ctypes.Structure):
     _fields_ = [("code", ctypes.c_int32), ("instance", ctypes.c_int32), ("where", ctypes.c_int32),
                 ("aux", ctypes.c_int32), ("aux2", ctypes.c_int32), ("message", ctypes.c_char * 256)]
@@ -95,10 +107,11 @@ _SIGS = {
     "gsls_prof_enable": ([ctypes.c_int32], ctypes.c_int),
     "gsls_prof_read": ([c_void_p, c_void_p, c_void_p, ctypes.c_int32], ctypes.c_int),
     "gsls_rti_apply": ([c_void_p] * 17, ctypes.c_int),
+    "gsls_rollout": ([c_void_p, ctypes.POINTER(RolloutArgs), ctypes.POINTER(RolloutOut), c_void_p], ctypes.c_int),
 }
 
 PROF_FAMILIES = ("leaf", "cvf_lqr", "gains", "cot", "replay", "sls_assemble", "sls_leaf", "sls_cvf", "sls_gains",
-                 "sls_matprod", "sls_phiu", "sls_rownorm", "sls_small", "linearize", "rti_misc")
+                 "sls_matprod", "sls_phiu", "sls_rownorm", "sls_small", "linearize", "rti_misc", "rollout")
 
 # every symbol include/gsls.h declares (checked by the CPU test suite)
 EXPORTS = tuple(_SIGS)

@@ -39,6 +39,7 @@ int rti_apply(Ctx* c, const double* px, const double* pu, const double* dx, cons
               double* plan_u, double* warm_x, double* warm_u, double* u0, const double* Qw, const double* Rw,
               const double* QNw, const double* xref, const double* uref, double* cost, cudaStream_t st);
 int sls_export(Ctx* c, float* phix, float* phiu, float* gains, cudaStream_t st);
+int rollout(Ctx* c, const gsls_rollout_args_t* in, const gsls_rollout_out_t* out, cudaStream_t st);
 }  // namespace gsls
 
 using namespace gsls;
@@ -236,6 +237,19 @@ int gsls_rti_apply(gsls_ctx* ctx, const double* prev_x, const double* prev_u, co
   if (cost && (!Qw || !Rw || !QNw || !xref || !uref)) return fail_null("cost weights");
   return rti_apply(ctx->impl, prev_x, prev_u, dx, du, plan_x, plan_u, warm_x, warm_u, u0, Qw, Rw, QNw, xref, uref,
                    cost, (cudaStream_t)stream);
+}
+
+int gsls_rollout(gsls_ctx* ctx, const gsls_rollout_args_t* args, const gsls_rollout_out_t* out, void* stream) {
+  if (!ctx || !args || !out || !args->params || !args->x || !args->u || !args->E || !args->E_pinv ||
+      !args->disturbances)
+    return fail_null("argument");
+  if (!out->x || !out->u || !out->w || !out->tube_margin || !out->max_w_norm || !out->flags ||
+      (ctx->impl->dims.nc > 0 && !out->stage_g) || (ctx->impl->dims.nf > 0 && !out->terminal_g))
+    return fail_null("output");
+  const int rc = rollout(ctx->impl, args, out, (cudaStream_t)stream);
+  if (rc == GSLS_ERR_ARG) set_error(rc, -1, 0, 0, 0, "model / dimension mismatch");
+  if (rc == GSLS_ERR_TOO_LARGE) set_error(rc, -1, 0, 0, 0, "rollout too large");
+  return rc;
 }
 
 }  // extern "C"

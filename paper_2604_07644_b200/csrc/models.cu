@@ -577,3 +577,219 @@ int traj_eval(Ctx* c, const gsls_linearize_args_t* in, double* out, cudaStream_t
 }
 
 }  // namespace gsls
+
+namespace gsls {
+
+// ---- closed-loop rollouts (rollout.py:47-93) -------------------------------------
+//
+// One CTA per (rollout, instance).  The horizon is sequential; inside a stage the
+// CTA evaluates the feedback u_k = v_k + sum_{j<k} Phi^u_{k,j} w_hat_j (one warp per
+// input row over the flattened (j, i) range), the model step, the disturbed state
+// x_{k+1} = f(x_k, u_k) + E d_k, the reconstruction w_hat_k = E^+ (x_{k+1} - f) and the
+// constraint / tube checks.  E is state-independent for every device model, so E and
+// its range-restricted pseudo-inverse (rollout.py:41-44) arrive precomputed.
+struct RolloutArgs {
+  int model;
+  const double* P;
+  const double* cons;
+  int n, m, c, nf, N, S;
+  const double *x, *u;      // nominal (B,N+1,n), (B,N,m)
+  const float* phiu;        // (B, N(N+1)/2, m, n) cell layout, or null (open loop)
+  const double *E, *Epinv;  // (n,n)
+  const double* dist;       // (B,S,N,n)
+  const double* h;          // (B,N,c) or null: no tube check
+  double tol_lin;
+  double *ox, *ou, *ow, *og, *ogf, *omargin, *omaxw;
+  int* oflags;              // (B,S,3): safe, tube_ok, disturbance_model_violated
+};
+
+__device__ inline double stage_con(const double* cons, int m, const double* x, const double* u, int r) {
+  const double* lo = cons + 1;
+  const double* hi = lo + m;
+  if (r < m) return u[r] - hi[r];
+  if (r < 2 * m) return lo[r - m] - u[r - m];
+  const double* o = hi + m + 3 * (r - 2 * m);
+  return o[2] * o[2] - (x[0] - o[0]) * (x[0] - o[0]) - (x[1] - o[1]) * (x[1] - o[1]);
+}
+
+__device__ inline double block_sum128(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r += red[w];
+  return r;
+}
+
+__device__ inline double block_min128(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = INFINITY;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmin(r, red[w]);
+  return r;
+}
+
+__global__ void __launch_bounds__(128) k_rollout(RolloutArgs a) {
+  const int s = blockIdx.x, inst = blockIdx.y;
+  const int n = a.n, m = a.m, c = a.c, nf = a.nf, N = a.N, S = a.S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  extern __shared__ double smr[];
+  double* x = smr;           // realized x_k
+  double* nom = x + n;       // f(x_k, u_k)
+  double* xn = nom + n;      // x_{k+1}
+  double* u = xn + n;        // u_k
+  double* wh = u + m;        // w_hat (N, n)
+  double* red = wh + (size_t)N * n;  // 32
+  const long long rs = (long long)inst * S + s;
+  const double* xnom = a.x + (size_t)inst * (N + 1) * n;
+  const double* unom = a.u + (size_t)inst * N * m;
+  const double* d = a.dist + (size_t)rs * N * n;
+  const double* h = a.h ? a.h + (size_t)inst * N * c : nullptr;
+  const int ncell = N * (N + 1) / 2;
+  const float* phiu = a.phiu ? a.phiu + (size_t)inst * ncell * m * n : nullptr;
+  double* ox = a.ox + (size_t)rs * (N + 1) * n;
+  LinArgs la{};
+  la.model = a.model;
+  la.P = a.P;
+  for (int i = tid; i < n; i += blockDim.x) {
+    x[i] = xnom[i];
+    ox[i] = xnom[i];
+  }
+  bool safe = true, tube_ok = true, violated = false;
+  double maxw = 0.0;
+  __syncthreads();
+  for (int k = 0; k < N; ++k) {
+    // u_k = v_k + sum_{j<k} Phi^u_{k,j} w_hat_j  (rollout.py:69-73)
+    for (int l = warp; l < m; l += nw) {
+      double acc = 0.0;
+      if (phiu)
+        for (int e = lane; e < k * n; e += 32) {
+          const int j = e / n, i = e - j * n;
+          const int cell = j * N - j * (j - 1) / 2 + (k - j - 1);
+          acc = fma((double)phiu[((size_t)cell * m + l) * n + i], wh[e], acc);
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) u[l] = unom[(size_t)k * m + l] + acc;
+    }
+    __syncthreads();
+    // nominal_next = f(x_k, u_k)
+    if (a.model == M_SYNTH) {
+      const double dt = a.P[0], cpl = a.P[1];
+      const double* A0 = a.P + 2;
+      const double* B0 = A0 + n * n;
+      const double* W = B0 + n * m;
+      for (int i = tid; i < n; i += blockDim.x) {
+        double sw = 0.0, fa = 0.0, fb = 0.0;
+        for (int j = 0; j < n; ++j) {
+          sw = fma(W[i * n + j], x[j], sw);
+          fa = fma(A0[i * n + j], x[j], fa);
+        }
+        for (int l = 0; l < m; ++l) fb = fma(B0[i * m + l], u[l], fb);
+        nom[i] = x[i] + dt * (fa + fb + cpl * ::tanh(sw));
+      }
+    } else if (tid == 0) {
+      step_value(la, x, u, nom);
+    }
+    __syncthreads();
+    // x_{k+1} = f + E d_k  (rollout.py:75-76)
+    for (int i = tid; i < n; i += blockDim.x) {
+      double v = nom[i];
+      for (int j = 0; j < n; ++j) v = fma(a.E[i * n + j], d[(size_t)k * n + j], v);
+      xn[i] = v;
+    }
+    __syncthreads();
+    // w_hat_k = E^+ (x_{k+1} - f)  (rollout.py:77)
+    double sq = 0.0;
+    for (int i = tid; i < n; i += blockDim.x) {
+      double v = 0.0;
+      for (int j = 0; j < n; ++j) v = fma(a.Epinv[i * n + j], xn[j] - nom[j], v);
+      wh[(size_t)k * n + i] = v;
+      sq = fma(v, v, sq);
+    }
+    const double wn = sqrt(block_sum128(sq, red));
+    if (wn > 1.0 + 1e-9) violated = true;  // rollout.py:78-79 (WNORM_TOL)
+    maxw = fmax(maxw, wn);
+    // stage constraints at (x_k, u_k) and the tube slack against the nominal + h_k (rollout.py:80-85)
+    double slack = INFINITY;
+    bool ok = true;
+    for (int r = tid; r < c; r += blockDim.x) {
+      const double g = stage_con(a.cons, m, x, u, r);
+      a.og[((size_t)rs * N + k) * c + r] = g;
+      ok = ok && (g <= 0.0);
+      if (h) slack = fmin(slack, stage_con(a.cons, m, xnom + (size_t)k * n, unom + (size_t)k * m, r) + h[(size_t)k * c + r] +
+                                     a.tol_lin - g);
+    }
+    const int all_ok = __syncthreads_and(ok);
+    safe = safe && all_ok;
+    if (h && c > 0) {
+      const double sl = block_min128(slack, red);
+      if (tid == 0) a.omargin[(size_t)rs * N + k] = sl;
+      tube_ok = tube_ok && (sl >= 0.0);
+    } else if (tid == 0) {
+      a.omargin[(size_t)rs * N + k] = INFINITY;
+    }
+    for (int i = tid; i < n; i += blockDim.x) {
+      a.ow[((size_t)rs * N + k) * n + i] = wh[(size_t)k * n + i];
+      ox[(size_t)(k + 1) * n + i] = xn[i];
+    }
+    for (int l = tid; l < m; l += blockDim.x) a.ou[((size_t)rs * N + k) * m + l] = u[l];
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) x[i] = xn[i];
+    __syncthreads();
+  }
+  // terminal constraints (obstacles) at x_N (rollout.py:86-87)
+  bool okf = true;
+  const int nobs = (int)a.cons[0];
+  for (int r = tid; r < nf; r += blockDim.x) {
+    double g = 0.0;
+    if (r < nobs) {
+      const double* o = a.cons + 1 + 2 * m + 3 * r;
+      g = o[2] * o[2] - (x[0] - o[0]) * (x[0] - o[0]) - (x[1] - o[1]) * (x[1] - o[1]);
+    }
+    a.ogf[(size_t)rs * nf + r] = g;
+    okf = okf && (g <= 0.0);
+  }
+  const int all_okf = __syncthreads_and(okf);
+  safe = safe && all_okf;
+  if (tid == 0) {
+    a.oflags[rs * 3 + 0] = safe;
+    a.oflags[rs * 3 + 1] = tube_ok;
+    a.oflags[rs * 3 + 2] = violated;
+    a.omaxw[rs] = maxw;
+  }
+}
+
+int rollout(Ctx* c, const gsls_rollout_args_t* in, const gsls_rollout_out_t* out, cudaStream_t st) {
+  const gsls_dims_t& d = c->dims;
+  if ((in->model_id == M_PLANAR && d.nx != 6) || (in->model_id == M_QUAD12 && d.nx != 12) ||
+      (in->model_id == M_DUBINS && d.nx != 3) || in->model_id < 1 || in->model_id > 5 || in->rollouts < 0)
+    return GSLS_ERR_ARG;
+  if (in->model_id == M_PENDULUM && d.nx > 2 * kMaxLinks) return GSLS_ERR_TOO_LARGE;
+  if (d.batch == 0 || in->rollouts == 0 || d.N == 0) return GSLS_OK;
+  RolloutArgs a{};
+  a.model = in->model_id;
+  a.P = in->params;
+  a.cons = in->params + in->cons_offset;
+  a.n = d.nx; a.m = d.nu; a.c = d.nc; a.nf = d.nf; a.N = d.N; a.S = in->rollouts;
+  a.x = in->x; a.u = in->u; a.phiu = in->phi_u; a.E = in->E; a.Epinv = in->E_pinv; a.dist = in->disturbances;
+  a.h = in->h; a.tol_lin = in->tol_lin;
+  a.ox = out->x; a.ou = out->u; a.ow = out->w; a.og = out->stage_g; a.ogf = out->terminal_g;
+  a.omargin = out->tube_margin; a.omaxw = out->max_w_norm; a.oflags = out->flags;
+  const size_t smem = (size_t)(3 * d.nx + d.nu + (size_t)d.N * d.nx + 32) * sizeof(double);
+  if (smem > 48 * 1024) {
+    if (smem > 227 * 1024) return GSLS_ERR_TOO_LARGE;
+    GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_rollout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  ProfScope ps(P_ROLLOUT, st, (double)in->rollouts * d.batch);
+  k_rollout<<<dim3(in->rollouts, d.batch), 128, smem, st>>>(a);
+  GSLS_CUDA_CHECK(cudaGetLastError());
+  return GSLS_OK;
+}
+
+}  // namespace gsls

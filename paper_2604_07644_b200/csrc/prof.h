@@ -8,7 +8,7 @@ namespace gsls {
 
 enum ProfId {
   P_LEAF = 0, P_CVF_LQR, P_GAINS, P_COT, P_REPLAY, P_SLS_ASSEMBLE, P_SLS_LEAF, P_SLS_CVF, P_SLS_GAINS,
-  P_SLS_MATPROD, P_SLS_PHIU, P_SLS_ROWNORM, P_SLS_SMALL, P_LINEARIZE, P_RTI_MISC, P_COUNT
+  P_SLS_MATPROD, P_SLS_PHIU, P_SLS_ROWNORM, P_SLS_SMALL, P_LINEARIZE, P_RTI_MISC, P_ROLLOUT, P_COUNT
 };
 
 void prof_begin(int id, cudaStream_t st);

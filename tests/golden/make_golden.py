@@ -21,7 +21,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-from scanmpc import admm, lqr, models, reference, scan, sls, sqp  # noqa: E402
+from scanmpc import admm, lqr, models, reference, rollout, scan, sls, sqp  # noqa: E402
 
 import problems as P  # noqa: E402
 from paper_2604_07644_b200 import models as ours  # noqa: E402
@@ -250,7 +250,62 @@ def gen_rti():
     save("rti", **out)
 
 
+def gen_rollout():
+    """rollout.closed_loop / sample_disturbance / adversarial_rows (rollout.py:41-160) on
+    nominal trajectories with a synthesized response (sls.synthesize on the linearization)."""
+    out = {}
+    cases = {
+        "dubins": (models.DubinsCar(obstacles=((1.0, 0.2, 0.3),)), np.array([0.0, 0.0, 0.1]), 20, 0.3),
+        "quad": (models.PlanarQuadrotor(obstacles=((1.5, 0.0, 0.35),)), np.array([0.2, 0.1, 0, 0, 0, 0]), 16, 3.0),
+        "pend2": (models.NLinkPendulum(n_links=2), np.array([0.3, -0.2, 0.0, 0.0]), 12, 0.5),
+        "q61": (ours.quadruped61(), None, 10, 1.0),
+    }
+    rng = np.random.default_rng(7)
+    for tag, (mdl, x0, N, uscale) in cases.items():
+        nx, nu = mdl.nx, mdl.nu
+        if x0 is None:
+            x0 = np.zeros(nx)
+            x0[0], x0[1] = -0.3, 0.05
+        # nominal: a rollout under small random inputs (dimensionally valid, not optimal)
+        u = rng.standard_normal((N, nu)) * 0.1 * uscale
+        x = np.zeros((N + 1, nx))
+        x[0] = x0
+        for k in range(N):
+            x[k + 1] = mdl.step(x[k], u[k])
+        traj = sqp.Trajectory(x=x, u=u, dt=mdl.dt)
+        qp = sqp.linearize(mdl, traj)
+        E = np.array([mdl.disturbance(x[k]) for k in range(N)])
+        w = sls.SlsWeights.identity(nx, nu)
+        costs = sls.assemble_costs(None, qp.C, qp.D, qp.CN, w)
+        resp = sls.synthesize(qp.A, qp.B, E, costs, executor=EX)
+        tight = sls.tighten(resp, qp.C, qp.D, qp.CN)
+        rows = rollout.adversarial_rows(mdl, traj)
+        dists = [rollout.sample_disturbance("uniform_ball", nx, N, 11),
+                 rollout.sample_disturbance("boundary", nx, N, 12),
+                 rollout.sample_disturbance("adversarial", nx, N, 0, rows=rows),
+                 rollout.sample_disturbance("uniform_ball", nx, N, 13) * 3.0]   # violates |w| <= 1
+        recs = [rollout.closed_loop(mdl, traj, resp, d, tight) for d in dists]
+        rec_nt = rollout.closed_loop(mdl, traj, resp, dists[0], None)          # no tube check
+        sup = rollout.superposition_check(traj, resp, recs[0].w, recs[0].x)
+        out[f"{tag}_x"], out[f"{tag}_u"], out[f"{tag}_N"] = x, u, np.int64(N)
+        out[f"{tag}_phiu"] = P.pack_lower(resp.Phi_u, N, 1, N, (nu, nx))
+        out[f"{tag}_phix"] = P.pack_lower(resp.Phi_x, N, 1, N + 1, (nx, nx))
+        out[f"{tag}_h"], out[f"{tag}_hf"] = tight.h, tight.hf
+        out[f"{tag}_rows"] = rows
+        out[f"{tag}_dist"] = np.array(dists)
+        for f in ("x", "u", "w", "stage_g", "terminal_g", "tube_margin"):
+            out[f"{tag}_rec_{f}"] = np.array([getattr(r, f) for r in recs])
+        for f in ("safe", "tube_ok", "disturbance_model_violated", "max_w_norm", "min_margin"):
+            out[f"{tag}_rec_{f}"] = np.array([getattr(r, f) for r in recs])
+        out[f"{tag}_nt_tube_margin"] = rec_nt.tube_margin
+        out[f"{tag}_nt_tube_ok"] = np.bool_(rec_nt.tube_ok)
+        out[f"{tag}_superposition"] = np.float64(sup)
+        print(tag, "safe", [r.safe for r in recs], "tube", [r.tube_ok for r in recs],
+              "viol", [r.disturbance_model_violated for r in recs], "sup", sup)
+    save("rollout", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["scan", "lqr", "admm", "sls", "models", "rti"]
+    which = sys.argv[1:] or ["scan", "lqr", "admm", "sls", "models", "rti", "rollout"]
     for w in which:
         globals()["gen_" + w]()

@@ -263,3 +263,48 @@ def test_rti_robust_golden(tag):
     assert rel(r.tightening.h, g[f"{tag}_h"]) <= 1e-7
     assert rel(r.plan.x, g[f"{tag}_plan_x"]) <= 1e-7
     assert rel(P.pack_lower(r.tau.tau, prev.N, 1, prev.N, (model.nc,)), g[f"{tag}_tau_out"]) <= 1e-6
+
+
+# --- rollout (rollout.py:41-180) ----------------------------------------------------
+
+@pytest.mark.parametrize("tag", P.ROLLOUT_TAGS)
+def test_rollout_golden(tag):
+    from oracle import rollout as orl
+    g = load_golden("rollout")
+    mdl = P.rollout_model(tag)
+    x, u, N = g[f"{tag}_x"], g[f"{tag}_u"], int(g[f"{tag}_N"])
+    phiu = g[f"{tag}_phiu"]
+    h = g[f"{tag}_h"]
+    # samplers reproduce the reference's seeded streams bit for bit
+    nx = mdl.nx
+    assert np.array_equal(orl.sample_disturbance("uniform_ball", nx, N, 11), g[f"{tag}_dist"][0])
+    assert np.array_equal(orl.sample_disturbance("boundary", nx, N, 12), g[f"{tag}_dist"][1])
+    rows = orl.adversarial_rows(mdl, x, u)
+    assert rel(rows, g[f"{tag}_rows"]) <= TOL
+    assert np.array_equal(orl.sample_disturbance("adversarial", nx, N, 0, rows=g[f"{tag}_rows"]), g[f"{tag}_dist"][2])
+    for i, d in enumerate(g[f"{tag}_dist"]):
+        r = orl.closed_loop(mdl, x, u, lambda k, j: phiu[k, j], d, h)
+        for f in ("x", "u", "w", "stage_g", "terminal_g"):
+            assert rel(getattr(r, f), g[f"{tag}_rec_{f}"][i]) <= TOL, (tag, i, f)
+        tm, gtm = r.tube_margin, g[f"{tag}_rec_tube_margin"][i]
+        assert np.array_equal(np.isinf(tm), np.isinf(gtm))
+        assert rel(np.where(np.isinf(tm), 0, tm), np.where(np.isinf(gtm), 0, gtm)) <= TOL
+        assert r.safe == bool(g[f"{tag}_rec_safe"][i])
+        assert r.tube_ok == bool(g[f"{tag}_rec_tube_ok"][i])
+        assert r.disturbance_model_violated == bool(g[f"{tag}_rec_disturbance_model_violated"][i])
+        assert abs(r.max_w_norm - g[f"{tag}_rec_max_w_norm"][i]) <= TOL * max(1, r.max_w_norm)
+    r = orl.closed_loop(mdl, x, u, lambda k, j: phiu[k, j], g[f"{tag}_dist"][0], None)
+    assert np.isinf(r.tube_margin).all() and r.tube_ok == bool(g[f"{tag}_nt_tube_ok"])
+    rec0 = orl.closed_loop(mdl, x, u, lambda k, j: phiu[k, j], g[f"{tag}_dist"][0], h)
+    sup = orl.superposition_check(x, lambda k, j: g[f"{tag}_phix"][k, j], rec0.w, rec0.x)
+    assert abs(sup - float(g[f"{tag}_superposition"])) <= 1e-9 * max(1.0, sup)
+
+
+def test_rollout_sampler_errors():
+    from oracle import rollout as orl
+    with pytest.raises(ValueError, match="adversarial sampling needs"):
+        orl.sample_disturbance("adversarial", 3, 4, 0)
+    with pytest.raises(ValueError, match="unknown disturbance kind"):
+        orl.sample_disturbance("gaussian", 3, 4, 0)
+    with pytest.raises(ValueError, match="rows must be"):
+        orl.sample_disturbance("adversarial", 3, 4, 0, rows=np.ones((3, 3)))
