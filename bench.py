@@ -371,6 +371,32 @@ def run_ours(args):
         dist.all_reduce(ms_e, op=dist.ReduceOp.MAX)
     e2e_value = world * B * args.steps / (float(ms_e) / 1e3)
 
+    # ---- closed-loop verification of the step's policies (rollout.py:47-93):
+    #      S disturbance sequences per instance under the synthesized Phi^u, device-timed ------
+    from paper_2604_07644_b200 import rollout as RO
+    S_ro, K_ro = 16, 5
+    _, phiu_cells, _ = eng.export_response()
+    gen = torch.Generator(device="cuda").manual_seed(rank)
+    dro = torch.randn(B, S_ro, N, n, dtype=torch.float64, device="cuda", generator=gen)
+    dro /= dro.norm(dim=-1, keepdim=True)
+    dro *= torch.rand(B, S_ro, N, 1, dtype=torch.float64, device="cuda", generator=gen) ** (1.0 / n)
+    ro_ws = RO.DeviceRollouts(m, N, B, S_ro)
+    ro_out = ro_ws.run(eng.plan_x, eng.plan_u, phiu_cells, dro, eng.h)
+    torch.cuda.synchronize()
+    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e4.record()
+    for _ in range(K_ro):
+        ro_out = ro_ws.run(eng.plan_x, eng.plan_u, phiu_cells, dro, eng.h)
+    e5.record()
+    torch.cuda.synchronize()
+    ro_ms = e4.elapsed_time(e5) / K_ro
+    fl = ro_out["flags"].cpu().numpy()
+    rollout_line = {"metric": "closed-loop rollouts/s (rollout.closed_loop under the step's Phi^u, h)",
+                    "value": B * S_ro / (ro_ms / 1e3), "unit": "rollouts/s", "rollouts_per_call": B * S_ro,
+                    "per_instance": S_ro, "N": N, "ms_per_call": ro_ms, "safe_fraction": float(fl[..., 0].mean()),
+                    "tube_ok_fraction": float(fl[..., 1].mean()), "disturbances": "uniform unit ball, torch seed = rank",
+                    "kernel": "k_rollout", "launches_per_call": 1}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -439,6 +465,7 @@ def run_ours(args):
            "admm_iterations_mean": total_iters / its_all.numel(),
            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
            "gpu_launches": launches, "roofline": roof, "roofline_by_kernel": rl, "phases": phases,
+           "rollout": rollout_line,
            "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
            "cpu_baseline": cpu}
     print(json.dumps(out), flush=True)
