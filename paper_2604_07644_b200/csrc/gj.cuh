@@ -478,18 +478,21 @@ __device__ bool gj_inverse_lookahead(const float* a, float* work, float* inv, fl
         const float piv = prv[s];
         if (!(fabsf(piv) > thresh) || !isfinite(piv)) fail = true;
         const float ip = __frcp_rn(piv);
+        // branch-free: every row takes the elimination update, the pivot row (lane-uniform
+        // values prv * ip) is selected in afterwards
+        float pip[PW];
+#pragma unroll
+        for (int t = 0; t < PW; ++t) pip[t] = (t == s) ? ip : prv[t] * ip;
 #pragma unroll
         for (int h = 0; h < PROWS; ++h) {
-          const int i = lane + 32 * h;
-          if (i == pr) {
+          const bool isp = (lane + 32 * h) == pr;
+          const float fi = pv[h][s] * ip;
 #pragma unroll
-            for (int t = 0; t < PW; ++t) pv[h][t] = (t == s) ? ip : pv[h][t] * ip;
-            used[h] = true;
-          } else {
-            const float fi = pv[h][s] * ip;
-#pragma unroll
-            for (int t = 0; t < PW; ++t) pv[h][t] = (t == s) ? -fi : fmaf(-fi, prv[t], pv[h][t]);
+          for (int t = 0; t < PW; ++t) {
+            const float e = (t == s) ? -fi : fmaf(-fi, prv[t], pv[h][t]);
+            pv[h][t] = isp ? pip[t] : e;
           }
+          used[h] = used[h] || isp;
         }
         if (lane == 0) {
           prow[k0 + s] = pr;

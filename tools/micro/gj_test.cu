@@ -6,7 +6,7 @@
 #ifndef GJ_REPS
 #define GJ_REPS 9
 #endif
-#define GJ_TRACE
+
 #include "../../paper_2604_07644_b200/csrc/gj.cuh"
 using namespace gsls;
 namespace gsls { void set_last_error(const char*, const char*, int) {} }
@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416) k(const float* A, float*
   long long t1 = clock64();
   if (threadIdx.x == 0 && which == 0) {
     printf("  n=%d lookahead: %lld cycles per inverse (incl. reload)\n", n, (t1 - t0) / GJ_REPS);
+#ifdef GJ_TRACE
     const long long* g = g_gj_trace;
     printf("   t0: setup %lld publish %lld panel0 %lld | panels (upd | sync | publish):", g[1] - g[0], g[2] - g[1], g[3] - g[2]);
     for (int t = 0; t < 8 && g[8 + 4 * t]; ++t) printf(" %lld|%lld|%lld", g[9 + 4 * t] - g[8 + 4 * t], g[10 + 4 * t] - g[9 + 4 * t], g[11 + 4 * t] - g[10 + 4 * t]);
@@ -38,6 +39,7 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416) k(const float* A, float*
     for (int t = 0; t < 8 && g[128 + 8 + 4 * t]; ++t) printf(" %lld", g[128 + 9 + 4 * t] - g[128 + 8 + 4 * t]);
     printf("  total %lld\n   factor(panel 0) steps:", g[4] - g[0]);
     for (int q = 1; q <= 8; ++q) printf(" %lld", g[200 + q] - g[200 + q - 1]);
+#endif
     printf("\n");
   }
   if (which == 0) r = gj_inverse_lookahead<NP>(a, work, work, invT, lds, n, scr, 1e-10f);
