@@ -454,16 +454,16 @@ __device__ bool gj_inverse_lookahead(const float* a, float* work, float* inv, fl
     }
     if (k0 == 0) GJS(0);
     bool fail = false;
+    // pivot-search key of row i for the current step: |value| bits, row index in the low 7
+    unsigned best = 0u;
+#pragma unroll
+    for (int h = 0; h < PROWS; ++h) {
+      const unsigned key = used[h] ? 0u : ((__float_as_uint(fabsf(pv[h][0])) & ~127u) | (unsigned)(127 - (lane + 32 * h)));
+      best = max(best, key);
+    }
 #pragma unroll
     for (int s = 0; s < PW; ++s) {
       if (s < pw) {
-        unsigned best = 0u;
-#pragma unroll
-        for (int h = 0; h < PROWS; ++h) {
-          const int i = lane + 32 * h;
-          const unsigned key = used[h] ? 0u : ((__float_as_uint(fabsf(pv[h][s])) & ~127u) | (unsigned)(127 - i));
-          best = max(best, key);
-        }
         const unsigned wbest = __reduce_max_sync(0xffffffffu, best);
         const int pr = 127 - (int)(wbest & 127u);
         const int ph = pr >> 5, pl = pr & 31;
@@ -477,7 +477,24 @@ __device__ bool gj_inverse_lookahead(const float* a, float* work, float* inv, fl
         }
         const float piv = prv[s];
         if (!(fabsf(piv) > thresh) || !isfinite(piv)) fail = true;
-        const float ip = __frcp_rn(piv);
+        // next step's key without the reciprocal: |piv a_{i,s+1} - a_{i,s} prv_{s+1}| =
+        // |piv| |a'_{i,s+1}|, and |piv| is common to every row, so the argmax is that of the
+        // updated column; the pivot search of step s+1 then overlaps this step's update
+        if (s + 1 < PW) {
+          best = 0u;
+#pragma unroll
+          for (int h = 0; h < PROWS; ++h) {
+            const bool live = !(used[h] || (lane + 32 * h) == pr);
+            const float sc = fmaf(piv, pv[h][s + 1], -(pv[h][s] * prv[s + 1]));
+            const unsigned key = live ? ((__float_as_uint(fabsf(sc)) & ~127u) | (unsigned)(127 - (lane + 32 * h))) : 0u;
+            best = max(best, key);
+          }
+        }
+        // MUFU reciprocal + one Newton step (~28 cycles on the pivot chain vs ~78 for
+        // __frcp_rn's range-checked path; tools/micro/redux.cu).  |piv| > thresh > 0 here.
+        float ip;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ip) : "f"(piv));
+        ip = fmaf(ip, fmaf(-piv, ip, 1.f), ip);
         // branch-free: every row takes the elimination update, the pivot row (lane-uniform
         // values prv * ip) is selected in afterwards
         float pip[PW];
