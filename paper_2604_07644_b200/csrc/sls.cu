@@ -233,6 +233,14 @@ __global__ void __launch_bounds__(256) k_sls_assemble(DevSls S, gsls_qp_t qp, co
 
 // Grid leaves (float64 algebra, float32 result): Qu^-1, P = Qx - Qux' Qu^-1 Qux,
 // A = A_k - B_k Qu^-1 Qux, C = B_k Qu^-1 B_k'.  1x4 output tiles.
+// L2 prefetch of a contiguous operand that a kernel reads only after its first phase
+// (one bulk request from one thread; the range is widened to 16-byte alignment).
+__device__ inline void prefetch_l2(const void* p, size_t bytes) {
+  const unsigned long long a = (unsigned long long)p & ~15ull;
+  const unsigned long long e = ((unsigned long long)p + bytes + 15ull) & ~15ull;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
+}
+
 __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   const int cell = blockIdx.x, inst = blockIdx.y;
   const int2 kj = S.cell_kj[cell];
@@ -256,6 +264,11 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
     }
     return;
   }
+  const size_t st = (size_t)inst * N + k;
+  if (threadIdx.x == 0) {  // the epilogue's operands, read after the inverse and the products
+    prefetch_l2(Qx, (size_t)n * n * sizeof(double));
+    prefetch_l2(qp.A + st * n * n, (size_t)n * n * sizeof(float));
+  }
   extern __shared__ double smd[];
   const int np = ldg;                // row length of the n-vectors below (padded, zero tail)
   double* Qu = smd;                  // m x m
@@ -266,7 +279,6 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   double* BQT = BT + m * np;         // m x np   (B_k Qu^-1)^T
   double* wk = BQT + m * np;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) Qu[e] = S.Qu[cb * m * m + e];
-  const size_t st = (size_t)inst * N + k;
   const float* Bg = qp.B + st * n * m;
   for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
     const int l = e / np, i = e - l * np;
@@ -360,6 +372,11 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   float* Pn = reinterpret_cast<float*>(wk + 2 * kMaxM * (kMaxM + 1) + 8);  // n x lds
   float* Ak = Pn + n * lds;                                                // n x lds
   const float* Pg = S.Ps + ((size_t)inst * S.cvf_nslots + S.cvf_out[cell_of(N, k + 1, j)]) * MS;
+  if (threadIdx.x == 0) {  // Qu, Qux: read after the B' P+ product
+    const size_t cbp = (size_t)inst * S.ncell + cell;
+    prefetch_l2(S.Qu + cbp * m * m, (size_t)m * m * sizeof(double));
+    prefetch_l2(S.Qux + cbp * m * n, (size_t)m * n * sizeof(double));
+  }
   cta_load_async(Pn, lds, Pg, n);
   cp_async_commit();
   const size_t st = (size_t)inst * N + k;
