@@ -84,13 +84,16 @@ def details(path: str) -> None:
         print(f"== launch {i}: {name}")
         for ln in lines:
             print("  " + ln)
+        uu = dict(zip(rh, raw[1])) if len(raw) > 1 else {}
         for k, v in rawv.get(i, {}).items():
-            print(f"  {k}: {v}")
+            print(f"  {k}: {v} {uu.get(k, '')}".rstrip())
         units = raw[1] if len(raw) > 1 else []
-        if units:
+        if units:  # each metric in its own unit (ncu scales them independently)
             u = dict(zip(rh, units))
-            b = sum(float((rawv.get(i, {}).get(k) or "0").replace(",", "")) for k in RAW[:2])
-            print(f"  traffic (dram read + write): {b:.4g} {u.get('dram__bytes_read.sum', '')}")
+            scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+            b = sum(float((rawv.get(i, {}).get(k) or "0").replace(",", "")) * scale.get(u.get(k, "byte"), 1.0)
+                    for k in RAW[:2])
+            print(f"  traffic (dram read + write): {b / 1e9:.4g} Gbyte")
 
 
 def lines(path: str, kernel: str) -> None:
