@@ -172,6 +172,15 @@ int gsls_ctx_export_solution(gsls_ctx* ctx, float* K, double* k, float* P, doubl
  * Phi^u, tau); cells with k = N carry the terminal ones (Qx_term, tau_term via
  * column j).  Phi^x is defined on every cell. */
 int gsls_sls_ncell(int32_t N);
+/* Column sharding of the SLS objects: restricts this context's
+ * SLS work and storage to disturbance columns [j0, j1) (j1 = -1: N).  Every SLS
+ * array then holds only the shard's cells, in the same order at shard-local index
+ * cell(k, j) - cell(j0 + 1, j0); gsls_sls_tighten returns the shard's partial sums
+ * of h and hf (sum them over shards, e.g. an all-reduce); tau_term is written for
+ * the shard's columns only.  Columns are independent (sls.py:227-318), so a
+ * shard's cells equal those of the unsharded synthesis.  Call before the first
+ * SLS call on ctx. */
+int gsls_sls_set_columns(gsls_ctx* ctx, int32_t j0, int32_t j1);
 /* Host-side inspection of the merged column schedules: cvf = 1 the reverse
  * CVF grid scan (leaves at cell(k, j) for k in [j+1, N]), cvf = 0 the forward
  * product scan (leaf of position p at cell(p+1, j)).  ops as gsls_scan_plan;

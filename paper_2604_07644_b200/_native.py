@@ -91,6 +91,7 @@ _SIGS = {
     "gsls_ctx_export_solution": ([c_void_p] * 6, ctypes.c_int),
     "gsls_admm_build_cache": ([c_void_p, ctypes.POINTER(Qp), c_void_p, c_void_p], ctypes.c_int),
     "gsls_sls_ncell": ([ctypes.c_int32], ctypes.c_int),
+    "gsls_sls_set_columns": ([c_void_p, ctypes.c_int32, ctypes.c_int32], ctypes.c_int),
     "gsls_sls_plan": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_int32] + [c_int32_p] * 6, ctypes.c_int),
     "gsls_sls_assemble": ([c_void_p, ctypes.POINTER(Qp)] + [c_void_p] * 5 + [ctypes.c_int32, c_void_p], ctypes.c_int),
     "gsls_sls_set_costs": ([c_void_p] * 5, ctypes.c_int),

@@ -40,6 +40,7 @@ int rti_apply(Ctx* c, const double* px, const double* pu, const double* dx, cons
               const double* QNw, const double* xref, const double* uref, double* cost, cudaStream_t st);
 int sls_export(Ctx* c, float* phix, float* phiu, float* gains, cudaStream_t st);
 int rollout(Ctx* c, const gsls_rollout_args_t* in, const gsls_rollout_out_t* out, cudaStream_t st);
+int sls_set_columns(Ctx* c, int j0, int j1);
 }  // namespace gsls
 
 using namespace gsls;
@@ -149,6 +150,11 @@ int gsls_ctx_export_solution(gsls_ctx* ctx, float* K, double* k, float* P, doubl
 }
 
 int gsls_sls_ncell(int32_t N) { return N * (N + 1) / 2; }
+
+int gsls_sls_set_columns(gsls_ctx* ctx, int32_t j0, int32_t j1) {
+  if (!ctx) return fail_null("ctx");
+  return sls_set_columns(ctx->impl, j0, j1);
+}
 
 int gsls_sls_plan(int32_t N, int32_t cvf, int32_t max_ops, int32_t* ops, int32_t* layer_off, int32_t* out_cell,
                   int32_t* n_ops, int32_t* n_layers, int32_t* n_slots) {

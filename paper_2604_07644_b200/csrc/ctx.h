@@ -78,6 +78,7 @@ struct Ctx {
   bool cache_valid = false;
   bool admm_prebuilt = false;  // gsls_admm_build_cache ran: the next ADMM solve skips its first build
   void* sls = nullptr;         // SLS workspace (sls.cu), allocated on first use
+  int sls_j0 = 0, sls_j1 = -1; // SLS disturbance-column shard [j0, j1) (-1: N), gsls_sls_set_columns
 };
 
 // Matrix half of the CVF combine on an explicit slot space (lqr.cu); shared by

@@ -31,30 +31,33 @@ int check_errors(Ctx* c, cudaStream_t st, const char* what);
 void set_error(int code, int inst, int where, int aux, int label, const char* msg);
 __host__ __device__ inline int cell_of(int N, int k, int j) { return j * N - j * (j - 1) / 2 + (k - j - 1); }
 
-// merge per-column plans into one layered plan with remapped slots
-static ScanPlan merge_columns(int N, bool cvf) {
-  const int ncell = N * (N + 1) / 2;
+// merge the per-column plans of columns [j0, j1) into one layered plan with remapped
+// slots; leaves sit at the shard-local cell index cell(k, j) - cell(j0 + 1, j0)
+static ScanPlan merge_columns(int N, bool cvf, int j0 = 0, int j1 = -1) {
+  if (j1 < 0) j1 = N;
+  const int cell0 = cell_of(N, j0 + 1, j0);
+  const int ncell = cell_of(N, j1 + 1, j1) - cell0;
   ScanPlan out;
   const int len = cvf ? N + 1 : N;
   out.layers = scan_depth(len);
   std::vector<std::vector<ScanOp>> per_layer(out.layers);
   out.out.assign(ncell, -1);
   int next = ncell;
-  for (int j = 0; j < N; ++j) {
+  for (int j = j0; j < j1; ++j) {
     std::vector<char> neutral(len, 0);
     for (int p = 0; p < len; ++p) neutral[p] = cvf ? (p <= j) : (p < j);
     ScanPlan pj = make_scan_plan(len, cvf, neutral, 0);
     const int base = next;
     auto remap = [&](int s) -> int {
       if (s < 0) return -1;
-      if (s < len) return cvf ? cell_of(N, s, j) : cell_of(N, s + 1, j);  // leaf position
+      if (s < len) return (cvf ? cell_of(N, s, j) : cell_of(N, s + 1, j)) - cell0;  // leaf position
       return base + (s - len);
     };
     next += pj.nslots - len;
     for (int l = 0; l < pj.layers; ++l)
       for (int o = pj.layer_off[l]; o < pj.layer_off[l + 1]; ++o)
         per_layer[l].push_back({remap(pj.ops[o].dst), remap(pj.ops[o].earlier), remap(pj.ops[o].later)});
-    for (int k = j + 1; k <= N; ++k) out.out[cell_of(N, k, j)] = remap(pj.out[cvf ? k : k - 1]);
+    for (int k = j + 1; k <= N; ++k) out.out[cell_of(N, k, j) - cell0] = remap(pj.out[cvf ? k : k - 1]);
   }
   for (int l = 0; l < out.layers; ++l) {
     out.layer_off.push_back((int)out.ops.size());
@@ -68,6 +71,7 @@ static ScanPlan merge_columns(int N, bool cvf) {
 
 struct DevSls {
   int n, m, c, nf, N, ldg, ncell, cmax;
+  int j0, j1, cell0;  // column shard [j0, j1); ncell counts its cells, which start at global cell0
   const int2* cell_kj;
   const int4* cvf_ops;
   const int* cvf_out;
@@ -107,18 +111,21 @@ static int sls_init(Ctx* c) {
   DevSls& S = s->dev;
   const int N = d.N, n = d.nx, m = d.nu;
   S.n = n; S.m = m; S.c = d.nc; S.nf = d.nf; S.N = N; S.ldg = ldg_of(n);
-  S.ncell = N * (N + 1) / 2;
+  S.j0 = c->sls_j0;
+  S.j1 = c->sls_j1 < 0 ? N : c->sls_j1;
+  S.cell0 = cell_of(N, S.j0 + 1, S.j0);
+  S.ncell = cell_of(N, S.j1 + 1, S.j1) - S.cell0;
   S.cmax = std::max(1, std::max(d.nc, d.nf));
-  s->cvf = merge_columns(N, true);
-  s->mp = merge_columns(N, false);
+  s->cvf = merge_columns(N, true, S.j0, S.j1);
+  s->mp = merge_columns(N, false, S.j0, S.j1);
   int rc = upload_plan(c, s->cvf, &S.cvf_ops, &S.cvf_out, &S.cvf_loff);
   if (!rc) rc = upload_plan(c, s->mp, &S.mp_ops, &S.mp_out, &S.mp_loff);
   if (rc) return rc;
   S.cvf_nslots = s->cvf.nslots; S.cvf_nops = (int)s->cvf.ops.size(); S.cvf_layers = s->cvf.layers;
   S.mp_nslots = s->mp.nslots; S.mp_nops = (int)s->mp.ops.size(); S.mp_layers = s->mp.layers;
   std::vector<int2> kj(S.ncell);
-  for (int j = 0; j < N; ++j)
-    for (int k = j + 1; k <= N; ++k) kj[cell_of(N, k, j)] = make_int2(k, j);
+  for (int j = S.j0; j < S.j1; ++j)
+    for (int k = j + 1; k <= N; ++k) kj[cell_of(N, k, j) - S.cell0] = make_int2(k, j);
   int2* dkj = (int2*)dev_alloc(c, sizeof(int2) * S.ncell);
   if (!dkj) return GSLS_ERR_CUDA;
   GSLS_CUDA_CHECK(cudaMemcpy(dkj, kj.data(), sizeof(int2) * S.ncell, cudaMemcpyHostToDevice));
@@ -350,8 +357,8 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   float* Mbase = S.Ms + (size_t)inst * S.mp_nslots * MS;
   float* MTbase = S.MsT + (size_t)inst * S.mp_nslots * MS;
   if (k == N) {
-    float* Ml = Mbase + (size_t)cell_of(N, j + 1, j) * MS;
-    float* MTl = MTbase + (size_t)cell_of(N, j + 1, j) * MS;
+    float* Ml = Mbase + (size_t)(cell_of(N, j + 1, j) - S.cell0) * MS;
+    float* MTl = MTbase + (size_t)(cell_of(N, j + 1, j) - S.cell0) * MS;
     const float* Ej = E + ((size_t)inst * N + j) * n * n;
     for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
       const int i = e / ldg, jj = e - i * ldg;
@@ -371,7 +378,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   double* wk = Ga + m * m;
   float* Pn = reinterpret_cast<float*>(wk + 2 * kMaxM * (kMaxM + 1) + 8);  // n x lds
   float* Ak = Pn + n * lds;                                                // n x lds
-  const float* Pg = S.Ps + ((size_t)inst * S.cvf_nslots + S.cvf_out[cell_of(N, k + 1, j)]) * MS;
+  const float* Pg = S.Ps + ((size_t)inst * S.cvf_nslots + S.cvf_out[cell_of(N, k + 1, j) - S.cell0]) * MS;
   if (threadIdx.x == 0) {  // Qu, Qux: read after the B' P+ product
     const size_t cbp = (size_t)inst * S.ncell + cell;
     prefetch_l2(S.Qu + cbp * m * m, (size_t)m * m * sizeof(double));
@@ -449,8 +456,8 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
     if (jj < n) Kg[l * n + jj] = (float)(-s);
   }
   __syncthreads();
-  float* Ml = Mbase + (size_t)cell_of(N, k + 1, j) * MS;  // product leaf of position k
-  float* MTl = MTbase + (size_t)cell_of(N, k + 1, j) * MS;
+  float* Ml = Mbase + (size_t)(cell_of(N, k + 1, j) - S.cell0) * MS;  // product leaf of position k
+  float* MTl = MTbase + (size_t)(cell_of(N, k + 1, j) - S.cell0) * MS;
   for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {  // A + B K (1x4 tiles)
     const int i = e / q4, j0 = (e - i * q4) << 2;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -587,12 +594,12 @@ __global__ void k_sls_tighten(DevSls S, double* h, double* hf) {
   for (int e = threadIdx.x; e < N * c; e += blockDim.x) {
     const int k = e / c, r = e - k * c;
     double s = 0.0;
-    for (int j = 0; j < k; ++j) s += rn[(size_t)cell_of(N, k, j) * S.cmax + r];
+    for (int j = S.j0; j < min(k, S.j1); ++j) s += rn[(size_t)(cell_of(N, k, j) - S.cell0) * S.cmax + r];
     h[(size_t)inst * N * c + e] = s;
   }
   for (int f = threadIdx.x; f < nf; f += blockDim.x) {
     double s = 0.0;
-    for (int j = 0; j < N; ++j) s += rn[(size_t)cell_of(N, N, j) * S.cmax + f];
+    for (int j = S.j0; j < S.j1; ++j) s += rn[(size_t)(cell_of(N, N, j) - S.cell0) * S.cmax + f];
     hf[(size_t)inst * nf + f] = s;
   }
 }
@@ -619,7 +626,8 @@ __global__ void k_sls_duals(DevSls S, const double* lam, double eps, double* tau
   }
   for (int e = threadIdx.x; e < N * nf; e += blockDim.x) {
     const int j = e / nf, f = e - j * nf;
-    const double v = S.have_response ? rn[(size_t)cell_of(N, N, j) * S.cmax + f] : 0.0;
+    if (j < S.j0 || j >= S.j1) continue;  // terminal cells of other shards' columns
+    const double v = S.have_response ? rn[(size_t)(cell_of(N, N, j) - S.cell0) * S.cmax + f] : 0.0;
     const double b = v * v;
     const double l = fmax(lam_t[f], 0.0);
     tau_term[(size_t)inst * N * nf + e] = l / sqrt(b + eps);
@@ -821,6 +829,22 @@ int sls_export_costs(Ctx* c, double* Qx, double* Qu, double* Qux, cudaStream_t s
 }
 
 int sls_ncell(int N) { return N * (N + 1) / 2; }
+
+int sls_set_columns(Ctx* c, int j0, int j1) {
+  const int N = c->dims.N;
+  if (j1 < 0) j1 = N;
+  if (j0 < 0 || j1 > N || j0 >= j1) {
+    set_error(GSLS_ERR_ARG, -1, 0, 0, 0, "SLS column range must satisfy 0 <= j0 < j1 <= N");
+    return GSLS_ERR_ARG;
+  }
+  if (c->sls && (c->sls_j0 != j0 || (c->sls_j1 < 0 ? N : c->sls_j1) != j1)) {
+    set_error(GSLS_ERR_ARG, -1, 0, 0, 0, "SLS column range must be set before the first SLS call");
+    return GSLS_ERR_ARG;
+  }
+  c->sls_j0 = j0;
+  c->sls_j1 = j1;
+  return GSLS_OK;
+}
 
 int sls_plan(int N, int cvf, int max_ops, int* ops, int* layer_off, int* out, int* n_ops, int* n_layers,
              int* n_slots) {

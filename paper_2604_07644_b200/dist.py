@@ -11,6 +11,7 @@ is the build's addition on top of the drop-in entry points.
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -77,6 +78,47 @@ def gather_results(local: torch.Tensor, world: int, out: torch.Tensor | None = N
     parts = [buf[r * mx:r * mx + c] for r, c in enumerate(counts)]
     full = torch.cat(parts, 0)
     return full if out is None else out.copy_(full)
+
+
+def column_shards(N: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous disturbance-column ranges [j0, j1), one per rank, balanced by SLS
+    cell count (column j holds N - j cells, so early columns are heavier)."""
+    if world < 1:
+        raise ValueError(f"bad world {world}")
+    if N < world:
+        raise ValueError(f"{N} columns cannot be split over {world} ranks")
+    total = N * (N + 1) // 2
+    prefix = [j * N - j * (j - 1) // 2 for j in range(N + 1)]   # cells in columns [0, j)
+    bounds = [0]
+    for r in range(1, world):
+        lo, hi = bounds[-1] + 1, N - (world - r)                 # at least one column per rank
+        target = total * r / world
+        bounds.append(min(range(lo, hi + 1), key=lambda j: abs(prefix[j] - target)))
+    bounds.append(N)
+    return [(bounds[r], bounds[r + 1]) for r in range(world)]
+
+
+def allreduce_tightening(h: torch.Tensor, hf: torch.Tensor, world: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """Sum the per-shard partial tightenings over ranks (one all-reduce of N*nc + nf
+    floats; NCCL on the GPU box, gloo in the CPU tests)."""
+    if world == 1:
+        return h, hf
+    flat = torch.cat([h.reshape(-1), hf.reshape(-1)])
+    dist.all_reduce(flat, op=dist.ReduceOp.SUM)
+    return flat[: h.numel()].reshape(h.shape), flat[h.numel():].reshape(hf.shape)
+
+
+def sls_tighten_sharded(A, B, E, costs, C, D, CN, rank: int, world: int, executor=None):
+    """SLS synthesis + tightening with the disturbance columns sharded over ranks
+    (SURVEY §8f row 3): each rank synthesizes its columns only (memory and work
+    divided by ~world) and the partial h, hf are all-reduced.  Returns
+    (sls.Tightening on every rank, this rank's (j0, j1), its shard-local phix, phiu)."""
+    from . import sls
+    N = np.asarray(A).shape[0]
+    cols = column_shards(N, world)[rank]
+    h, hf, phix, phiu = sls.synthesize_tighten_columns(A, B, E, costs, C, D, CN, cols, executor)
+    h, hf = allreduce_tightening(h, hf, world)
+    return sls.Tightening(h=h.cpu().numpy(), hf=hf.cpu().numpy()), cols, phix, phiu
 
 
 def max_over_ranks(ms: float, world: int, device=None) -> float:

@@ -199,12 +199,19 @@ class _Ws:
         return self.version
 
 
-def _ws(n, m, c, nf, N, executor=None) -> _Ws:
+def _ws(n, m, c, nf, N, executor=None, columns=None) -> _Ws:
     dev = resolve(executor)
     cache = dev.__dict__.setdefault("_sls_ws", {})
-    key = (n, m, c, nf, N)
+    key = (n, m, c, nf, N) + ((tuple(columns),) if columns is not None else ())
     if key not in cache:
-        cache[key] = _Ws(*key)
+        ws = _Ws(n, m, c, nf, N)
+        if columns is not None:  # column shard: every SLS array holds only the shard's cells
+            j0, j1 = columns
+            nat.check(ws.ctx.lib.gsls_sls_set_columns(ws.ctx.handle, j0, j1), "sls columns")
+            ws.columns = (j0, j1)
+            ws.cell0 = cell_index(N, j0 + 1, j0)
+            ws.ncell = cell_index(N, j1 + 1, j1) - ws.cell0
+        cache[key] = ws
     return cache[key]
 
 
@@ -345,6 +352,42 @@ def tighten(response: SlsResponse, C, D, CN, executor=None) -> Tightening:
     nat.check(ws.ctx.lib.gsls_sls_tighten(ws.ctx.handle, ctypes.byref(s), h.data_ptr() if h.numel() else None,
                                           hf.data_ptr() if hf.numel() else None, stream_ptr()), "tighten")
     return Tightening(h=to_host(h[0]), hf=to_host(hf[0]))
+
+
+def synthesize_tighten_columns(A, B, E, costs: SlsCosts, C, D, CN, columns, executor=None):
+    """One column shard of synthesize + tighten: the disturbance
+    columns j in ``columns = (j0, j1)`` only (sls.py:227-341; columns are independent).
+
+    Returns (h_part, hf_part, phix, phiu): the shard's partial sums of the stage /
+    terminal tightening (sum them over shards) and its response cells, shard-local
+    (cell(k, j) - cell(j0 + 1, j0)), float32 device tensors."""
+    A, B, E = np.asarray(A, float), np.asarray(B, float), np.asarray(E, float)
+    C, D, CN = np.asarray(C, float), np.asarray(D, float), np.asarray(CN, float)
+    N, n, m = A.shape[0], A.shape[-1], B.shape[-1]
+    c, nf = C.shape[1], CN.shape[0]
+    ws = _ws(n, m, c, nf, N, executor, columns=columns)
+    sl = slice(ws.cell0, ws.cell0 + ws.ncell)
+    Qx = to_dev(ragged_to_cells(costs.Qx, N, (n, n), terminal=costs.Qx_term)[sl], F64)[None].contiguous()
+    Qu = to_dev(ragged_to_cells(costs.Qu, N, (m, m))[sl], F64)[None].contiguous()
+    Qux = to_dev(ragged_to_cells(costs.Qux, N, (m, n))[sl], F64)[None].contiguous()
+    lib, hd = ws.ctx.lib, ws.ctx.handle
+    nat.check(lib.gsls_sls_set_costs(hd, Qx.data_ptr(), Qu.data_ptr(), Qux.data_ptr(), stream_ptr()), "set costs")
+    ws.qp.A.copy_(to_dev(A, F32)[None])
+    ws.qp.B.copy_(to_dev(B, F32)[None])
+    ws.E.copy_(to_dev(E, F32)[None])
+    _set_constraints(ws, C, D, CN)
+    st = ws.qp.cstruct()
+    nat.check(lib.gsls_sls_synthesize(hd, ctypes.byref(st), ws.E.data_ptr(), stream_ptr()), "synthesize")
+    dev = ws.qp.QN.device
+    h = torch.zeros(1, N, c, dtype=F64, device=dev)
+    hf = torch.zeros(1, nf, dtype=F64, device=dev)
+    nat.check(lib.gsls_sls_tighten(hd, ctypes.byref(st), h.data_ptr() if h.numel() else None,
+                                   hf.data_ptr() if hf.numel() else None, stream_ptr()), "tighten")
+    phix = torch.empty(ws.ncell, n, n, dtype=F32, device=dev)
+    phiu = torch.empty(ws.ncell, m, n, dtype=F32, device=dev)
+    nat.check(lib.gsls_sls_export(hd, phix.data_ptr(), phiu.data_ptr(), None, stream_ptr()), "export response")
+    ws.resp_ver = ws.bump()
+    return h[0], hf[0], phix, phiu
 
 
 def sls_cost(response: SlsResponse, weights: SlsWeights) -> float:

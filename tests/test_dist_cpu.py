@@ -78,3 +78,78 @@ def test_gloo_world2_gather_matches_single_rank(total):
     assert full.shape == ref.shape
     np.testing.assert_array_equal(full, ref)
     assert ms == 11.0
+
+
+# --- SLS disturbance columns sharded over ranks -----------------------
+
+def test_column_shards_cover_and_balance():
+    for N in (1, 2, 7, 25, 64, 2047):
+        for world in (1, 2, 3, 8):
+            if world > N:
+                with pytest.raises(ValueError):
+                    D.column_shards(N, world)
+                continue
+            sh = D.column_shards(N, world)
+            assert sh[0][0] == 0 and sh[-1][1] == N and len(sh) == world
+            assert all(a < b for a, b in sh) and all(sh[r][1] == sh[r + 1][0] for r in range(world - 1))
+            cells = [sum(N - j for j in range(a, b)) for a, b in sh]
+            # within one (largest) column of the even split
+            assert max(cells) - N * (N + 1) / 2 / world <= N
+
+
+def _sls_problem(seed=0, N=9, nx=3, nu=2, nc=2):
+    from oracle import sls as osls
+    rng = np.random.default_rng(seed)
+    A = np.eye(nx) + 0.1 * rng.standard_normal((N, nx, nx))
+    B = rng.standard_normal((N, nx, nu))
+    E = 0.05 * rng.standard_normal((N, nx, nx))
+    C = rng.standard_normal((N, nc, nx))
+    Dm = rng.standard_normal((N, nc, nu))
+    CN = rng.standard_normal((1, nx))
+    costs = osls.assemble_costs(None, C, Dm, CN, osls.Weights.identity(nx, nu))
+    return A, B, E, C, Dm, CN, osls.synthesize(A, B, E, costs)
+
+
+def _partial_tighten(resp, C, Dm, CN, j0, j1):
+    """The shard's partial sums: columns j in [j0, j1) only (sls.py:329-341 restricted)."""
+    from oracle import sls as osls
+    N, nc, nf = resp.N, C.shape[1], CN.shape[0]
+    h, hf = np.zeros((N, nc)), np.zeros(nf)
+    for k in range(1, N):
+        for j in range(j0, min(k, j1)):
+            h[k] += osls.row_norms(C[k] @ resp.phi_x(k, j) + Dm[k] @ resp.phi_u(k, j))
+    for j in range(j0, j1):
+        hf += osls.row_norms(CN @ resp.phi_x(N, j))
+    return h, hf
+
+
+def _sls_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A, B, E, C, Dm, CN, resp = _sls_problem()
+        j0, j1 = D.column_shards(resp.N, world)[rank]
+        h, hf = _partial_tighten(resp, C, Dm, CN, j0, j1)
+        H, HF = D.allreduce_tightening(torch.as_tensor(h), torch.as_tensor(hf), world)
+        if rank == 0:
+            q.put((H.numpy(), HF.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_tightening_matches_unsharded():
+    from oracle import sls as osls
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sls_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    H, HF = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A, B, E, C, Dm, CN, resp = _sls_problem()
+    ref = osls.tighten(resp, C, Dm, CN)
+    np.testing.assert_allclose(H, ref.h, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(HF, ref.hf, rtol=1e-12, atol=1e-12)
