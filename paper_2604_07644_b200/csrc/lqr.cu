@@ -321,11 +321,14 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   float* rec = a.rec ? a.rec + (long long)inst * a.rec_inst_stride + (size_t)(a.op_base + blockIdx.x) * 4 * MS
                      : nullptr;
 
+  // fin: an unrecorded combine whose output only feeds the scan result (plan .w): its
+  // A and C are never read, so Ar^T, W2, Psi, A and C are skipped (4 of 8 GEMMs)
+  const bool fin = (op.w & 1) && rec == nullptr;
   cta_load_async(b0, lds, a.Ps + ib + ol, n);   // Pr (= Pr^T)
   cta_load_async(b1, lds, a.Cs + ib + oe, n);   // Cl (= Cl^T)
   cp_async_commit();
   cta_load_async(b3, lds, a.As + ib + oe, n);   // Al
-  cta_load_async(b4, lds, a.ATs + ib + ol, n);  // Ar^T
+  if (!fin) cta_load_async(b4, lds, a.ATs + ib + ol, n);  // Ar^T
   cp_async_commit();
   cp_async_wait<1>();
   __syncthreads();
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   CTRACE(2);
   gemm_tn(n, b0, b3, lds, EpiSmem{b5, lds, n, false});  // W1 = Pr Al
   __syncthreads();
-  gemm_tn(n, b1, b4, lds, EpiSmem{b0, lds, n, false});  // W2 = Cl Ar^T (over Pr)
+  if (!fin) gemm_tn(n, b1, b4, lds, EpiSmem{b0, lds, n, false});  // W2 = Cl Ar^T (over Pr)
   __syncthreads();
   CTRACE(3);
   // Minv = M1^{-1} -> b1 (row-major, over Cl), Minv^T -> b2 (over M1, read first)
@@ -353,6 +356,10 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   __syncthreads();
   if (rec) cta_store(rec + 1 * MS, b1, lds, n);          // X record
   gemm_tn(n, b3, b1, lds, EpiGlobal{a.Ps + ib + od, a.Ps + ib + oe, ldg, n, nullptr});  // P = Al^T V + Pl
+  if (fin) {
+    CTRACE(5);
+    return;
+  }
   gemm_tn(n, b2, b4, lds, EpiSmem{b5, lds, n, false});  // Psi^T = Minv Ar^T (over W1)
   __syncthreads();
   if (rec) cta_store(rec + 2 * MS, b5, lds, n);          // Psi record
@@ -652,7 +659,19 @@ int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_l
 
 int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff) {
   std::vector<int4> h(p.ops.size() ? p.ops.size() : 1);
-  for (size_t i = 0; i < p.ops.size(); ++i) h[i] = make_int4(p.ops[i].dst, p.ops[i].earlier, p.ops[i].later, 0);
+  // .w = 1: no later layer reads this op's output slot, so only its scan output is
+  // consumed (k_cvf_combine then skips the A / C half of an unrecorded combine)
+  std::vector<char> read_later(std::max(p.nslots, 1), 0);
+  for (int l = (int)p.layer_off.size() - 2; l >= 0; --l) {
+    for (int o = p.layer_off[l]; o < p.layer_off[l + 1]; ++o) {
+      const ScanOp& q = p.ops[o];
+      h[o] = make_int4(q.dst, q.earlier, q.later, (q.dst >= 0 && !read_later[q.dst]) ? 1 : 0);
+    }
+    for (int o = p.layer_off[l]; o < p.layer_off[l + 1]; ++o) {
+      if (p.ops[o].earlier >= 0) read_later[p.ops[o].earlier] = 1;
+      if (p.ops[o].later >= 0) read_later[p.ops[o].later] = 1;
+    }
+  }
   int4* dops = (int4*)dev_alloc(c, h.size() * sizeof(int4));
   int* dout = (int*)dev_alloc(c, (p.out.size() + 1) * sizeof(int));
   int* dl = (int*)dev_alloc(c, (p.layer_off.size() + 1) * sizeof(int));
