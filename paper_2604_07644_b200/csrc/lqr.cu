@@ -363,6 +363,10 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   gemm_tn(n, b2, b4, lds, EpiSmem{b5, lds, n, false});  // Psi^T = Minv Ar^T (over W1)
   __syncthreads();
   if (rec) cta_store(rec + 2 * MS, b5, lds, n);          // Psi record
+  if (op.w & 1) {  // recorded combine whose A, C no later layer reads
+    CTRACE(5);
+    return;
+  }
   gemm_tn(n, b5, b3, lds, EpiGlobal{a.As + ib + od, nullptr, ldg, n, a.ATs + ib + od});  // A = Psi Al (+ A^T)
   gemm_tn(n, b5, b0, lds, EpiGlobal{a.Cs + ib + od, a.Cs + ib + ol, ldg, n, nullptr});   // C = Psi W2 + Cr
   __syncthreads();
