@@ -499,7 +499,8 @@ __global__ void __launch_bounds__(512) k_matprod(float* Ms, float* MsT, long lon
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
-  gemm_tn(n, Lt, Er, lds, EpiGlobal{base + (size_t)op.x * MS, nullptr, ldg, n, baseT + (size_t)op.x * MS});
+  // plan .w = 1: no later product reads this slot, so its transposed copy is dead
+  gemm_tn(n, Lt, Er, lds, EpiGlobal{base + (size_t)op.x * MS, nullptr, ldg, n, (op.w & 1) ? nullptr : baseT + (size_t)op.x * MS});
 }
 
 // Phi^u_{k,j} = K_{k,j} Phi^x_{k,j} (sls.py:310-318).
