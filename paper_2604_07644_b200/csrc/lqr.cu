@@ -339,7 +339,9 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   CTRACE(2);
   gemm_tn(n, b0, b3, lds, EpiSmem{b5, lds, n, false});  // W1 = Pr Al
   __syncthreads();
-  if (!fin) gemm_tn(n, b1, b4, lds, EpiSmem{b0, lds, n, false});  // W2 = Cl Ar^T (over Pr)
+  // C dead (plan .w bit 1): W2 only feeds C (and the -Y record)
+  const bool need_w2 = !fin && (rec != nullptr || !(op.w & 2));
+  if (need_w2) gemm_tn(n, b1, b4, lds, EpiSmem{b0, lds, n, false});  // W2 = Cl Ar^T (over Pr)
   __syncthreads();
   CTRACE(3);
   // Minv = M1^{-1} -> b1 (row-major, over Cl), Minv^T -> b2 (over M1, read first)
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
     return;
   }
   gemm_tn(n, b5, b3, lds, EpiGlobal{a.As + ib + od, nullptr, ldg, n, a.ATs + ib + od});  // A = Psi Al (+ A^T)
-  gemm_tn(n, b5, b0, lds, EpiGlobal{a.Cs + ib + od, a.Cs + ib + ol, ldg, n, nullptr});   // C = Psi W2 + Cr
+  if (!(op.w & 2)) gemm_tn(n, b5, b0, lds, EpiGlobal{a.Cs + ib + od, a.Cs + ib + ol, ldg, n, nullptr});  // C = Psi W2 + Cr
   __syncthreads();
   CTRACE(5);
 #undef CTRACE
@@ -663,17 +665,26 @@ int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_l
 
 int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff) {
   std::vector<int4> h(p.ops.size() ? p.ops.size() : 1);
-  // .w = 1: no later layer reads this op's output slot, so only its scan output is
-  // consumed (k_cvf_combine then skips the A / C half of an unrecorded combine)
-  std::vector<char> read_later(std::max(p.nslots, 1), 0);
+  // .w bit 0: no later layer reads this op's output slot, so only its scan output is
+  // consumed (k_cvf_combine then skips the A / C half of an unrecorded combine).
+  // .w bit 1: the output's C is dead: no later op reads the slot as its earlier operand
+  // (C_l enters M1) nor as the later operand of a combine that computes its own C.
+  const int ns = std::max(p.nslots, 1);
+  std::vector<char> read_later(ns, 0), needs_c(ns, 0);
   for (int l = (int)p.layer_off.size() - 2; l >= 0; --l) {
     for (int o = p.layer_off[l]; o < p.layer_off[l + 1]; ++o) {
       const ScanOp& q = p.ops[o];
-      h[o] = make_int4(q.dst, q.earlier, q.later, (q.dst >= 0 && !read_later[q.dst]) ? 1 : 0);
+      const bool fin = q.dst >= 0 && !read_later[q.dst];
+      const bool cdead = q.dst >= 0 && !needs_c[q.dst];
+      h[o] = make_int4(q.dst, q.earlier, q.later, (fin ? 1 : 0) | (cdead ? 2 : 0));
     }
     for (int o = p.layer_off[l]; o < p.layer_off[l + 1]; ++o) {
-      if (p.ops[o].earlier >= 0) read_later[p.ops[o].earlier] = 1;
-      if (p.ops[o].later >= 0) read_later[p.ops[o].later] = 1;
+      const ScanOp& q = p.ops[o];
+      if (q.earlier >= 0) read_later[q.earlier] = needs_c[q.earlier] = 1;
+      if (q.later >= 0) {
+        read_later[q.later] = 1;
+        if (!(h[o].w & 2)) needs_c[q.later] = 1;  // this op forms C = Psi W2 + C_r
+      }
     }
   }
   int4* dops = (int4*)dev_alloc(c, h.size() * sizeof(int4));
