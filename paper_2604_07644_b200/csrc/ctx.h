@@ -98,7 +98,8 @@ struct CombineArgs {
 int launch_combine(const CombineArgs& a, int nops, int count, cudaStream_t st);
 int combine_threads(int n);
 int matmul_threads(int n);
-int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff);
+enum { PLAN_CVF = 0, PLAN_CVF_REC = 1, PLAN_OTHER = 2 };  // upload_plan dead-output analysis
+int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff, int kind);
 void sls_destroy(Ctx* c);
 
 void* dev_alloc(Ctx* c, size_t bytes);

@@ -321,8 +321,8 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   float* rec = a.rec ? a.rec + (long long)inst * a.rec_inst_stride + (size_t)(a.op_base + blockIdx.x) * 4 * MS
                      : nullptr;
 
-  // fin: an unrecorded combine whose output only feeds the scan result (plan .w): its
-  // A and C are never read, so Ar^T, W2, Psi, A and C are skipped (4 of 8 GEMMs)
+  // fin: an unrecorded combine whose output's A, A^T and C are all dead (plan .w bit 0):
+  // only P is formed, so Ar^T, W2, Psi, A and C are skipped (4 of 8 GEMMs)
   const bool fin = (op.w & 1) && rec == nullptr;
   cta_load_async(b0, lds, a.Ps + ib + ol, n);   // Pr (= Pr^T)
   cta_load_async(b1, lds, a.Cs + ib + oe, n);   // Cl (= Cl^T)
@@ -663,27 +663,37 @@ int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_l
 // ---------------------------------------------------------------------------
 // context
 
-int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff) {
+int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff, int kind) {
   std::vector<int4> h(p.ops.size() ? p.ops.size() : 1);
-  // .w bit 0: no later layer reads this op's output slot, so only its scan output is
-  // consumed (k_cvf_combine then skips the A / C half of an unrecorded combine).
-  // .w bit 1: the output's C is dead: no later op reads the slot as its earlier operand
-  // (C_l enters M1) nor as the later operand of a combine that computes its own C.
+  // Dead-output flags in .w, from the last layer back (kind: PLAN_CVF / PLAN_CVF_REC /
+  // PLAN_OTHER).  For a CVF combine (dst <- earlier (x) later) a reader needs, of its
+  // earlier operand, C, A and P always; of its later operand, P always, A^T when the
+  // reader forms Psi (its own A, A^T or C is live, or it is recorded) and C when the
+  // reader forms its own C.
+  //   bit 0: CVF: the output's A, A^T and C are all dead (only P may be read);
+  //          other plans: the slot is never read again.
+  //   bit 1: CVF: the output's C is dead.
   const int ns = std::max(p.nslots, 1);
-  std::vector<char> read_later(ns, 0), needs_c(ns, 0);
+  std::vector<char> rd(ns, 0), nA(ns, 0), nAT(ns, 0), nC(ns, 0);
+  const bool cvf = kind != PLAN_OTHER, rec = kind == PLAN_CVF_REC;
   for (int l = (int)p.layer_off.size() - 2; l >= 0; --l) {
     for (int o = p.layer_off[l]; o < p.layer_off[l + 1]; ++o) {
       const ScanOp& q = p.ops[o];
-      const bool fin = q.dst >= 0 && !read_later[q.dst];
-      const bool cdead = q.dst >= 0 && !needs_c[q.dst];
-      h[o] = make_int4(q.dst, q.earlier, q.later, (fin ? 1 : 0) | (cdead ? 2 : 0));
+      int w = 0;
+      if (q.dst >= 0) {
+        if (!cvf) w = rd[q.dst] ? 0 : 1;
+        else w = ((nA[q.dst] || nAT[q.dst] || nC[q.dst]) ? 0 : 1) | (nC[q.dst] ? 0 : 2);
+      }
+      h[o] = make_int4(q.dst, q.earlier, q.later, w);
     }
     for (int o = p.layer_off[l]; o < p.layer_off[l + 1]; ++o) {
       const ScanOp& q = p.ops[o];
-      if (q.earlier >= 0) read_later[q.earlier] = needs_c[q.earlier] = 1;
+      const bool psi = rec || !(h[o].w & 1), ownc = !(h[o].w & 2);
+      if (q.earlier >= 0) rd[q.earlier] = nA[q.earlier] = nC[q.earlier] = 1;
       if (q.later >= 0) {
-        read_later[q.later] = 1;
-        if (!(h[o].w & 2)) needs_c[q.later] = 1;  // this op forms C = Psi W2 + C_r
+        rd[q.later] = 1;
+        if (psi) nAT[q.later] = 1;
+        if (ownc) nC[q.later] = 1;
       }
     }
   }
@@ -732,8 +742,8 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
 
   DevLqr& L = c->dev;
   L.n = d.nx; L.m = d.nu; L.c = d.nc; L.nf = d.nf; L.N = d.N; L.ldg = c->ldg; L.mtot = c->mtot;
-  int rc = upload_plan(c, c->cvf, &L.cvf_ops, &L.cvf_out, &L.cvf_loff);
-  if (!rc && d.N > 0) rc = upload_plan(c, c->cot, &L.cot_ops, &L.cot_out, &L.cot_loff);
+  int rc = upload_plan(c, c->cvf, &L.cvf_ops, &L.cvf_out, &L.cvf_loff, PLAN_CVF_REC);
+  if (!rc && d.N > 0) rc = upload_plan(c, c->cot, &L.cot_ops, &L.cot_out, &L.cot_loff, PLAN_OTHER);
   if (rc) { delete c; return rc; }
   L.cvf_nphys = compress_slots(c->cvf, c->cvf_phys);
   L.cot_nphys = d.N > 0 ? compress_slots(c->cot, c->cot_phys) : 0;

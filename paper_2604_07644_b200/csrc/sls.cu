@@ -118,8 +118,8 @@ static int sls_init(Ctx* c) {
   S.cmax = std::max(1, std::max(d.nc, d.nf));
   s->cvf = merge_columns(N, true, S.j0, S.j1);
   s->mp = merge_columns(N, false, S.j0, S.j1);
-  int rc = upload_plan(c, s->cvf, &S.cvf_ops, &S.cvf_out, &S.cvf_loff);
-  if (!rc) rc = upload_plan(c, s->mp, &S.mp_ops, &S.mp_out, &S.mp_loff);
+  int rc = upload_plan(c, s->cvf, &S.cvf_ops, &S.cvf_out, &S.cvf_loff, PLAN_CVF);
+  if (!rc) rc = upload_plan(c, s->mp, &S.mp_ops, &S.mp_out, &S.mp_loff, PLAN_OTHER);
   if (rc) return rc;
   S.cvf_nslots = s->cvf.nslots; S.cvf_nops = (int)s->cvf.ops.size(); S.cvf_layers = s->cvf.layers;
   S.mp_nslots = s->mp.nslots; S.mp_nops = (int)s->mp.ops.size(); S.mp_layers = s->mp.layers;
