@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
     CTRACE(5);
     return;
   }
-  gemm_tn(n, b5, b3, lds, EpiGlobal{a.As + ib + od, nullptr, ldg, n, a.ATs + ib + od});  // A = Psi Al (+ A^T)
+  gemm_tn(n, b5, b3, lds, EpiGlobal{a.As + ib + od, nullptr, ldg, n, (op.w & 4) ? nullptr : a.ATs + ib + od});  // A = Psi Al (+ A^T)
   if (!(op.w & 2)) gemm_tn(n, b5, b0, lds, EpiGlobal{a.Cs + ib + od, a.Cs + ib + ol, ldg, n, nullptr});  // C = Psi W2 + Cr
   __syncthreads();
   CTRACE(5);
@@ -673,6 +673,7 @@ int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, co
   //   bit 0: CVF: the output's A, A^T and C are all dead (only P may be read);
   //          other plans: the slot is never read again.
   //   bit 1: CVF: the output's C is dead.
+  //   bit 2: CVF: the output's A^T is dead (no transposed copy).
   const int ns = std::max(p.nslots, 1);
   std::vector<char> rd(ns, 0), nA(ns, 0), nAT(ns, 0), nC(ns, 0);
   const bool cvf = kind != PLAN_OTHER, rec = kind == PLAN_CVF_REC;
@@ -682,7 +683,7 @@ int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, co
       int w = 0;
       if (q.dst >= 0) {
         if (!cvf) w = rd[q.dst] ? 0 : 1;
-        else w = ((nA[q.dst] || nAT[q.dst] || nC[q.dst]) ? 0 : 1) | (nC[q.dst] ? 0 : 2);
+        else w = ((nA[q.dst] || nAT[q.dst] || nC[q.dst]) ? 0 : 1) | (nC[q.dst] ? 0 : 2) | (nAT[q.dst] ? 0 : 4);
       }
       h[o] = make_int4(q.dst, q.earlier, q.later, w);
     }
