@@ -99,7 +99,8 @@ int launch_combine(const CombineArgs& a, int nops, int count, cudaStream_t st);
 int combine_threads(int n);
 int matmul_threads(int n);
 enum { PLAN_CVF = 0, PLAN_CVF_REC = 1, PLAN_OTHER = 2 };  // upload_plan dead-output analysis
-int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff, int kind);
+int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff, int kind,
+                const int** leaf_dead = nullptr);
 void sls_destroy(Ctx* c);
 
 void* dev_alloc(Ctx* c, size_t bytes);

@@ -663,7 +663,8 @@ int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_l
 // ---------------------------------------------------------------------------
 // context
 
-int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff, int kind) {
+int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff, int kind,
+                const int** leaf_dead) {
   std::vector<int4> h(p.ops.size() ? p.ops.size() : 1);
   // Dead-output flags in .w, from the last layer back (kind: PLAN_CVF / PLAN_CVF_REC /
   // PLAN_OTHER).  For a CVF combine (dst <- earlier (x) later) a reader needs, of its
@@ -697,6 +698,14 @@ int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, co
         if (ownc) nC[q.later] = 1;
       }
     }
+  }
+  if (leaf_dead) {  // per leaf slot (< p.length): bit 0 A dead, bit 1 A^T dead, bit 2 C dead
+    std::vector<int> lf(std::max(p.length, 1), 0);
+    for (int i = 0; i < p.length && i < ns; ++i) lf[i] = (nA[i] ? 0 : 1) | (nAT[i] ? 0 : 2) | (nC[i] ? 0 : 4);
+    int* dlf = (int*)dev_alloc(c, lf.size() * sizeof(int));
+    if (!dlf) return GSLS_ERR_CUDA;
+    GSLS_CUDA_CHECK(cudaMemcpy(dlf, lf.data(), lf.size() * sizeof(int), cudaMemcpyHostToDevice));
+    *leaf_dead = dlf;
   }
   int4* dops = (int4*)dev_alloc(c, h.size() * sizeof(int4));
   int* dout = (int*)dev_alloc(c, (p.out.size() + 1) * sizeof(int));

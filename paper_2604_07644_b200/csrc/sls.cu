@@ -73,6 +73,7 @@ struct DevSls {
   int n, m, c, nf, N, ldg, ncell, cmax;
   int j0, j1, cell0;  // column shard [j0, j1); ncell counts its cells, which start at global cell0
   const int2* cell_kj;
+  const int* leaf_dead;  // per cell: bit 0 A, bit 1 A^T, bit 2 C of its CVF leaf never read
   const int4* cvf_ops;
   const int* cvf_out;
   const int* cvf_loff;
@@ -118,7 +119,7 @@ static int sls_init(Ctx* c) {
   S.cmax = std::max(1, std::max(d.nc, d.nf));
   s->cvf = merge_columns(N, true, S.j0, S.j1);
   s->mp = merge_columns(N, false, S.j0, S.j1);
-  int rc = upload_plan(c, s->cvf, &S.cvf_ops, &S.cvf_out, &S.cvf_loff, PLAN_CVF);
+  int rc = upload_plan(c, s->cvf, &S.cvf_ops, &S.cvf_out, &S.cvf_loff, PLAN_CVF, &S.leaf_dead);
   if (!rc) rc = upload_plan(c, s->mp, &S.mp_ops, &S.mp_out, &S.mp_loff, PLAN_OTHER);
   if (rc) return rc;
   S.cvf_nslots = s->cvf.nslots; S.cvf_nops = (int)s->cvf.ops.size(); S.cvf_layers = s->cvf.layers;
@@ -311,6 +312,7 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   }
   __syncthreads();
   const float* Ak = qp.A + st * n * n;
+  const int dead = S.leaf_dead[cell];  // parts of this leaf no combine reads (scan-plan analysis)
   const int q4 = np >> 2;
   for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
     const int i = e / q4, j0 = (e - i * q4) << 2;
@@ -337,11 +339,11 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
       po[t] = in ? (float)(Qx[i * n + jj] - p4[t]) : 0.f;
       ao[t] = in ? (float)((double)Ak[i * n + jj] - a4[t]) : 0.f;
       co[t] = in ? (float)c4[t] : 0.f;
-      if (in) ATd[(size_t)jj * ldg + i] = ao[t];
+      if (in && !(dead & 2)) ATd[(size_t)jj * ldg + i] = ao[t];
     }
     *reinterpret_cast<float4*>(Pd + (size_t)i * ldg + j0) = make_float4(po[0], po[1], po[2], po[3]);
-    *reinterpret_cast<float4*>(Ad + (size_t)i * ldg + j0) = make_float4(ao[0], ao[1], ao[2], ao[3]);
-    *reinterpret_cast<float4*>(Cd + (size_t)i * ldg + j0) = make_float4(co[0], co[1], co[2], co[3]);
+    if (!(dead & 1)) *reinterpret_cast<float4*>(Ad + (size_t)i * ldg + j0) = make_float4(ao[0], ao[1], ao[2], ao[3]);
+    if (!(dead & 4)) *reinterpret_cast<float4*>(Cd + (size_t)i * ldg + j0) = make_float4(co[0], co[1], co[2], co[3]);
   }
 }
 
