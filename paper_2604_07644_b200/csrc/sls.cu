@@ -479,9 +479,18 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
     for (int t = 0; t < 4; ++t) {
       const int jj = j0 + t;
       o[t] = (jj < n) ? (float)((double)a4[t] + acc[t]) : 0.f;
-      if (jj < n) MTl[(size_t)jj * ldg + i] = o[t];
+      if (jj < n) Pn[jj * lds + i] = o[t];  // transpose staged in smem (P+ is dead here)
     }
     *reinterpret_cast<float4*>(Ml + (size_t)i * ldg + j0) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+  __syncthreads();
+  // M^T rows: coalesced 16-byte stores instead of one scattered store per element
+  for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
+    const int jj = e / q4, i0 = (e - jj * q4) << 2;
+    float v[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) v[t] = (i0 + t < n) ? Pn[jj * lds + i0 + t] : 0.f;
+    *reinterpret_cast<float4*>(MTl + (size_t)jj * ldg + i0) = make_float4(v[0], v[1], v[2], v[3]);
   }
 }
 
