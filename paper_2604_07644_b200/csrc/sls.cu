@@ -571,15 +571,42 @@ __global__ void __launch_bounds__(256) k_sls_rownorm(DevSls S, gsls_qp_t qp) {
   const size_t st = (size_t)inst * N + k;
   const float* Ck = qp.C + st * c * n;
   const float* Dk = qp.D + st * c * m;
+  // C_k, D_k staged in smem; thread task = (row r, 4 columns): 4 independent FMA chains
+  // per l from one broadcast C value and one 16-byte Phi^x row load
+  float* Cs = Pu + m * n;          // c x n
+  float* Ds = Cs + c * n;          // c x m
+  const int poff = (n * ldg + m * n + c * n + c * m + 1) & ~1;        // 8-byte aligned
+  double* part = reinterpret_cast<double*>(sm + poff);              // c x q4 partial sums of squares
+  for (int e = threadIdx.x; e < c * n; e += blockDim.x) Cs[e] = Ck[e];
+  for (int e = threadIdx.x; e < c * m; e += blockDim.x) Ds[e] = Dk[e];
+  __syncthreads();
+  const int q4 = ldg >> 2;
+  for (int t = threadIdx.x; t < c * q4; t += blockDim.x) {
+    const int r = t / q4, i0 = (t - r * q4) << 2;
+    float s[4] = {0.f, 0.f, 0.f, 0.f}, u[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int l = 0; l < n; ++l) {
+      const float cv = Cs[r * n + l];
+      const float4 p = *reinterpret_cast<const float4*>(Px + l * ldg + i0);
+      s[0] = fmaf(cv, p.x, s[0]); s[1] = fmaf(cv, p.y, s[1]); s[2] = fmaf(cv, p.z, s[2]); s[3] = fmaf(cv, p.w, s[3]);
+    }
+    for (int a = 0; a < m; ++a) {
+      const float dv = Ds[r * m + a];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) u[q] = fmaf(dv, (i0 + q < n) ? Pu[a * n + i0 + q] : 0.f, u[q]);
+    }
+    double ss = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (i0 + q < n) {
+        const double v = (double)(s[q] + u[q]);
+        ss += v * v;
+      }
+    part[t] = ss;
+  }
+  __syncthreads();
   for (int r = warp; r < c; r += nw) {
     double ss = 0.0;
-    for (int i = lane; i < n; i += 32) {
-      float s1 = 0.f, s2 = 0.f;
-      for (int l = 0; l < n; ++l) s1 = fmaf(Ck[r * n + l], Px[l * ldg + i], s1);
-      for (int a = 0; a < m; ++a) s2 = fmaf(Dk[r * m + a], Pu[a * n + i], s2);
-      const double v = (double)(s1 + s2);
-      ss += v * v;
-    }
+    for (int q = lane; q < q4; q += 32) ss += part[r * q4 + q];
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     if (lane == 0) rn[r] = sqrt(ss);
   }
@@ -762,7 +789,8 @@ int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st,
 
 static int sls_rownorms(Ctx* c, const gsls_qp_t* qp, cudaStream_t st) {
   DevSls& S = sls_of(c)->dev;
-  const size_t sb = ((size_t)S.n * S.ldg + S.m * S.n) * sizeof(float);
+  const size_t sb = (((size_t)S.n * S.ldg + S.m * S.n + (size_t)S.c * S.n + S.c * S.m + 1) & ~(size_t)1) * sizeof(float) +
+                    (size_t)S.c * (S.ldg / 4) * sizeof(double);
   int rc = smem_attr((const void*)k_sls_rownorm, sb);
   if (rc) return rc;
   ProfScope ps(P_SLS_ROWNORM, st, (double)S.ncell * c->dims.batch);
