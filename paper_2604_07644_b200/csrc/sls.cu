@@ -529,11 +529,24 @@ __global__ void __launch_bounds__(256) k_sls_phiu(DevSls S) {
   const size_t cb = (size_t)inst * S.ncell + cell;
   const float* Kg = S.Kc + cb * m * n;
   float* Pug = S.Phiu + cb * m * n;
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
-    const int a = e / n, i = e - a * n;
-    float s = 0.f;
-    for (int l = 0; l < n; ++l) s = fmaf(Kg[a * n + l], Px[l * ldg + i], s);
-    Pug[e] = s;
+  float* Ks = Px + n * ldg;  // K staged in smem (m x n)
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) Ks[e] = Kg[e];
+  __syncthreads();
+  // Phi^u = K Phi^x: thread task = (row a, 4 columns), one broadcast K value and one
+  // 16-byte Phi^x row load per l
+  const int q4 = ldg >> 2;
+  for (int t = threadIdx.x; t < m * q4; t += blockDim.x) {
+    const int a = t / q4, i0 = (t - a * q4) << 2;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    for (int l = 0; l < n; ++l) {
+      const float kv = Ks[a * n + l];
+      const float4 p = *reinterpret_cast<const float4*>(Px + l * ldg + i0);
+      s0 = fmaf(kv, p.x, s0); s1 = fmaf(kv, p.y, s1); s2 = fmaf(kv, p.z, s2); s3 = fmaf(kv, p.w, s3);
+    }
+    const float sv[4] = {s0, s1, s2, s3};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (i0 + q < n) Pug[a * n + i0 + q] = sv[q];
   }
 }
 
@@ -777,7 +790,7 @@ int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st,
     }
   }
   {
-    const size_t sb = (size_t)n * ldg * sizeof(float);
+    const size_t sb = ((size_t)n * ldg + (size_t)m * n) * sizeof(float);
     if ((rc = smem_attr((const void*)k_sls_phiu, sb))) return rc;
     ProfScope ps(P_SLS_PHIU, st, (double)S.ncell * B);
     k_sls_phiu<<<dim3(S.ncell, B), 256, sb, st>>>(S);
