@@ -387,17 +387,22 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
     prefetch_l2(S.Qux + cbp * m * n, (size_t)m * n * sizeof(double));
   }
   cta_load_async(Pn, lds, Pg, n);
-  cp_async_commit();
   const size_t st = (size_t)inst * N + k;
   const float* Bg = qp.B + st * n * m;
   const float* Ag = qp.A + st * n * n;
+  for (int e = threadIdx.x; e < n * np; e += blockDim.x) {  // A_k: 4-byte async copies (rows of n floats)
+    const int i = e / np, jj = e - i * np;
+    if (jj < n) {
+      const unsigned d = (unsigned)__cvta_generic_to_shared(Ak + i * lds + jj);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(Ag + i * n + jj) : "memory");
+    } else {
+      Ak[i * lds + jj] = 0.f;
+    }
+  }
+  cp_async_commit();
   for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
     const int l = e / np, i = e - l * np;
     BT[e] = (i < n) ? (double)Bg[i * m + l] : 0.0;
-  }
-  for (int e = threadIdx.x; e < n * np; e += blockDim.x) {
-    const int i = e / np, jj = e - i * np;
-    Ak[i * lds + jj] = (jj < n) ? Ag[i * n + jj] : 0.f;
   }
   cp_async_wait<0>();
   __syncthreads();
