@@ -48,6 +48,7 @@ struct ReplayArgs {
   long long scratch_floats;
   int max_layer;  // max ops in any scan layer (t1/t2 sizing)
   unsigned long long* trace;  // GSLS_REPLAY_TRACE: phase timestamps of the first iteration (rank 0)
+  int prefetch;               // k_replay: bulk-prefetch the next tree layer's records into L2
 };
 
 constexpr int kReplayThreads = 512;
@@ -192,6 +193,18 @@ __device__ __forceinline__ double widen_scaled(uint32_t u) {
   return __hiloint2double((int)hi, (int)(u << 29));
 }
 constexpr double kWidenUnscale = 0x1p896;
+
+// L2 prefetch of a contiguous byte range (the next tree layer's recorded operators),
+// issued by one thread in <= 1 MB bulk requests; addresses widened to 16-byte alignment.
+__device__ inline void prefetch_l2_range(const void* p, size_t bytes) {
+  unsigned long long a = (unsigned long long)p & ~15ull;
+  const unsigned long long e = ((unsigned long long)p + bytes + 15ull) & ~15ull;
+  while (a < e) {
+    const unsigned long long len = (e - a) < (1ull << 20) ? (e - a) : (1ull << 20);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)len) : "memory");
+    a += len;
+  }
+}
 
 // Stage operator product for one (4*RQ)-row block: acc = M x (+ M2 x2), both
 // column-major with leading dimension ld (rows padded with zeros).  Lane
@@ -541,7 +554,15 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
   };
   TR();
 
+  // one CTA per instance: every stage's operators are contiguous, so whole phases are
+  // prefetched into L2 one phase ahead (the next layer's records, the next phase's
+  // stage operators)
+  const bool pf = a.prefetch && cs == 1 && admm && tid == 0;
+  if (pf) prefetch_l2_range(X23, (size_t)N * c * L.ld2n * sizeof(float));
   for (;;) {
+    if (pf && L.cvf_layers > 0)
+      prefetch_l2_range(cvf_rec + (size_t)s_cvf_loff[0] * 4 * MS,
+                        (size_t)(s_cvf_loff[1] - s_cvf_loff[0]) * 4 * MS * sizeof(float));
     // ---- CVF leaves: [p; b]_k = pb0_k + X23_k (y - z)_k (fused augment_linear +
     //      _linear_element_terms, admm.py:113-121, lqr.py:338-342) --------------------
     if (admm) {
@@ -601,6 +622,15 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
     // ---- CVF replay (reverse tree): ops of a layer spread over the cluster ------
     for (int lay = 0; lay < L.cvf_layers; ++lay) {
       const int o0 = s_cvf_loff[lay], no = s_cvf_loff[lay + 1] - o0;
+      if (pf && lay + 1 == L.cvf_layers) {  // the feedforward's stage operators
+        prefetch_l2_range(XK, (size_t)N * (n + c) * L.ldm * sizeof(float));
+        prefetch_l2_range(Bcm, (size_t)N * m * L.ldn * sizeof(float));
+      }
+      if (tid == 0 && lay + 1 < L.cvf_layers && a.prefetch) {  // next layer's records -> L2 during this round
+        const int p0 = s_cvf_loff[lay + 1], pn = s_cvf_loff[lay + 2] - p0, pp = (pn + cs - 1) / cs;
+        const int plo = min(pn, rank * pp), pnl = min(pn, plo + pp) - plo;
+        if (pnl > 0) prefetch_l2_range(cvf_rec + (size_t)(p0 + plo) * 4 * MS, (size_t)pnl * 4 * MS * sizeof(float));
+      }
       if (no == 0) continue;
       const int per = (no + cs - 1) / cs;
       const int lo = min(no, rank * per), nl = min(no, lo + per) - lo;
@@ -622,6 +652,8 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
       TR();
     }
 
+    if (pf && L.cot_layers > 0)
+      prefetch_l2_range(cot_rec + (size_t)s_cot_loff[0] * MS, (size_t)(s_cot_loff[1] - s_cot_loff[0]) * MS * sizeof(float));
     // ---- feedforward k = -Gamma (B'(p+ + P+ b) + r) and COT leaves ---------------
     //      (lqr.py:345-356; ADMM: kf = kk0 + X5 p+ + X4 (y - z), cb = B kf + b)
     if (admm) {
@@ -687,6 +719,15 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
     // ---- COT replay (forward tree): 1 round per layer -------------------------
     for (int lay = 0; lay < L.cot_layers; ++lay) {
       const int o0 = s_cot_loff[lay], no = s_cot_loff[lay + 1] - o0;
+      if (pf && lay + 1 == L.cot_layers) {  // the constraint phase, then the next iteration's leaves
+        prefetch_l2_range(ZD, (size_t)N * (n + m) * L.ldc * sizeof(float));
+        prefetch_l2_range(X23, (size_t)N * c * L.ld2n * sizeof(float));
+      }
+      if (tid == 0 && lay + 1 < L.cot_layers && a.prefetch) {
+        const int p0 = s_cot_loff[lay + 1], pn = s_cot_loff[lay + 2] - p0, pp = (pn + cs - 1) / cs;
+        const int plo = min(pn, rank * pp), pnl = min(pn, plo + pp) - plo;
+        if (pnl > 0) prefetch_l2_range(cot_rec + (size_t)(p0 + plo) * MS, (size_t)pnl * MS * sizeof(float));
+      }
       if (no == 0) continue;
       const int per = (no + cs - 1) / cs;
       const int lo = min(no, rank * per), nl = min(no, lo + per) - lo;
@@ -1479,6 +1520,10 @@ static int replay_cluster(Ctx* c, int count, size_t smem_bytes, const void* kern
 static int launch_replay(Ctx* c, ReplayArgs& a, int count, cudaStream_t st) {
   if (count == 0) return GSLS_OK;
   a.L = c->dev;
+  {
+    const char* pf = getenv("GSLS_REPLAY_PREFETCH");
+    a.prefetch = (pf && pf[0] == '0') ? 0 : 1;
+  }
   a.max_layer = std::max(1, std::max(c->cvf_max_layer, c->cot_max_layer));
   size_t sb = 0;
   if (c->d_scratch) {
