@@ -276,14 +276,19 @@ __device__ inline int warp_spd_inverse(const T* M, int ldm, T* inv, int m, T* wo
     }
     __syncwarp();
     bool ok = true, small = false;
+    T rd = T(0);  // lane j keeps 1 / L[j][j]: multiplies instead of divisions on the chain
     for (int j = 0; j < m; ++j) {
       const T d = L[j * ld + j];
       if (!(d > T(0)) || !isfinite((double)d)) { ok = false; break; }
-      const T piv = sqrt(d);
+      const T r = rsqrt(d);
+      const T piv = d * r;
       if ((double)piv * (double)piv < 1e-10) small = true;
       __syncwarp();
-      if (lane == j) L[j * ld + j] = piv;
-      if (lane > j && lane < m) L[lane * ld + j] /= piv;
+      if (lane == j) {
+        L[j * ld + j] = piv;
+        rd = r;
+      }
+      if (lane > j && lane < m) L[lane * ld + j] *= r;
       __syncwarp();
       if (lane > j && lane < m) {
         const T lij = L[lane * ld + j];
@@ -295,12 +300,15 @@ __device__ inline int warp_spd_inverse(const T* M, int ldm, T* inv, int m, T* wo
       if (attempt == 1) return 1;
       continue;
     }
-    if (lane < m) {  // X = L^{-1}: lane j solves L x = e_j
+    {  // X = L^{-1}: lane j solves L x = e_j
       const int j = lane;
       for (int i = 0; i < m; ++i) {
-        T s = (i == j) ? T(1) : T(0);
-        for (int k = j; k < i; ++k) s = fma(-L[i * ld + k], X[k * ld + j], s);
-        X[i * ld + j] = (i < j) ? T(0) : s / L[i * ld + i];
+        const T ri = __shfl_sync(0xffffffffu, rd, i);
+        if (j < m) {
+          T s = (i == j) ? T(1) : T(0);
+          for (int k = j; k < i; ++k) s = fma(-L[i * ld + k], X[k * ld + j], s);
+          X[i * ld + j] = (i < j) ? T(0) : s * ri;
+        }
       }
     }
     __syncwarp();
