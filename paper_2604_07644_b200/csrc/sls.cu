@@ -431,7 +431,13 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
     for (int i = 0; i < n; ++i) s = fma(BtP[l * np + i], BT[t * np + i], s);
     H[e] = Qu[e] + s;
   }
-  for (int e = threadIdx.x; e < m * q4; e += blockDim.x) {  // Qux + B' P+ A (1x4 tiles)
+  __syncthreads();
+  // warp 0 inverts H while warps 1.. form G = Qux + B' P+ A (independent of the inverse)
+  if (threadIdx.x < 32) {
+    if (warp_spd_inverse(H, m, Ga, m, wk) && threadIdx.x == 0)
+      raise_err(S.err + inst, GSLS_ERR_SINGULAR_STAGE, k, j, GSLS_LABEL_QU_BPB);
+  }
+  for (int e = (int)threadIdx.x - 32; e >= 0 && e < m * q4; e += (int)blockDim.x - 32) {  // 1x4 tiles
     const int l = e / q4, j0 = (e - l * q4) << 2;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int i = 0; i < n; ++i) {
@@ -447,11 +453,6 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
       const int jj = j0 + t;
       Gm[l * np + jj] = (jj < n) ? Qux[l * n + jj] + acc[t] : 0.0;
     }
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    if (warp_spd_inverse(H, m, Ga, m, wk) && threadIdx.x == 0)
-      raise_err(S.err + inst, GSLS_ERR_SINGULAR_STAGE, k, j, GSLS_LABEL_QU_BPB);
   }
   __syncthreads();
   float* Kg = S.Kc + cb * m * n;
