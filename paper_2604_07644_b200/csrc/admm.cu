@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
   // one CTA per instance: every stage's operators are contiguous, so whole phases are
   // prefetched into L2 one phase ahead (the next layer's records, the next phase's
   // stage operators)
-  const bool pf = a.prefetch && cs == 1 && admm && tid == 0;
+  const bool pf = a.prefetch == 2 && cs == 1 && admm && tid == 0;  // stage operators too (GSLS_REPLAY_PREFETCH=2)
   if (pf) prefetch_l2_range(X23, (size_t)N * c * L.ld2n * sizeof(float));
   for (;;) {
     if (pf && L.cvf_layers > 0)
@@ -1522,7 +1522,7 @@ static int launch_replay(Ctx* c, ReplayArgs& a, int count, cudaStream_t st) {
   a.L = c->dev;
   {
     const char* pf = getenv("GSLS_REPLAY_PREFETCH");
-    a.prefetch = (pf && pf[0] == '0') ? 0 : 1;
+    a.prefetch = pf ? (pf[0] - '0') : 1;  // 0 off, 1 the next layer's records, 2 also stage operators
   }
   a.max_layer = std::max(1, std::max(c->cvf_max_layer, c->cot_max_layer));
   size_t sb = 0;
