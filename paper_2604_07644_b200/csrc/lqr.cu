@@ -430,13 +430,14 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
     for (int j = 0; j < n; ++j) s = fma(BtP[l * n + j], Bst[j * m + t], s);
     H[e] = Rhat[e] + s;
   }
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+  __syncthreads();
+  // warps 1.. form G = Shat + B' P+ A while warp 0 inverts H (independent)
+  for (int e = (int)threadIdx.x - 32; e >= 0 && e < m * n; e += (int)blockDim.x - 32) {
     const int l = e / n, j = e - l * n;
     double s = 0.0;
     for (int i = 0; i < n; ++i) s = fma(BtP[l * n + i], (double)Ag[i * n + j], s);
     Gm[e] = Shat[e] + s;
   }
-  __syncthreads();
   if (threadIdx.x < 32) {
     if (warp_spd_inverse(H, m, Ga, m, wk) && threadIdx.x == 0)
       raise_err(L.err + inst, GSLS_ERR_SINGULAR_STAGE, k, -1, GSLS_LABEL_R_BPB);
