@@ -1,12 +1,18 @@
-"""Batches of independent MPC instances partitioned across GPUs.
+"""Multi-GPU: batches of independent MPC instances, and one long-horizon SLS.
 
-A single solve stays on one GPU (north star); a batch of scenarios is split
-into contiguous per-rank blocks with no communication inside the step.  After
-each batched step the ranks exchange one compact result record per instance
-(``RESULT_FIELDS``) with a single ``all_gather_into_tensor`` — NCCL over
-NVLink on the GPU box, gloo in the CPU tests.  The reference has no
-multi-process path at all (scan.py:97-128 is thread-level only); this module
-is the build's addition on top of the drop-in entry points.
+* Batches: a batch of scenarios is split into contiguous per-rank
+  blocks with no communication inside the step.  After each batched step the
+  ranks exchange one compact result record per instance (``RESULT_FIELDS``)
+  with a single ``all_gather_into_tensor`` — NCCL over NVLink on the GPU box,
+  gloo in the CPU tests.  A single QP solve stays on one GPU (north star).
+* One SLS across ranks: the disturbance columns of one
+  synthesis are independent, so ``column_shards`` gives each rank a contiguous
+  column range balanced by cell count, ``sls.synthesize_tighten_columns``
+  synthesizes only that shard (``gsls_sls_set_columns``: storage and work divide
+  by the rank count), and ``allreduce_tightening`` sums the partial h, hf.
+
+The reference has no multi-process path at all (scan.py:97-128 is thread-level
+only); this module is the build's addition on top of the drop-in entry points.
 """
 
 from __future__ import annotations
