@@ -634,7 +634,7 @@ __device__ inline double block_min128(double v, double* red) {
   return r;
 }
 
-__global__ void __launch_bounds__(128) k_rollout(RolloutArgs a) {
+__global__ void __launch_bounds__(128, 8) k_rollout(RolloutArgs a) {
   const int s = blockIdx.x, inst = blockIdx.y;
   const int n = a.n, m = a.m, c = a.c, nf = a.nf, N = a.N, S = a.S;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -668,10 +668,10 @@ __global__ void __launch_bounds__(128) k_rollout(RolloutArgs a) {
     for (int l = warp; l < m; l += nw) {
       double acc = 0.0;
       if (phiu)
-        for (int e = lane; e < k * n; e += 32) {
-          const int j = e / n, i = e - j * n;
-          const int cell = j * N - j * (j - 1) / 2 + (k - j - 1);
-          acc = fma((double)phiu[((size_t)cell * m + l) * n + i], wh[e], acc);
+        for (int j = 0; j < k; ++j) {  // row l of Phi^u_{k,j} (contiguous) against w_hat_j
+          const float* pr = phiu + ((size_t)(j * N - j * (j - 1) / 2 + (k - j - 1)) * m + l) * n;
+          const double* wj = wh + (size_t)j * n;
+          for (int i = lane; i < n; i += 32) acc = fma((double)pr[i], wj[i], acc);
         }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
