@@ -162,16 +162,17 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
     for (int r = 0; r < c; ++r) s = fma(Dst[r * m + i], Dst[r * m + j], s);
     Rh[e] = (double)Rg[e] + rho * s;
   }
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+  __syncthreads();
+  // warp 0 inverts R-hat while warps 1.. form S-hat (independent of the inverse)
+  if (threadIdx.x < 32) {
+    if (warp_spd_inverse(Rh, m, Ri, m, wk) && threadIdx.x == 0)
+      raise_err(L.err + inst, GSLS_ERR_SINGULAR_STAGE, k, -1, GSLS_LABEL_R);
+  }
+  for (int e = (int)threadIdx.x - 32; e >= 0 && e < m * n; e += (int)blockDim.x - 32) {
     const int i = e / n, j = e - i * n;
     double s = 0.0;
     for (int r = 0; r < c; ++r) s = fma(Dst[r * m + i], Cst[r * n + j], s);
     Sh[e] = (Sg ? (double)Sg[e] : 0.0) + rho * s;
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    if (warp_spd_inverse(Rh, m, Ri, m, wk) && threadIdx.x == 0)
-      raise_err(L.err + inst, GSLS_ERR_SINGULAR_STAGE, k, -1, GSLS_LABEL_R);
   }
   __syncthreads();
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
