@@ -675,20 +675,34 @@ __device__ bool gj_inverse_lookahead44(const float* a, float* work, float* inv, 
   const int tid = threadIdx.x;
   const bool part = tid < NT;
   const bool pwarp = (tid >> 5) == NW;  // the panel warp
-  static_assert(NP == 64, "4x4 row tiles: (NP / 4)^2 == NP * 4 row threads");
+  constexpr int TC = NP / 16;  // columns per row thread: 4 (NP = 64) or 5 (NP = 80)
+  static_assert(NP == 64 || NP == 80, "4 x TC row tiles: (NP / 4) x 16 == NP * 4 row threads");
   const int lane = tid & 31, warp = tid >> 5;
-  const int rg = tid >> 4, cg = tid & 15;  // rows 4rg..4rg+3, columns 4cg..4cg+3
-  float r[4][4];
+  const int rg = tid >> 4, cg = tid & 15;  // rows 4rg..4rg+3, columns TC cg..TC cg+TC-1
+  float r[4][TC];
   float mx = 0.f;
   GJT(0);
 #pragma unroll
   for (int rr = 0; rr < 4; ++rr)
 #pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-      const int row = 4 * rg + rr, col = 4 * cg + cc;
+    for (int cc = 0; cc < TC; ++cc) {
+      const int row = 4 * rg + rr, col = TC * cg + cc;
       r[rr][cc] = (part && row < n && col < n) ? a[row * lds + col] : 0.f;
       mx = fmaxf(mx, fabsf(r[rr][cc]));
     }
+  auto publish_rows = [&]() {  // this thread's TC-column segment of its 4 rows
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      if (4 * rg + rr >= n) break;
+      float* dst = work + (4 * rg + rr) * lds + TC * cg;
+      if constexpr (TC == 4) {
+        *reinterpret_cast<float4*>(dst) = make_float4(r[rr][0], r[rr][1], r[rr][2], r[rr][3]);
+      } else {
+#pragma unroll
+        for (int cc = 0; cc < TC; ++cc) dst[cc] = r[rr][cc];
+      }
+    }
+  };
   mx = warp_max(mx);
   if (part && lane == 0) pan0[warp] = mx;
   for (int i = tid; i < NP; i += blockDim.x) pstep[i] = -1;
@@ -706,13 +720,7 @@ __device__ bool gj_inverse_lookahead44(const float* a, float* work, float* inv, 
     if (cc < lds) work[i * lds + cc] = 0.f;
   }
   // publish the rows (pre-panel-0 state)
-  if (part && 4 * cg < n) {
-#pragma unroll
-    for (int rr = 0; rr < 4; ++rr)
-      if (4 * rg + rr < n)
-        *reinterpret_cast<float4*>(work + (4 * rg + rr) * lds + 4 * cg) =
-            make_float4(r[rr][0], r[rr][1], r[rr][2], r[rr][3]);
-  }
+  if (part && TC * cg < n) publish_rows();
   __syncthreads();
   const float thresh = rel_tol * misc[0];
   GJT(2);
@@ -877,30 +885,36 @@ __device__ bool gj_inverse_lookahead44(const float* a, float* work, float* inv, 
         const int st = pstep[i];  // entries of panel t+1 may land concurrently: never in [k0, k0 + pw)
         mine[rr] = (st >= k0 && st < k0 + pw);
       }
-      float v[4][4];
+      float v[4][TC];
 #pragma unroll
       for (int rr = 0; rr < 4; ++rr)
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) v[rr][cc] = mine[rr] ? 0.f : r[rr][cc];
-      if (4 * cg < n) {
+        for (int cc = 0; cc < TC; ++cc) v[rr][cc] = mine[rr] ? 0.f : r[rr][cc];
+      if (TC * cg < n) {
 #pragma unroll
         for (int s = 0; s < PW; ++s) {
           if (s < pw) {
-            const float4 tt = *reinterpret_cast<const float4*>(work + prow[k0 + s] * lds + 4 * cg);
+            const float* pr = work + prow[k0 + s] * lds + TC * cg;
+            float tt[TC];
+            if constexpr (TC == 4) {
+              const float4 q4 = *reinterpret_cast<const float4*>(pr);
+              tt[0] = q4.x; tt[1] = q4.y; tt[2] = q4.z; tt[3] = q4.w;
+            } else {
+#pragma unroll
+              for (int cc = 0; cc < TC; ++cc) tt[cc] = pr[cc];
+            }
 #pragma unroll
             for (int rr = 0; rr < 4; ++rr) {
               const float f = cf[rr][s];
-              v[rr][0] = fmaf(f, tt.x, v[rr][0]);
-              v[rr][1] = fmaf(f, tt.y, v[rr][1]);
-              v[rr][2] = fmaf(f, tt.z, v[rr][2]);
-              v[rr][3] = fmaf(f, tt.w, v[rr][3]);
+#pragma unroll
+              for (int cc = 0; cc < TC; ++cc) v[rr][cc] = fmaf(f, tt[cc], v[rr][cc]);
             }
           }
         }
       }
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {  // panel columns take their eliminated entries
-        const int rel = 4 * cg + cc - k0;
+      for (int cc = 0; cc < TC; ++cc) {  // panel columns take their eliminated entries
+        const int rel = TC * cg + cc - k0;
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
           float x = v[rr][cc];
@@ -914,13 +928,7 @@ __device__ bool gj_inverse_lookahead44(const float* a, float* work, float* inv, 
     __syncthreads();  // panel t consumed, panel t+1 factored
     if (t < 8) GJT(10 + 4 * t);
     if (t + 1 < npan) {  // publish the rows after panel t
-      if (part && 4 * cg < n) {
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr)
-          if (4 * rg + rr < n)
-            *reinterpret_cast<float4*>(work + (4 * rg + rr) * lds + 4 * cg) =
-                make_float4(r[rr][0], r[rr][1], r[rr][2], r[rr][3]);
-      }
+      if (part && TC * cg < n) publish_rows();
       __syncthreads();
     }
     if (t < 8) GJT(11 + 4 * t);
@@ -934,8 +942,8 @@ __device__ bool gj_inverse_lookahead44(const float* a, float* work, float* inv, 
       if (row >= n) break;
       const int qi = pstep[row];
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        const int col = 4 * cg + cc;
+      for (int cc = 0; cc < TC; ++cc) {
+        const int col = TC * cg + cc;
         if (col < n) {
           const int d = prow[col];
           if (inv) inv[qi * lds + d] = r[rr][cc];

@@ -346,9 +346,8 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   __syncthreads();
   CTRACE(3);
   // Minv = M1^{-1} -> b1 (row-major, over Cl), Minv^T -> b2 (over M1, read first)
-  bool ok;  // work: b1 (Cl is dead); NP = 64 uses 4x4 (row, column) tiles for the row update
-  if constexpr (NP == 64) ok = gj_inverse_lookahead44<NP>(b2, b1, b1, b2, lds, n, gjbuf, a.rel_tol);
-  else ok = gj_inverse_lookahead<NP>(b2, b1, b1, b2, lds, n, gjbuf, a.rel_tol);
+  // work: b1 (Cl is dead); row threads on 4 x (NP/16) (row, column) tiles
+  const bool ok = gj_inverse_lookahead44<NP>(b2, b1, b1, b2, lds, n, gjbuf, a.rel_tol);
   if (!ok && threadIdx.x == 0)
     raise_err(a.err ? a.err + inst : nullptr, GSLS_ERR_ILL_CONDITIONED, a.op_base + blockIdx.x);
   CTRACE(4);

@@ -29,8 +29,7 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416) k(const float* A, float*
   bool r;
   long long t0 = clock64();
   for (int rep = 0; rep < GJ_REPS; ++rep) {  // timing repetitions (a is re-read each time)
-    if constexpr (NP == 64) GJ_LA(64)(a, work, nullptr, invT, lds, n, scr, 1e-10f);
-    else gj_inverse_lookahead<NP>(a, work, nullptr, invT, lds, n, scr, 1e-10f);
+    GJ_LA(NP)(a, work, nullptr, invT, lds, n, scr, 1e-10f);
     for (int e = threadIdx.x; e < n * lds; e += blockDim.x) a[e] = (e % lds < n) ? A[(e / lds) * n + e % lds] : 0.f;
     __syncthreads();
   }
@@ -48,7 +47,7 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416) k(const float* A, float*
 #endif
     printf("\n");
   }
-  if (which == 0) { if constexpr (NP == 64) r = GJ_LA(64)(a, work, work, invT, lds, n, scr, 1e-10f); else r = gj_inverse_lookahead<NP>(a, work, work, invT, lds, n, scr, 1e-10f); }
+  if (which == 0) r = GJ_LA(NP)(a, work, work, invT, lds, n, scr, 1e-10f);
   else r = gj_inverse_panel<NP>(a, work, work, invT, lds, n, scr, 1e-10f);
   if (threadIdx.x == 0) *ok = r;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
