@@ -131,6 +131,8 @@ def bytes_replay_iter(n, m, c, nf, N):
 # --------------------------------------------------------------------------- CPU arms
 
 def _oracle_worker(args):
+    """One oracle rti_robust_step of scenario `idx` (float64 numpy, one core); returns its
+    wall time and the outputs the parity block compares with the GPU's instance `idx`."""
     tag, idx = args
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     sys.path.insert(0, ROOT)
@@ -143,9 +145,39 @@ def _oracle_worker(args):
     tau.tau = wl.tau
     tau.tau_term = wl.tau_term
     x = wl.scenario_states(idx, 1)[0]
+    st = oracle.admm.State.fresh(wl.N * m.nc + m.nf, rs.sqp.admm.rho0)
+    prev = oracle.sqp.Trajectory(wl.prev_x, wl.prev_u, m.dt)
     t = time.perf_counter()
-    r = oracle.sls.rti_robust_step(m, x, oracle.sqp.Trajectory(wl.prev_x, wl.prev_u, m.dt), tau, rs)
-    return time.perf_counter() - t, r.stats.admm_iterations
+    r = oracle.sls.rti_robust_step(m, x, prev, tau, rs, warm_admm=st)
+    dt = time.perf_counter() - t
+    qp = oracle.sqp.linearize(m, prev, r.tightening, x)
+    f = np.concatenate([qp.f.ravel(), qp.fN])
+    return {"t": dt, "iters": r.stats.admm_iterations, "rho_changes": st.generation, "idx": idx,
+            "active": st.z >= f - 1e-12, "u0": r.u0, "h": r.tightening.h, "hf": r.tightening.hf}
+
+
+def parity_block(eng, res, first=0):
+    """bench.py parity: the GPU instances `first + r['idx']` of the timed batch vs the oracle
+    results `res` (same scenarios): ADMM iterations, rho changes and the active set exactly,
+    u0 / h within 1e-4 (reference.relative_error)."""
+    import oracle
+    z = eng.state.z.cpu().numpy()
+    f = np.concatenate([eng.qp.f.cpu().numpy().reshape(eng.B, -1), eng.qp.fN.cpu().numpy()], axis=1)
+    its, rc = eng.stats.iterations.cpu().numpy(), eng.stats.rho_changes.cpu().numpy()
+    u0, h = eng.u0.cpu().numpy(), eng.h.cpu().numpy()
+    n_it = n_act = 0
+    e_u0 = e_h = 0.0
+    for r in res:
+        i = r["idx"] - first
+        n_it += int(its[i] == r["iters"] and rc[i] == r["rho_changes"])
+        n_act += int(((z[i] >= f[i] - 1e-12) == r["active"]).all())
+        e_u0 = max(e_u0, oracle.relative_error(u0[i], r["u0"]))
+        e_h = max(e_h, oracle.relative_error(h[i], r["h"]))
+    n = len(res)
+    return {"instances": n, "checker": "oracle (float64 restatement of the reference, pinned by tests/golden)",
+            "admm_iterations_and_rho_changes_exact": f"{n_it}/{n}", "active_set_exact": f"{n_act}/{n}",
+            "u0_max_rel_err": e_u0, "h_max_rel_err": e_h, "tol": 1e-4,
+            "pass": bool(n_it == n and n_act == n and e_u0 <= 1e-4 and e_h <= 1e-4)}
 
 
 def oracle_settings(model):
@@ -191,7 +223,7 @@ def run_reference(args):
             dt, res = cpu_round(pool, "q61", (args.warmup + k) * cores, cores)
             t_tot += dt
             n_tot += len(res)
-            per.extend(r[0] for r in res)
+            per.extend(r["t"] for r in res)
     finally:
         pool.close()
     value = n_tot / t_tot
@@ -442,6 +474,7 @@ def run_ours(args):
 
     # ---- CPU baseline (rank 0, N=1 only) -----------------------------------------
     cpu = None
+    parity = None
     if world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
         pool = make_pool(cores)
@@ -451,6 +484,7 @@ def run_ours(args):
             pool.close()
         cpu = {"value": len(res) / dt, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{cores} q61 scenarios, one oracle rti_robust_step each (single-threaded numpy per core)"}
+        parity = parity_block(eng, res)
 
     launches = int(pl.sum())
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -467,7 +501,7 @@ def run_ours(args):
            "gpu_launches": launches, "roofline": roof, "roofline_by_kernel": rl, "phases": phases,
            "rollout": rollout_line,
            "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
-           "cpu_baseline": cpu}
+           "cpu_baseline": cpu, "parity": parity}
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()

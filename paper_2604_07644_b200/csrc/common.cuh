@@ -27,21 +27,49 @@ __host__ __device__ inline int lds_of(int n) {
 }
 __host__ __device__ inline size_t mat_elems(int n) { return (size_t)n * ldg_of(n); }
 
-// Per-instance error record written by kernels (first writer wins).
+// Per-instance error record.  Kernels run stages / cells / ops in parallel, but
+// the reference raises the FIRST failure of its sequential loops: spd_inverse
+// names the lowest stage (lqr.py:204-215), _locate_singular the first valid
+// (k, j) in row-major order (sls.py:321-326), linearize the first stage, its
+// dynamics before its constraints (sqp.py:122-131), and the phases run in
+// order (leaves, then the scan, then the gains; lqr.py:379-402).  So every
+// raise is packed into one 64-bit key ordered as (phase, where, aux, label),
+// and the record keeps the minimum (atomicMax on the complement; 0 = none).
 struct ErrSlot {
-  int code;   // gsls_status_t
-  int where;  // stage / op / position
-  int aux;    // column j (SLS) or -1
-  int label;  // GSLS_LABEL_*
+  unsigned long long key;
 };
+
+struct ErrInfo {
+  int code, where, aux, label;
+};
+
+__host__ __device__ inline int err_phase(int code, int label) {
+  if (code == GSLS_ERR_ILL_CONDITIONED) return 2;                              // the combine tree
+  if (label == GSLS_LABEL_R_BPB || label == GSLS_LABEL_QU_BPB) return 3;      // gains after the scan
+  return 1;                                                                    // leaves / linearize
+}
+
+__host__ __device__ inline unsigned long long err_pack(int code, int where, int aux, int label) {
+  const unsigned long long p = (unsigned long long)(err_phase(code, label) & 0xF) << 60 |
+                               (unsigned long long)((unsigned)where & 0xFFFFFFu) << 36 |
+                               (unsigned long long)((unsigned)(aux + 1) & 0xFFFFFu) << 16 |
+                               (unsigned long long)(code & 0xFF) << 8 | (unsigned long long)(label & 0xFF);
+  return ~p;
+}
+
+__host__ __device__ inline ErrInfo err_unpack(unsigned long long key) {
+  const unsigned long long p = ~key;
+  ErrInfo e;
+  e.code = (int)((p >> 8) & 0xFF);
+  e.label = (int)(p & 0xFF);
+  e.where = (int)((p >> 36) & 0xFFFFFFu);
+  e.aux = (int)((p >> 16) & 0xFFFFFu) - 1;
+  return e;
+}
 
 __device__ inline void raise_err(ErrSlot* e, int code, int where, int aux = -1, int label = 0) {
   if (e == nullptr) return;
-  if (atomicCAS(&e->code, 0, code) == 0) {
-    e->where = where;
-    e->aux = aux;
-    e->label = label;
-  }
+  atomicMax(&e->key, err_pack(code, where, aux, label));
 }
 
 __device__ inline float warp_sum(float v) {

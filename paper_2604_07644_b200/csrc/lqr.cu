@@ -76,24 +76,25 @@ int check_errors(Ctx* c, cudaStream_t st, const char* what) {
   GSLS_CUDA_CHECK(cudaMemcpyAsync(h.data(), c->dev.err, sizeof(ErrSlot) * B, cudaMemcpyDeviceToHost, st));
   GSLS_CUDA_CHECK(cudaStreamSynchronize(st));
   for (int i = 0; i < B; ++i) {
-    if (h[i].code == 0) continue;
+    if (h[i].key == 0) continue;
+    const ErrInfo e = err_unpack(h[i].key);
     char msg[256];
-    if (h[i].code == GSLS_ERR_SINGULAR_STAGE) {
-      if (h[i].aux >= 0)
-        snprintf(msg, sizeof msg, "singular %s block at (k=%d, j=%d)", label_text(h[i].label), h[i].where, h[i].aux);
+    if (e.code == GSLS_ERR_SINGULAR_STAGE) {
+      if (e.aux >= 0)
+        snprintf(msg, sizeof msg, "singular %s block at (k=%d, j=%d)", label_text(e.label), e.where, e.aux);
       else
-        snprintf(msg, sizeof msg, "singular %s at stage %d", label_text(h[i].label), h[i].where);
-    } else if (h[i].code == GSLS_ERR_ILL_CONDITIONED) {
+        snprintf(msg, sizeof msg, "singular %s at stage %d", label_text(e.label), e.where);
+    } else if (e.code == GSLS_ERR_ILL_CONDITIONED) {
       snprintf(msg, sizeof msg, "ill-conditioned combine");
-    } else if (h[i].code == GSLS_ERR_NONFINITE) {
+    } else if (e.code == GSLS_ERR_NONFINITE) {
       snprintf(msg, sizeof msg, "non-finite %s at stage %d",
-               h[i].label == GSLS_LABEL_NONFINITE_CON ? "constraints" : "dynamics", h[i].where);
+               e.label == GSLS_LABEL_NONFINITE_CON ? "constraints" : "dynamics", e.where);
     } else {
       snprintf(msg, sizeof msg, "%s failed", what);
     }
-    set_error(h[i].code, i, h[i].where, h[i].aux, h[i].label, msg);
+    set_error(e.code, i, e.where, e.aux, e.label, msg);
     cudaMemsetAsync(c->dev.err, 0, sizeof(ErrSlot) * B, st);
-    return h[i].code;
+    return e.code;
   }
   return GSLS_OK;
 }
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   CTRACE(0);
   const int inst = inst_of(a.list);
   const int4 op = a.ops[blockIdx.x];
-  const int n = a.n, ldg = ldg_of(n), lds = lds_of(n);
+  const int n = a.n, ldg = ldg_of(n), lds = gj_lds(NP, n);  // >= lds_of(n): the inverse's column tiles fit a row
   const size_t MS = (size_t)n * ldg;
   const size_t BS = (size_t)n * lds;
   extern __shared__ float sm[];
@@ -379,7 +380,8 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
 }
 
 size_t combine_smem_bytes(int n) {
-  return (6 * (size_t)n * lds_of(n) + gjl_scratch_words(n <= 64 ? 64 : 80)) * sizeof(float);
+  const int NP = n <= 64 ? 64 : 80;
+  return (6 * (size_t)n * gj_lds(NP, n) + gjl_scratch_words(NP)) * sizeof(float);
 }
 
 int combine_threads(int n) {  // k_cvf_combine: 4*NP row threads + the inverse's panel warp, >= GEMM tiles

@@ -73,6 +73,9 @@ class SqpStats:
     cost: float = np.nan
     scan_layers: int = 0
     admm_converged: bool = True
+    # extension (not in the reference dataclass): one (iterations, converged, rho_changes,
+    # cache_builds) record per inner admm.solve_qp call, for parity checks and profiling
+    qp_calls: list = field(default_factory=list)
 
 
 @dataclass
@@ -143,6 +146,15 @@ class _Sqp:
         self.written = True
         return x, u
 
+    def export_qp(self, x_bar0=None) -> LtvQpData:
+        """Host copy of the QP data held in the device buffers (last linearization)."""
+        nat.check(self.ctx.lib.gsls_ctx_check(self.ctx.handle, stream_ptr()), "linearize")
+        q = self.qp
+        h = lambda t: to_host(t[0])  # noqa: E731
+        return LtvQpData(A=h(q.A), B=h(q.B), b=h(q.b), Q=h(q.Q), R=h(q.R), S=h(q.S), q=h(q.q), r=h(q.r),
+                         QN=h(q.QN), qN=h(q.qN), C=h(q.C), D=h(q.D), f=h(q.f), CN=h(q.CN), fN=h(q.fN),
+                         dx0=h(q.dx0) if x_bar0 is not None else np.zeros(self.dims[0]))
+
     def evaluate(self, traj, tight=None, xbar0=None) -> np.ndarray:
         x, u = to_dev(traj.x, F64)[None], to_dev(traj.u, F64)[None]
         h, hf = _tight_dev(tight)
@@ -184,12 +196,7 @@ def linearize(model, traj: Trajectory, tightenings=None, x_bar0=None, executor=N
     """Stagewise QP data around ``traj`` (sqp.py:105-147), evaluated on the device."""
     ws = _workspace(model, traj.N, executor)
     ws.linearize(traj, tightenings, x_bar0)
-    nat.check(ws.ctx.lib.gsls_ctx_check(ws.ctx.handle, stream_ptr()), "linearize")
-    q = ws.qp
-    h = lambda t: to_host(t[0])  # noqa: E731
-    return LtvQpData(A=h(q.A), B=h(q.B), b=h(q.b), Q=h(q.Q), R=h(q.R), S=h(q.S), q=h(q.q), r=h(q.r),
-                     QN=h(q.QN), qN=h(q.qN), C=h(q.C), D=h(q.D), f=h(q.f), CN=h(q.CN), fN=h(q.fN),
-                     dx0=h(q.dx0) if x_bar0 is not None else np.zeros(model.nx))
+    return ws.export_qp(x_bar0)
 
 
 def solve_nmpc(model, x_bar0, settings: SqpSettings, initial: Trajectory, tightenings=None, executor=None,
@@ -208,14 +215,18 @@ def solve_nmpc(model, x_bar0, settings: SqpSettings, initial: Trajectory, tighte
     lam_s, lam_t = np.zeros((N, c)), np.zeros(nf)
     bad = 0
     scale = 1.0
+    have_qp = False
     for _ in range(settings.max_sqp_iters):
         inner = settings.admm if scale == 1.0 else replace(
             settings.admm, tol_primal=settings.admm.tol_primal * scale, tol_dual=settings.admm.tol_dual * scale)
         ws.linearize(traj, tightenings, x_bar0)
         dx_t, du_t, ast, dstats = ws.admm(inner, ast)
-        its = int(dstats.iterations[0])
+        rec = torch.stack([dstats.iterations, dstats.converged, dstats.rho_changes, dstats.cache_builds]).cpu()
+        its = int(rec[0, 0])
+        stats.qp_calls.append(tuple(int(v) for v in rec[:, 0]))
         stats.admm_iterations += its
-        stats.admm_converged = stats.admm_converged and bool(dstats.converged[0])
+        stats.admm_converged = stats.admm_converged and bool(rec[1, 0])
+        have_qp = True
         stats.scan_layers = scan_depth(N + 1)
         lam_s, lam_t = ast.lam[: N * c].reshape(N, c), ast.lam[N * c:]
         dx, du = to_host(dx_t[0]), to_host(du_t[0])
@@ -254,7 +265,9 @@ def solve_nmpc(model, x_bar0, settings: SqpSettings, initial: Trajectory, tighte
         scale = 1.0
         traj = traj.applied(dx, du, alpha)
     stats.cost = float(ws.evaluate(traj)[0])
-    return NmpcResult(trajectory=traj, lam_stage=lam_s, lam_terminal=lam_t, stats=stats, qp=None)
+    # the last QP, as the reference returns it (sqp.py:268-269; None without an iteration)
+    qp = ws.export_qp(x_bar0) if have_qp else None
+    return NmpcResult(trajectory=traj, lam_stage=lam_s, lam_terminal=lam_t, stats=stats, qp=qp)
 
 
 def rti_step(model, x_bar0, previous: Trajectory | None, settings: SqpSettings, tightenings=None, executor=None,

@@ -179,14 +179,33 @@ def gen_models():
     save("models", **out)
 
 
+def _rti_with_active(model, x, warm, tau, rs):
+    """rti_robust_step with an explicit fresh AdmmState: identical to warm_admm=None
+    (admm.py:164 builds the same fresh state), but the reference mutates it in place,
+    so its final z gives the active set z >= f (f = the tightened offsets)."""
+    nc, nf, N = model.nc, model.nf, warm.N
+    st = admm.AdmmState.fresh(N * nc + nf, rs.sqp.admm.rho0)
+    r = sls.rti_robust_step(model, x, warm, tau, rs, executor=EX, warm_admm=st)
+    qp = sqp.linearize(model, warm, r.tightening, x)
+    f = np.concatenate([qp.f.ravel(), qp.fN])
+    r.stats.rho_changes_ = _rho_changes(st)
+    return r, st.z >= f - 1e-12
+
+
+def _rho_changes(st):
+    return st.generation
+
+
 def _rti_case(model, x0, N, st, rs, steps, tag, out):
     nom = sqp.solve_nmpc(model, x0, st, sqp.initial_guess(model, x0, N, "rollout"), executor=EX)
     warm, tau, u = nom.trajectory.shifted(), None, nom.trajectory.u[0]
     x = np.asarray(x0, float)
     for s in range(steps):
         x = model.step(x, u)
-        r = sls.rti_robust_step(model, x, warm, tau, rs, executor=EX)
+        r, act = _rti_with_active(model, x, warm, tau, rs)
         if s == steps - 1:
+            out[f"{tag}_active"] = act
+            out[f"{tag}_rho_changes"] = np.int64(r.stats.rho_changes_)
             N_ = warm.N
             out.update(traj_dict(warm, f"{tag}_prev_"))
             out[f"{tag}_xbar0"] = x
@@ -212,8 +231,9 @@ def gen_rti():
                                       obstacles=((1.5, 0.0, 0.35),))
     st = sqp.SqpSettings(max_sqp_iters=50, kkt_tol=5e-4,
                          admm=admm.AdmmSettings(rho0=10.0, tol_primal=2e-5, tol_dual=2e-5, max_iter=1500))
+    # max_iter 3000: the golden step terminates on its own residual test (661 iterations)
     st_rti = sqp.SqpSettings(max_sqp_iters=30, kkt_tol=2e-3,
-                             admm=admm.AdmmSettings(rho0=10.0, tol_primal=1e-3, tol_dual=1e-3, max_iter=300))
+                             admm=admm.AdmmSettings(rho0=10.0, tol_primal=1e-3, tol_dual=1e-3, max_iter=3000))
     rs = sls.RobustSettings(sqp=st_rti, weights=sls.SlsWeights(np.diag([20.0, 20, 1, 4, 4, 0.5]), 0.3 * np.eye(2),
                                                                np.diag([20.0, 20, 1, 4, 4, 0.5])), eps=1e-4)
     x0 = np.array([0.4, 0.3, 0, 0, 0, 0])
@@ -222,8 +242,10 @@ def gen_rti():
     warm, tau, u, x = nom.trajectory.shifted(), None, nom.trajectory.u[0], x0
     for s in range(3):
         x = quad_ref.step(x, u)
-        r = sls.rti_robust_step(quad_ref, x, warm, tau, rs, executor=EX)
+        r, act = _rti_with_active(quad_ref, x, warm, tau, rs)
         if s == 2:
+            out["pq_active"] = act
+            out["pq_rho_changes"] = np.int64(r.stats.rho_changes_)
             out.update(traj_dict(warm, "pq_prev_"))
             out["pq_xbar0"] = x
             out["pq_tau_in"] = P.pack_lower(tau.tau, 20, 1, 20, (quad_ref.nc,))
@@ -235,6 +257,7 @@ def gen_rti():
             out["pq_tau_out"] = P.pack_lower(r.tau.tau, 20, 1, 20, (quad_ref.nc,))
             out["pq_tau_term_out"] = r.tau.tau_term
             out["pq_admm_iters"] = np.int64(r.stats.admm_iterations)
+            out["pq_converged"] = np.bool_(r.stats.converged)
             print("pq admm iters", r.stats.admm_iterations, r.stats.converged)
         warm, tau, u = r.warm_start, r.tau, r.u0
 
@@ -305,7 +328,219 @@ def gen_rollout():
     save("rollout", **out)
 
 
+def _batch_worker(args):
+    """One reference rti_robust_step of scenario `idx` of the cfg-D / E-RTI workload."""
+    tag, idx = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from paper_2604_07644_b200 import scenarios as S
+    wl = S.rti_workload(tag)
+    m = wl.model
+    st = sqp.SqpSettings(admm=admm.AdmmSettings(**S.ADMM), **S.SQP)
+    rs = sls.RobustSettings(sqp=st, eps=S.EPS,
+                            weights=sls.SlsWeights(np.eye(m.nx), S.RBAR * np.eye(m.nu), np.eye(m.nx)))
+    tau = sls.SlsDuals.zero(wl.N, m.nc, m.nf, S.EPS)
+    tau.tau = [np.array(t) for t in wl.tau]
+    tau.tau_term = np.array(wl.tau_term)
+    x = wl.scenario_states(idx, 1)[0]
+    prev = sqp.Trajectory(wl.prev_x, wl.prev_u, m.dt)
+    r, act = _rti_with_active(m, x, prev, tau, rs)
+    return dict(x=x, iters=r.stats.admm_iterations, converged=r.stats.converged, active=act,
+                rho_changes=r.stats.rho_changes_, u0=r.u0, h=r.tightening.h, hf=r.tightening.hf,
+                lam=np.concatenate([r.lam_stage.ravel(), r.lam_terminal]), plan_x=r.plan.x, plan_u=r.plan.u,
+                tau=P.pack_lower(r.tau.tau, wl.N, 1, wl.N, (m.nc,)), tau_term=r.tau.tau_term)
+
+
+def gen_batch():
+    """The benched cfg-D batch (and E-RTI) through the REAL reference, per instance:
+    scenarios 0..63 of q61 and 0..15 of h75 (paper_2604_07644_b200.scenarios)."""
+    import multiprocessing as mp
+    out = {}
+    with mp.get_context("spawn").Pool(os.cpu_count()) as pool:
+        for tag, count in (("q61", 64), ("h75", 16)):
+            res = pool.map(_batch_worker, [(tag, i) for i in range(count)])
+            for k in res[0]:
+                arr = np.array([r[k] for r in res])
+                if arr.dtype == np.float64 and k in ("plan_x", "plan_u", "tau", "lam"):
+                    arr = arr.astype(np.float32)   # 1e-4 checks; keeps the fixture small
+                out[f"{tag}_{k}"] = arr
+            its = out[f"{tag}_iters"]
+            print(tag, "iterations", its.min(), its.max(), its.mean(), "converged", out[f"{tag}_converged"].all())
+    save("batch", **out)
+
+
+class _QpRecorder:
+    """Records every admm.solve_qp the reference makes (iterations, convergence, rho changes)."""
+
+    def __init__(self):
+        self.calls = []
+        self._orig = admm.solve_qp
+
+    def __enter__(self):
+        def wrap(*a, **k):
+            r = self._orig(*a, **k)
+            self.calls.append((r.stats.iterations, int(r.stats.converged), r.stats.rho_changes, r.stats.cache_builds))
+            return r
+        sqp.admm.solve_qp = wrap
+        return self
+
+    def __exit__(self, *exc):
+        sqp.admm.solve_qp = self._orig
+
+
+def gen_cfgb():
+    """BASELINE cfg-B: sqp.solve_nmpc of the 12D quadrotor, N=100, 5 obstacles (sqp.py:190-269)."""
+    from paper_2604_07644_b200 import scenarios as S
+    m = S.cfgb_model()
+    N = S.CFGB["N"]
+    x0 = S.quad12_start()
+    xg, ug = S.hover_guess(m, x0, N)
+    st = sqp.SqpSettings(admm=admm.AdmmSettings(**S.CFGB["admm"]), **S.CFGB["sqp"])
+    with _QpRecorder() as rec:
+        r = sqp.solve_nmpc(m, x0, st, sqp.Trajectory(xg, ug, m.dt), executor=EX)
+    print("cfgB", r.stats, "qp calls", len(rec.calls))
+    save("cfgb", x=r.trajectory.x, u=r.trajectory.u, lam_s=r.lam_stage, lam_t=r.lam_terminal,
+         sqp_iters=np.int64(r.stats.iterations), converged=np.bool_(r.stats.converged),
+         residual=np.float64(r.stats.residual), admm_iters=np.int64(r.stats.admm_iterations),
+         cost=np.float64(r.stats.cost), qp_calls=np.array(rec.calls), qp_f=r.qp.f, qp_A0=r.qp.A[0])
+
+
+def gen_cfgc():
+    """BASELINE cfg-C: sls.solve_robust on the 12D quadrotor (sls.py:400-469), N=50."""
+    from paper_2604_07644_b200 import scenarios as S
+    m = S.cfgc_model()
+    N = S.CFGC["N"]
+    x0 = S.quad12_start()
+    xg, ug = S.hover_guess(m, x0, N)
+    st = sqp.SqpSettings(admm=admm.AdmmSettings(**S.CFGC["admm"]), **S.CFGC["sqp"])
+    rs = sls.RobustSettings(sqp=st, weights=sls.SlsWeights.identity(m.nx, m.nu), eps=S.CFGC["eps"],
+                            tol_h=S.CFGC["tol_h"], max_alternations=S.CFGC["max_alternations"])
+    with _QpRecorder() as rec:
+        r = sls.solve_robust(m, x0, rs, initial=sqp.Trajectory(xg, ug, m.dt), executor=EX)
+    print("cfgC", r.stats, "qp calls", len(rec.calls))
+    save("cfgc", x=r.trajectory.x, u=r.trajectory.u, h=r.tightening.h, hf=r.tightening.hf,
+         lam_s=r.lam_stage, lam_t=r.lam_terminal, alternations=np.int64(r.stats.alternations),
+         converged=np.bool_(r.stats.converged), dh=np.float64(r.stats.dh),
+         sqp_iters=np.int64(r.stats.sqp_iterations), qp_calls=np.array(rec.calls),
+         tau=P.pack_lower(r.duals.tau, N, 1, N, (m.nc,)), tau_term=r.duals.tau_term,
+         **pack_resp(r.response, N, m.nx, m.nu, "resp_"))
+
+
+def gen_cfge():
+    """BASELINE cfg-E: admm.solve_qp of the 75D/19u humanoid linearized over N=2047
+    (192,493 variables, 81,882 constraints; admm.py:153-203)."""
+    from paper_2604_07644_b200 import scenarios as S
+    m = S.cfge_model()
+    N = S.CFGE["N"]
+    x, u = S.cfge_trajectory(m, N)
+    qp = sqp.linearize(m, sqp.Trajectory(x, u, m.dt), None, S.cfge_start(m))
+    st = admm.AdmmSettings(**S.CFGE["admm"])
+    stt = admm.AdmmState.fresh(N * qp.nc + qp.nf, st.rho0)
+    import time
+    t = time.perf_counter()
+    r = admm.solve_qp(qp, st, warm_start=stt, executor=EX)
+    print("cfgE", r.stats, "%.1f s" % (time.perf_counter() - t))
+    f = np.concatenate([qp.f.ravel(), qp.fN])
+    act = r.state.z >= f - 1e-12
+    save("cfge", iters=np.int64(r.stats.iterations), converged=np.bool_(r.stats.converged),
+         rho_changes=np.int64(r.stats.rho_changes), builds=np.int64(r.stats.cache_builds),
+         active=np.packbits(act), n_active=np.int64(act.sum()), dx=r.dx.astype(np.float32),
+         du=r.du.astype(np.float32), lam=r.state.lam.astype(np.float32),
+         checksum=np.float64(sum(float(np.abs(getattr(qp, k)).sum()) for k in FIELDS)))
+
+
+def _nominal_worker(args):
+    tag, idx = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from paper_2604_07644_b200 import scenarios as S
+    wl = S.rti_workload(tag)
+    m = wl.model
+    st = sqp.SqpSettings(admm=admm.AdmmSettings(**S.ADMM), **S.SQP)
+    x = wl.scenario_states(idx, 1)[0]
+    prev = sqp.Trajectory(wl.prev_x, wl.prev_u, m.dt)
+    ast = admm.AdmmState.fresh(wl.N * m.nc + m.nf, st.admm.rho0)
+    r = sqp.rti_step(m, x, prev, st, executor=EX, warm_admm=ast)
+    qp = sqp.linearize(m, prev, None, x)
+    f = np.concatenate([qp.f.ravel(), qp.fN])
+    return dict(iters=r.stats.admm_iterations, converged=r.stats.converged, active=ast.z >= f - 1e-12,
+                rho_changes=ast.generation, u0=r.u0, plan_x=r.plan.x, plan_u=r.plan.u, warm_x=r.warm_start.x,
+                lam=np.concatenate([r.lam_stage.ravel(), r.lam_terminal]), cost=r.stats.cost)
+
+
+def gen_nominal():
+    """Nominal sqp.rti_step (sqp.py:272-302) on the cfg-D workload, scenarios 0..7."""
+    import multiprocessing as mp
+    out = {}
+    with mp.get_context("spawn").Pool(os.cpu_count()) as pool:
+        res = pool.map(_nominal_worker, [("q61", i) for i in range(8)])
+    for k in res[0]:
+        out[f"q61_{k}"] = np.array([r[k] for r in res])
+    print("nominal q61 iterations", out["q61_iters"])
+    save("nominal", **out)
+
+
+def gen_errors():
+    """Error paths of the reference (exception class + message) and the ridge branch."""
+    out = {}
+    # spd_inverse ridge branch (lqr.py:198-216): input 0 is decoupled (B[:, :, 0] = 0, S[:, 0] = 0) and
+    # R[3][0, 0] = 1e-12, so the stage-3 Cholesky pivot^2 < 1e-10 and the block is refactored
+    # with the 1e-9 ridge instead of raising
+    qp = P.random_ltv_qp(np.random.default_rng(21), 4, 2, 12)
+    B = qp.B.copy(); B[:, :, 0] = 0.0
+    S = qp.S.copy(); S[:, 0, :] = 0.0
+    R = qp.R.copy(); R[3] = np.diag([1e-12, 1.0])
+    qp = qp.replace(B=B, S=S, R=R)
+    sol = lqr.solve(ref_qp(qp), executor=EX)
+    out.update({f"ridge_{k}": v for k, v in qp_dict(qp).items()})
+    out.update(ridge_dx=sol.dx, ridge_du=sol.du, ridge_K=sol.K, ridge_k=sol.k)
+    # a singular R at stage 5 and 8: the reference names stage 5 (lqr.py:204-215)
+    qp2 = P.random_ltv_qp(np.random.default_rng(22), 4, 2, 12)
+    R2 = qp2.R.copy(); R2[5] = -np.eye(2); R2[8] = -np.eye(2)
+    qp2 = qp2.replace(R=R2)
+    try:
+        lqr.solve(ref_qp(qp2), executor=EX)
+        raise SystemExit("expected SingularStageError")
+    except lqr.SingularStageError as e:
+        out["singR_msg"] = np.array(str(e))
+    out.update({f"singR_{k}": v for k, v in qp_dict(qp2).items()})
+    # SLS input-cost block singular at (k=3, j=1) only: Rbar = -0.5 I, and tau weights the
+    # D rows of every other valid cell (D' tau D >= 2 I there); _locate_singular names the
+    # first failing (k, j) in row-major order (sls.py:258-261, :321-326)
+    rng = np.random.default_rng(23)
+    N, nx, nu, c = 6, 3, 2, 2
+    A = np.tile(np.eye(nx), (N, 1, 1)) + 0.05 * rng.standard_normal((N, nx, nx))
+    Bm = rng.standard_normal((N, nx, nu))
+    E = 0.1 * np.tile(np.eye(nx), (N, 1, 1))
+    C = rng.standard_normal((N, c, nx))
+    D = np.tile(np.eye(nu), (N, 1, 1))
+    CN = rng.standard_normal((1, nx))
+    du = sls.SlsDuals.zero(N, c, 1, 1e-8)
+    for j in range(N):
+        for k in range(j + 1, N):
+            du.tau[j][k - j - 1] = 0.0 if (k, j) in ((3, 1), (4, 2)) else 3.0
+    costs = sls.assemble_costs(du, C, D, CN, sls.SlsWeights(np.eye(nx), -0.5 * np.eye(nu), np.eye(nx)))
+    try:
+        sls.synthesize(A, Bm, E, costs, executor=EX)
+        raise SystemExit("expected SingularStageError")
+    except lqr.SingularStageError as e:
+        out["singQu_msg"] = np.array(str(e))
+    out.update(singQu_A=A, singQu_B=Bm, singQu_E=E, singQu_C=C, singQu_D=D, singQu_CN=CN,
+               singQu_tau=P.pack_lower(du.tau, N, 1, N, (c,)))
+    # non-finite dynamics: x[5] = nan -> the reference names stage 5 (sqp.py:125-126)
+    m = models.DubinsCar(obstacles=((1.0, 0.5, 0.3),))
+    x = np.zeros((9, 3)); x[:, 0] = np.linspace(0, 1, 9); x[5, 2] = np.nan
+    try:
+        sqp.linearize(m, sqp.Trajectory(x, np.zeros((8, 1)), m.dt))
+        raise SystemExit("expected ArithmeticError")
+    except ArithmeticError as e:
+        out["nonfinite_msg"] = np.array(str(e))
+    out["nonfinite_x"] = x
+    for k in ("singR_msg", "singQu_msg", "nonfinite_msg"):
+        print(k, out[k])
+    save("errors", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["scan", "lqr", "admm", "sls", "models", "rti", "rollout"]
+    which = sys.argv[1:] or ["scan", "lqr", "admm", "sls", "models", "rti", "rollout", "batch", "cfgb", "cfgc",
+                             "cfge", "errors", "nominal"]
     for w in which:
         globals()["gen_" + w]()

@@ -227,7 +227,7 @@ def rti_case(tag):
     if tag == "pq":
         model = M.PlanarQuadrotor(dt=0.05, thrust_max=30.0, goal=(2.6, 0, 0, 0, 0, 0), obstacles=((1.5, 0.0, 0.35),))
         st = osqp.Settings(max_sqp_iters=30, kkt_tol=2e-3,
-                           admm=oadmm.Settings(rho0=10.0, tol_primal=1e-3, tol_dual=1e-3, max_iter=300))
+                           admm=oadmm.Settings(rho0=10.0, tol_primal=1e-3, tol_dual=1e-3, max_iter=3000))
         Q = np.diag([20.0, 20, 1, 4, 4, 0.5])
         rs = osls.RobustSettings(sqp=st, weights=osls.Weights(Q, 0.3 * np.eye(2), Q), eps=1e-4)
     else:
@@ -308,3 +308,128 @@ def test_rollout_sampler_errors():
         orl.sample_disturbance("gaussian", 3, 4, 0)
     with pytest.raises(ValueError, match="rows must be"):
         orl.sample_disturbance("adversarial", 3, 4, 0, rows=np.ones((3, 3)))
+
+
+# --- benched batch, nominal RTI, configs B / C / E, error paths (make_golden.py) -------------
+
+def _oracle_rti(tag, idx, robust=True):
+    from paper_2604_07644_b200 import scenarios as S
+    import bench
+    wl = S.rti_workload(tag)
+    m = wl.model
+    rs = bench.oracle_settings(m)
+    x = wl.scenario_states(idx, 1)[0]
+    prev = osqp.Trajectory(wl.prev_x, wl.prev_u, m.dt)
+    st = oadmm.State.fresh(wl.N * m.nc + m.nf, rs.sqp.admm.rho0)
+    if robust:
+        tau = osls.Duals.zero(wl.N, m.nc, m.nf, rs.eps)
+        tau.tau, tau.tau_term = wl.tau, wl.tau_term
+        r = osls.rti_robust_step(m, x, prev, tau, rs, warm_admm=st)
+        qp = osqp.linearize(m, prev, r.tightening, x)
+    else:
+        r = osqp.rti_step(m, x, prev, rs.sqp, warm_admm=st)
+        qp = osqp.linearize(m, prev, None, x)
+    f = np.concatenate([qp.f.ravel(), qp.fN])
+    return r, st, st.z >= f - 1e-12
+
+
+@pytest.mark.parametrize("tag,idx", [("q61", 0), ("q61", 5), ("q61", 37), ("h75", 9)])
+def test_batch_golden(tag, idx):
+    """The oracle reproduces the reference on benched scenarios (bench.py's CPU arms)."""
+    g = load_golden("batch")
+    r, st, act = _oracle_rti(tag, idx)
+    assert r.stats.admm_iterations == g[f"{tag}_iters"][idx]
+    assert st.generation == g[f"{tag}_rho_changes"][idx]
+    assert (act == g[f"{tag}_active"][idx]).all()
+    assert rel(r.u0, g[f"{tag}_u0"][idx]) <= 1e-7
+    assert rel(r.tightening.h, g[f"{tag}_h"][idx]) <= 1e-7
+
+
+def test_nominal_golden():
+    g = load_golden("nominal")
+    r, st, act = _oracle_rti("q61", 2, robust=False)
+    assert r.stats.admm_iterations == g["q61_iters"][2]
+    assert (act == g["q61_active"][2]).all()
+    assert rel(r.u0, g["q61_u0"][2]) <= 1e-7 and rel(r.plan.x, g["q61_plan_x"][2]) <= 1e-7
+
+
+def _qp_counter(monkeypatch):
+    calls = []
+    orig = oadmm.solve_qp
+
+    def wrap(*a, **k):
+        r = orig(*a, **k)
+        calls.append((r.stats.iterations, int(r.stats.converged), r.stats.rho_changes, r.stats.cache_builds))
+        return r
+    monkeypatch.setattr(osqp.admm, "solve_qp", wrap)
+    return calls
+
+
+def test_cfgb_golden(monkeypatch):
+    from paper_2604_07644_b200 import scenarios as S
+    g = load_golden("cfgb")
+    calls = _qp_counter(monkeypatch)
+    m = S.cfgb_model()
+    x0 = S.quad12_start()
+    xg, ug = S.hover_guess(m, x0, S.CFGB["N"])
+    st = osqp.Settings(admm=oadmm.Settings(**S.CFGB["admm"]), **S.CFGB["sqp"])
+    r = osqp.solve_nmpc(m, x0, st, osqp.Trajectory(xg, ug, m.dt))
+    assert (np.array(calls) == g["qp_calls"]).all()
+    assert r.stats.iterations == int(g["sqp_iters"]) and r.stats.converged
+    assert rel(r.trajectory.x, g["x"]) <= 1e-7 and rel(r.lam_stage, g["lam_s"]) <= 1e-6
+
+
+def test_cfgc_golden():
+    """Pins the oracle's solve_robust (sls.py:400-469) against the real reference."""
+    from paper_2604_07644_b200 import scenarios as S
+    g = load_golden("cfgc")
+    m = S.cfgc_model()
+    x0 = S.quad12_start()
+    N = S.CFGC["N"]
+    xg, ug = S.hover_guess(m, x0, N)
+    st = osqp.Settings(admm=oadmm.Settings(**S.CFGC["admm"]), **S.CFGC["sqp"])
+    rs = osls.RobustSettings(sqp=st, weights=osls.Weights.identity(m.nx, m.nu), eps=S.CFGC["eps"],
+                             tol_h=S.CFGC["tol_h"], max_alternations=S.CFGC["max_alternations"])
+    r = osls.solve_robust(m, x0, rs, initial=osqp.Trajectory(xg, ug, m.dt))
+    assert r.stats.alternations == int(g["alternations"]) and r.stats.converged == bool(g["converged"])
+    assert r.stats.sqp_iterations == int(g["sqp_iters"])
+    assert rel(r.trajectory.x, g["x"]) <= 1e-6 and rel(r.tightening.h, g["h"]) <= 1e-6
+    assert rel(P.pack_lower(r.duals.tau, N, 1, N, (m.nc,)), g["tau"]) <= 1e-6
+
+
+def test_cfge_golden():
+    from paper_2604_07644_b200 import scenarios as S
+    g = load_golden("cfge")
+    m = S.cfge_model()
+    N = S.CFGE["N"]
+    x, u = S.cfge_trajectory(m, N)
+    qp = osqp.linearize(m, osqp.Trajectory(x, u, m.dt), None, S.cfge_start(m))
+    assert sum(float(np.abs(getattr(qp, k)).sum()) for k in olqr.FIELDS) == pytest.approx(float(g["checksum"]),
+                                                                                          rel=1e-12)
+    res = oadmm.solve_qp(qp, oadmm.Settings(**S.CFGE["admm"]))
+    assert res.stats.iterations == int(g["iters"]) and res.stats.rho_changes == int(g["rho_changes"])
+    f = oadmm.offsets(qp)
+    act = res.state.z >= f - 1e-12
+    assert (act == np.unpackbits(g["active"])[: f.size].astype(bool)).all()
+    assert rel(res.dx, g["dx"].astype(float)) <= 1e-6
+
+
+def test_error_goldens():
+    g = load_golden("errors")
+    qp = olqr.QP(**{k: g[f"ridge_qp_{k}"] for k in olqr.FIELDS})
+    sol = olqr.solve(qp)
+    assert rel(sol.dx, g["ridge_dx"]) <= 1e-8 and rel(sol.K, g["ridge_K"]) <= 1e-8
+    with pytest.raises(olqr.SingularStageError, match="^" + str(g["singR_msg"]) + "$"):
+        olqr.solve(olqr.QP(**{k: g[f"singR_qp_{k}"] for k in olqr.FIELDS}))
+    N, c = g["singQu_A"].shape[0], g["singQu_C"].shape[1]
+    nx, nu = g["singQu_A"].shape[-1], g["singQu_D"].shape[-1]
+    du = osls.Duals.zero(N, c, 1, 1e-8)
+    du.tau = P.unpack_lower(g["singQu_tau"], N, 1, N)
+    costs = osls.assemble_costs(du, g["singQu_C"], g["singQu_D"], g["singQu_CN"],
+                                osls.Weights(np.eye(nx), -0.5 * np.eye(nu), np.eye(nx)))
+    with pytest.raises(olqr.SingularStageError, match=r"^singular Qu block at \(k=3, j=1\)$"):
+        osls.synthesize(g["singQu_A"], g["singQu_B"], g["singQu_E"], costs)
+    m = M.DubinsCar(obstacles=((1.0, 0.5, 0.3),))
+    x = g["nonfinite_x"]
+    with pytest.raises(ArithmeticError, match="^" + str(g["nonfinite_msg"]) + "$"):
+        osqp.linearize(m, osqp.Trajectory(x, np.zeros((x.shape[0] - 1, 1)), m.dt))
