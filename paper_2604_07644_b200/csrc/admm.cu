@@ -31,7 +31,7 @@ int check_errors(Ctx* c, cudaStream_t st, const char* what);
 void set_error(int code, int inst, int where, int aux, int label, const char* msg);
 
 enum { MODE_LQR = 0, MODE_ADMM = 1 };
-enum { ST_DONE = 0, ST_REBUILD = 1 };
+enum { ST_DONE = 0, ST_REBUILD = 1, ST_CONTINUE = 2 };  // per-instance exit status of a replay launch
 
 struct ReplayArgs {
   DevLqr L;
@@ -49,6 +49,7 @@ struct ReplayArgs {
   int max_layer;  // max ops in any scan layer (t1/t2 sizing)
   unsigned long long* trace;  // GSLS_REPLAY_TRACE: phase timestamps of the first iteration (rank 0)
   int prefetch;               // k_replay: bulk-prefetch the next tree layer's records into L2
+  int cap;                    // ADMM: pause (ST_CONTINUE) an undecided instance at this iteration (0: none)
 };
 
 constexpr int kReplayThreads = 512;
@@ -851,6 +852,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
         }
         if (it >= a.set.max_iter) flag = 1;
         else if (changed) flag = 2;
+        else if (a.cap > 0 && it >= a.cap) flag = 3;  // paused: resumes bitwise-identically in the next launch
       }
       if (lead) a.stats.iterations[inst] = it;
       s_flag = flag;
@@ -892,7 +894,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
           L.last_k[(size_t)inst * N * m + e] = kf[e];
         }
       }
-      if (rank == 0 && tid == 0) a.status[inst] = (flag == 2) ? ST_REBUILD : ST_DONE;
+      if (rank == 0 && tid == 0) a.status[inst] = (flag == 2) ? ST_REBUILD : (flag == 3) ? ST_CONTINUE : ST_DONE;
     }
     cl.sync();
     TR();
@@ -1427,6 +1429,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
         }
         if (it >= a.set.max_iter) flag = 1;
         else if (changed) flag = 2;
+        else if (a.cap > 0 && it >= a.cap) flag = 3;  // paused: resumes bitwise-identically in the next launch
       }
       if (lead) a.stats.iterations[inst] = it;
       s_flag = flag;
@@ -1471,7 +1474,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
         L.last_k[(size_t)inst * N * m + e] = kf[e];
       }
     }
-    if (rank == 0 && tid == 0) a.status[inst] = (flag == 2) ? ST_REBUILD : ST_DONE;
+    if (rank == 0 && tid == 0) a.status[inst] = (flag == 2) ? ST_REBUILD : (flag == 3) ? ST_CONTINUE : ST_DONE;
     cl.sync();
     return;
   }
@@ -1733,18 +1736,34 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
   GSLS_CUDA_CHECK(cudaMemsetAsync(stats->iterations, 0, sizeof(int32_t) * B, st));
   GSLS_CUDA_CHECK(cudaMemsetAsync(stats->converged, 0, sizeof(int32_t) * B, st));
   GSLS_CUDA_CHECK(cudaMemsetAsync(stats->rho_changes, 0, sizeof(int32_t) * B, st));
-  std::vector<int> builds(B, 0), list(B), status(B);
+  std::vector<int> builds(B, 0), list(B), status(B), rebuild;
   for (int i = 0; i < B; ++i) list[i] = i;
+  rebuild = list;
   c->cache_valid = false;  // the ADMM rebuilds the cache at augmented costs
   bool prebuilt = c->admm_prebuilt;  // first build already issued by admm_build (possibly on another stream)
   c->admm_prebuilt = false;
-  while (!list.empty()) {
-    const int cnt = (int)list.size();
-    GSLS_CUDA_CHECK(cudaMemcpyAsync(c->d_inst_list, list.data(), sizeof(int) * cnt, cudaMemcpyHostToDevice, st));
-    int rc = prebuilt ? GSLS_OK : build_cache(c, qp, state->rho, c->d_inst_list, cnt, st);
-    prebuilt = false;
-    if (rc) return rc;
-    for (int i : list) builds[i]++;
+  // Large batches: every launch pauses the undecided instances at the next rho decision
+  // point (iteration sigma, 2 sigma, ...), so the instances that commit a rho change there
+  // are rebuilt as one batched wave instead of waiting behind instances that iterate on
+  // without one (up to max_iter); paused instances resume, bitwise identically, in the next
+  // launch together with the rebuilt ones.  Once few instances remain (<= 2 per SM) the
+  // last launches run uncapped.
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const char* capenv = getenv("GSLS_ADMM_FIRST_CAP");
+  int cap = (B > sms) ? s->sigma : 0;
+  if (capenv) cap = atoi(capenv);
+  const bool verbose = getenv("GSLS_ADMM_VERBOSE") != nullptr;  // per-wave timing (diagnostics)
+  cudaEvent_t ev[3] = {};
+  if (verbose) for (auto& e : ev) cudaEventCreate(&e);
+  int wave = 0;
+  auto replay_wave = [&](const std::vector<int>& ids, int* dlist, cudaStream_t sx) -> int {
+    if (ids.empty()) return GSLS_OK;
+    GSLS_CUDA_CHECK(cudaMemcpyAsync(dlist, ids.data(), sizeof(int) * ids.size(), cudaMemcpyHostToDevice, sx));
     ReplayArgs a{};
     a.qp = *qp;
     a.mode = MODE_ADMM;
@@ -1753,22 +1772,74 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
     a.stats = *stats;
     a.status = c->d_status;
     a.dx = dx; a.du = du;
-    a.list = c->d_inst_list;
+    a.list = dlist;
+    a.cap = cap;
     const char* sg = getenv("GSLS_REPLAY_STAGED");
-    rc = (sg && sg[0] == '0') ? GSLS_ERR_TOO_LARGE : launch_admm_staged(c, a, cnt, st);
-    if (rc == GSLS_ERR_TOO_LARGE) rc = launch_replay(c, a, cnt, st);
+    int rc = (sg && sg[0] == '0') ? GSLS_ERR_TOO_LARGE : launch_admm_staged(c, a, (int)ids.size(), sx);
+    if (rc == GSLS_ERR_TOO_LARGE) rc = launch_replay(c, a, (int)ids.size(), sx);
+    return rc;
+  };
+  while (!list.empty()) {
+    const int cnt = (int)list.size(), nreb = (int)rebuild.size();
+    if (verbose) cudaEventRecord(ev[0], st);
+    int rc = GSLS_OK;
+    if (prebuilt) {  // the first build already ran (admm_build): one launch over every instance
+      for (int i : rebuild) builds[i]++;
+      prebuilt = false;
+      rc = replay_wave(list, c->d_inst_list, st);
+    } else if (nreb == cnt) {  // every live instance needs its (first or re-) build
+      GSLS_CUDA_CHECK(cudaMemcpyAsync(c->d_build_list, rebuild.data(), sizeof(int) * nreb, cudaMemcpyHostToDevice, st));
+      if ((rc = build_cache(c, qp, state->rho, c->d_build_list, nreb, st))) return rc;
+      for (int i : rebuild) builds[i]++;
+      rc = replay_wave(list, c->d_inst_list, st);
+    } else {
+      // instances that committed a rho change are rebuilt and replayed on the side stream
+      // while the others continue on the main stream (disjoint instances and cache slices)
+      std::vector<int> cont;
+      for (int i : list)
+        if (std::find(rebuild.begin(), rebuild.end(), i) == rebuild.end()) cont.push_back(i);
+      if (nreb > 0) {
+        if (!c->side) {
+          GSLS_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+          GSLS_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+          GSLS_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        }
+        GSLS_CUDA_CHECK(cudaEventRecord(c->ev_fork, st));
+        GSLS_CUDA_CHECK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+        GSLS_CUDA_CHECK(cudaMemcpyAsync(c->d_build_list, rebuild.data(), sizeof(int) * nreb, cudaMemcpyHostToDevice,
+                                        c->side));
+        if ((rc = build_cache(c, qp, state->rho, c->d_build_list, nreb, c->side))) return rc;
+        for (int i : rebuild) builds[i]++;
+        if ((rc = replay_wave(rebuild, c->d_build_list, c->side))) return rc;
+        GSLS_CUDA_CHECK(cudaEventRecord(c->ev_join, c->side));
+      }
+      rc = replay_wave(cont, c->d_inst_list, st);
+      if (nreb > 0) GSLS_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_join, 0));
+    }
     if (rc) return rc;
+    if (verbose) cudaEventRecord(ev[1], st);
     rc = check_errors(c, st, "admm");  // synchronizes
     if (rc) return rc;
     GSLS_CUDA_CHECK(cudaMemcpyAsync(status.data(), c->d_status, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
     GSLS_CUDA_CHECK(cudaStreamSynchronize(st));
-    std::vector<int> next;
-    for (int i : list)
-      if (status[i] == ST_REBUILD) next.push_back(i);
+    if (verbose) {
+      float tw = 0.f;
+      cudaEventElapsedTime(&tw, ev[0], ev[1]);
+      fprintf(stderr, "admm wave %d: %d instances (%d rebuilt, cap %d): %.3f ms\n", wave, cnt, nreb, cap, tw);
+    }
+    ++wave;
+    std::vector<int> next, nrb;
+    for (int i : list) {
+      if (status[i] == ST_REBUILD) { next.push_back(i); nrb.push_back(i); }
+      else if (status[i] == ST_CONTINUE) next.push_back(i);
+    }
     list.swap(next);
+    rebuild.swap(nrb);
+    cap = (cap > 0 && !capenv) ? cap + s->sigma : 0;
   }
   GSLS_CUDA_CHECK(cudaMemcpyAsync(stats->cache_builds, builds.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice, st));
   GSLS_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (verbose) for (auto& e : ev) cudaEventDestroy(e);
   return GSLS_OK;
 }
 

@@ -69,7 +69,10 @@ struct Ctx {
   int64_t bytes = 0;
   DevLqr dev{};
   int* d_inst_all = nullptr;   // 0..batch-1
-  int* d_inst_list = nullptr;  // scratch list (batch)
+  int* d_inst_list = nullptr;  // scratch list (batch): instances of a replay launch
+  int* d_build_list = nullptr; // scratch list (batch): instances of a cache rebuild
+  cudaStream_t side = nullptr;  // ADMM driver: rebuild + replay of the rebuilt instances, beside the others
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int32_t* d_status = nullptr; // [batch] per-instance ADMM exit status
   double* d_scratch = nullptr; // global fallback for replay vectors
   size_t scratch_floats = 0;   // per instance (doubles)

@@ -808,12 +808,13 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
   L.ZD = (float*)dev_alloc(c, std::max<size_t>(1, B * N * (n + m) * L.ldc) * 4);
   c->d_inst_all = (int*)dev_alloc(c, B * sizeof(int));
   c->d_inst_list = (int*)dev_alloc(c, B * sizeof(int));
+  c->d_build_list = (int*)dev_alloc(c, B * sizeof(int));
   c->d_status = (int32_t*)dev_alloc(c, B * sizeof(int32_t));
   c->scratch_floats = replay_smem_floats(c);  // doubles
   if (c->scratch_floats * 8 > kReplaySmemMax) c->d_scratch = (double*)dev_alloc(c, B * c->scratch_floats * 8);
   bool fail = !L.Ps || !L.As || !L.Cs || !L.ATs || !L.cotAT || !L.cvf_rec || !L.cotA || !L.cot_rec || !L.Rhat || !L.Shat || !L.Shat64 || !L.Rinv ||
               !L.Gamma || !L.K || !L.cvec || !L.v0 || !L.last_k || !L.last_p || !L.err || !L.X23 || !L.pb0 || !L.XK || !L.kk0 ||
-              !L.Bcm || !L.ZD || !c->d_inst_all || !c->d_inst_list || !c->d_status ||
+              !L.Bcm || !L.ZD || !c->d_inst_all || !c->d_inst_list || !c->d_build_list || !c->d_status ||
               (c->scratch_floats * 8 > kReplaySmemMax && !c->d_scratch);
   if (fail) {
     for (void* p : c->allocs) cudaFree(p);
@@ -831,6 +832,9 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
 
 void ctx_destroy(Ctx* c) {
   if (!c) return;
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->sls) sls_destroy(c);
   for (void* p : c->allocs) cudaFree(p);
   delete c;

@@ -58,7 +58,8 @@ def test_cfgb_solve_nmpc_quadrotor12(mods):
     # inner ADMM counts: exact, except that a QP whose primal residual creeps across the
     # 1e-3 tolerance (relative margin < 2e-4 at the exit) may exit one iteration apart.
     # The float64 reference itself flips there: re-solving QP call 3 from its own warm
-    # state with the trajectory perturbed by 1e-7 gives 516 instead of 517
+    # state with the trajectory perturbed by 1e-6 gives 516 instead of 517 (the device
+    # trajectories carry about 5e-7 of float32 error)
     # (tools/probe/chain_sensitivity.py midchain, profiles/r02/chain_sensitivity.txt).
     d = np.abs(calls[:, 0] - ref[:, 0])
     assert d.max() <= 1 and (d > 0).sum() <= 2, (calls[:, 0].tolist(), ref[:, 0].tolist())
