@@ -30,7 +30,9 @@ typedef enum {
   GSLS_ERR_CACHE_INVALIDATED = 5, /* lqr.CacheInvalidatedError (lqr.py:39, :426-427)        */
   GSLS_ERR_NONFINITE = 6,         /* ArithmeticError non-finite dynamics (sqp.py:125-131)   */
   GSLS_ERR_TOO_LARGE = 7,         /* dimensions beyond the compiled limits                  */
-  GSLS_ERR_NO_DEVICE = 8
+  GSLS_ERR_NO_DEVICE = 8,
+  GSLS_ERR_LOWRANK = 9            /* internal: a factored combine met an indefinite P (never
+                                     returned; the scan is re-run with dense combines)     */
 } gsls_status_t;
 
 /* labels carried with GSLS_ERR_SINGULAR_STAGE (error.aux2) */

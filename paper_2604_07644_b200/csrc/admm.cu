@@ -31,7 +31,7 @@ int check_errors(Ctx* c, cudaStream_t st, const char* what);
 void set_error(int code, int inst, int where, int aux, int label, const char* msg);
 
 enum { MODE_LQR = 0, MODE_ADMM = 1 };
-enum { ST_DONE = 0, ST_REBUILD = 1, ST_CONTINUE = 2 };  // per-instance exit status of a replay launch
+enum { ST_DONE = 0, ST_REBUILD = 1, ST_CONTINUE = 2, ST_BUILD_ERR = 3 };  // per-instance exit status of a replay launch
 
 struct ReplayArgs {
   DevLqr L;
@@ -436,6 +436,10 @@ __device__ inline void gdotc(int cs, int total, int len, int gt, int gs, Term te
 __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
   const DevLqr& L = a.L;
   const int inst = a.list ? a.list[blockIdx.y] : (int)blockIdx.y;
+  if (a.mode == MODE_ADMM && L.err[inst].key != 0) {  // its (re)build raised: the host driver decides
+    if (cluster_rank() == 0 && threadIdx.x == 0) a.status[inst] = ST_BUILD_ERR;
+    return;
+  }
   const int n = L.n, m = L.m, c = L.c, nf = L.nf, N = L.N, ldg = L.ldg, mtot = L.mtot;
   const size_t MS = (size_t)n * ldg;
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -1031,6 +1035,10 @@ struct ItemEpi {
 __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a, int R, int max_items) {
   const DevLqr& L = a.L;
   const int inst = a.list ? a.list[blockIdx.y] : (int)blockIdx.y;
+  if (L.err[inst].key != 0) {  // its (re)build raised: the host driver decides
+    if (cluster_rank() == 0 && threadIdx.x == 0) a.status[inst] = ST_BUILD_ERR;
+    return;
+  }
   const int n = L.n, m = L.m, c = L.c, nf = L.nf, N = L.N, ldg = L.ldg, mtot = L.mtot;
   const size_t MS = (size_t)n * ldg;
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
@@ -1677,6 +1685,10 @@ int lqr_solve(Ctx* c, const gsls_qp_t* qp, int generation, double* dx, double* d
   int rc = build_cache(c, qp, nullptr, nullptr, B, st);
   if (rc) return rc;
   rc = check_errors(c, st, "lqr build");
+  if (rc == GSLS_ERR_LOWRANK) {  // indefinite P met by a factored combine: dense re-run
+    if ((rc = build_cache(c, qp, nullptr, nullptr, B, st))) return rc;
+    rc = check_errors(c, st, "lqr build");
+  }
   if (rc) { c->cache_valid = false; return rc; }
   c->cache_valid = true;
   c->generation = generation;
@@ -1819,7 +1831,9 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
     if (rc) return rc;
     if (verbose) cudaEventRecord(ev[1], st);
     rc = check_errors(c, st, "admm");  // synchronizes
-    if (rc) return rc;
+    // GSLS_ERR_LOWRANK: a factored combine met an indefinite P; the tree is now dense and
+    // the instances whose build failed (ST_BUILD_ERR, state untouched) are rebuilt
+    if (rc && rc != GSLS_ERR_LOWRANK) return rc;
     GSLS_CUDA_CHECK(cudaMemcpyAsync(status.data(), c->d_status, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
     GSLS_CUDA_CHECK(cudaStreamSynchronize(st));
     if (verbose) {
@@ -1832,6 +1846,7 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
     for (int i : list) {
       if (status[i] == ST_REBUILD) { next.push_back(i); nrb.push_back(i); }
       else if (status[i] == ST_CONTINUE) next.push_back(i);
+      else if (status[i] == ST_BUILD_ERR) { next.push_back(i); nrb.push_back(i); builds[i]--; }
     }
     list.swap(next);
     rebuild.swap(nrb);

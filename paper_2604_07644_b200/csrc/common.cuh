@@ -44,7 +44,7 @@ struct ErrInfo {
 };
 
 __host__ __device__ inline int err_phase(int code, int label) {
-  if (code == GSLS_ERR_ILL_CONDITIONED) return 2;                              // the combine tree
+  if (code == GSLS_ERR_ILL_CONDITIONED || code == GSLS_ERR_LOWRANK) return 2;  // the combine tree
   if (label == GSLS_LABEL_R_BPB || label == GSLS_LABEL_QU_BPB) return 3;      // gains after the scan
   return 1;                                                                    // leaves / linearize
 }

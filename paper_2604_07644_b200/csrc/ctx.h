@@ -19,6 +19,7 @@ struct DevLqr {
   const int4* cvf_ops;
   const int* cvf_out;
   const int* cvf_loff;   // layer offsets (cvf_layers + 1)
+  const int* cvf_leaf;   // per leaf: bit 3 = C stored as a factor (upload_plan)
   int cvf_nslots, cvf_nops, cvf_layers;
   // COT plan (forward scan over N elements)
   const int4* cot_ops;
@@ -82,6 +83,12 @@ struct Ctx {
   bool admm_prebuilt = false;  // gsls_admm_build_cache ran: the next ADMM solve skips its first build
   void* sls = nullptr;         // SLS workspace (sls.cu), allocated on first use
   int sls_j0 = 0, sls_j1 = -1; // SLS disturbance-column shard [j0, j1) (-1: N), gsls_sls_set_columns
+  // CVF plan variants for the LQR tree: [0] factored combines where C has low rank, [1] all
+  // dense.  A factored combine that meets an indefinite P raises GSLS_ERR_LOWRANK; the
+  // context then switches to the dense variant for good and the scan is re-run.
+  const int4* cvf_ops_v[2] = {nullptr, nullptr};
+  const int* cvf_leaf_v[2] = {nullptr, nullptr};
+  bool lqr_dense = false;
 };
 
 // Matrix half of the CVF combine on an explicit slot space (lqr.cu); shared by
@@ -97,19 +104,24 @@ struct CombineArgs {
   const int* list;
   ErrSlot* err;
   float rel_tol;
+  int label;                   // GSLS_ERR_LOWRANK label: 0 LQR tree, 1 SLS tree
 };
 int launch_combine(const CombineArgs& a, int nops, int count, cudaStream_t st);
 int combine_threads(int n);
 int matmul_threads(int n);
 enum { PLAN_CVF = 0, PLAN_CVF_REC = 1, PLAN_OTHER = 2 };  // upload_plan dead-output analysis
 int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff, int kind,
-                const int** leaf_dead = nullptr);
+                const int** leaf_dead = nullptr, const std::vector<int>* leaf_rank = nullptr, int rmax = 0);
+// Largest C-factor rank the factored combine carries for state dimension n (0: off).
+// GSLS_LOWRANK=0 disables the factored path (every combine dense).
+int factor_rmax(int n);
 void sls_destroy(Ctx* c);
 
 void* dev_alloc(Ctx* c, size_t bytes);
 int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_list, int count,
                 cudaStream_t st);
 int check_errors(Ctx* c, cudaStream_t st, const char* what);
+void sls_use_dense(Ctx* c);  // SLS tree: switch to the all-dense plan variant (sls.cu)
 
 // replay-kernel launch (admm.cu)
 struct ReplayArgs;

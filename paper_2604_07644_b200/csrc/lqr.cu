@@ -17,6 +17,7 @@
 #include "prof.h"
 #include "smallmat.cuh"
 #include "gj.cuh"
+#include "lowrank.cuh"
 
 namespace gsls {
 
@@ -75,6 +76,29 @@ int check_errors(Ctx* c, cudaStream_t st, const char* what) {
   std::vector<ErrSlot> h(B);
   GSLS_CUDA_CHECK(cudaMemcpyAsync(h.data(), c->dev.err, sizeof(ErrSlot) * B, cudaMemcpyDeviceToHost, st));
   GSLS_CUDA_CHECK(cudaStreamSynchronize(st));
+  // A factored combine met an indefinite P (lowrank.cuh): switch that tree to dense
+  // combines, clear those records and tell the caller to re-run the scan.
+  bool lr[2] = {false, false};
+  for (int i = 0; i < B; ++i) {
+    if (h[i].key == 0) continue;
+    const ErrInfo e = err_unpack(h[i].key);
+    if (e.code != GSLS_ERR_LOWRANK) continue;
+    lr[e.label == 1] = true;
+    h[i].key = 0;
+  }
+  if (lr[0] || lr[1]) {
+    if (lr[0]) {  // the LQR cache of those instances is not valid: every caller rebuilds
+      c->lqr_dense = true;
+      c->dev.cvf_ops = c->cvf_ops_v[1];
+      c->dev.cvf_leaf = c->cvf_leaf_v[1];
+      c->cache_valid = false;
+      c->admm_prebuilt = false;
+    }
+    if (lr[1]) sls_use_dense(c);
+    GSLS_CUDA_CHECK(cudaMemcpyAsync(c->dev.err, h.data(), sizeof(ErrSlot) * B, cudaMemcpyHostToDevice, st));
+    GSLS_CUDA_CHECK(cudaStreamSynchronize(st));
+    return GSLS_ERR_LOWRANK;
+  }
   for (int i = 0; i < B; ++i) {
     if (h[i].key == 0) continue;
     const ErrInfo e = err_unpack(h[i].key);
@@ -191,9 +215,18 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   __syncthreads();
   const float* Qg = qp.Q + st * n * n;
   const float* Ag = qp.A + st * n * n;
+  // C-hat = B R-hat^-1 B' is stored as the factor B L^-T (R-hat = L L', L^-1 left in
+  // the inverse's work area) when the scan plan carries it factored (lowrank.cuh)
+  const bool cfac = L.cvf_leaf && (L.cvf_leaf[k] & 8);
+  const double* Linv = wk + kMaxM * (kMaxM + 1);
   for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
     const int i = e / ldg, j = e - i * ldg;
     double p = 0.0, a = 0.0, cc = 0.0;
+    if (cfac && j < m) {
+      double f = 0.0;
+      for (int b = 0; b <= j; ++b) f = fma(Bst[i * m + b], Linv[j * (kMaxM + 1) + b], f);
+      cc = f;
+    }
     if (j < n) {
       double s = 0.0;
       for (int r = 0; r < c; ++r) s = fma(Cst[r * n + i], Cst[r * n + j], s);
@@ -206,7 +239,7 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
       }
       p = qh - sr;
       a = (double)Ag[i * n + j] - br;
-      cc = bb;
+      if (!cfac) cc = bb;
     }
     Pd[e] = (float)p;
     Ad[e] = (float)a;
@@ -300,6 +333,102 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
 // GSLS_COMBINE_TRACE: clock64 at the phase points of one CTA mid-grid (diagnostics only).
 __device__ long long* g_comb_trace = nullptr;
 
+// Factored combine (lowrank.cuh) of one op: C_l = F F' with F the earlier slot's
+// factor (rank re = op.w bits 8-15), C_r the later slot's factor (rank rl, bits
+// 16-23) or dense (rl = 255); bit 3: the output C is stored as the factor
+// [U, F_r].  Same outputs and record layout as the dense path below.  Six
+// ldg x lds buffers:
+//   b0 Pr -> Pm | b1 F -> Fh -> X' | b2 W -> V -> Fr' | b3 Al | b4 Ar' -> Psi' | sb S -> U' -> V' -> T
+// Returns false (block-uniform) when S has a pivot below 0.5 (P_r indefinite).
+template <int NP>
+__device__ __forceinline__ bool cvf_combine_factored(const CombineArgs& a, const int4 op, int inst, float* sm,
+                                                     float* rec) {
+  const int n = a.n, ldg = ldg_of(n), lds = gj_lds(NP, n);
+  const int re = (op.w >> 8) & 0xFF, rl = (op.w >> 16) & 0xFF;
+  const int R = round_up(re, 4);
+  const size_t MS = (size_t)n * ldg;
+  const size_t BSL = (size_t)ldg * lds;
+  float* b0 = sm;
+  float* b1 = b0 + BSL;
+  float* b2 = b1 + BSL;
+  float* b3 = b2 + BSL;
+  float* b4 = b3 + BSL;
+  float* sb = b4 + BSL;
+  const long long ib = (long long)inst * a.inst_stride;
+  const size_t oe = (size_t)op.y * MS, ol = (size_t)op.z * MS, od = (size_t)op.x * MS;
+  const bool need_a = !(op.w & 1);                // A (A^T unless bit 2) live
+  const bool need_c = !(op.w & 2);                // C live
+  const bool need_psi = rec != nullptr || need_a;
+  const bool need_u = need_psi || need_c;
+  const bool out_factor = (op.w & 8) != 0;
+  const float* Cr = a.Cs + ib + ol;
+  float* Cd = a.Cs + ib + od;
+  cta_load_async(b0, lds, a.Ps + ib + ol, n);  // Pr
+  cta_load_async(b1, lds, a.Cs + ib + oe, n);  // F (columns >= re stored as zero)
+  cp_async_commit();
+  cta_load_async(b3, lds, a.As + ib + oe, n);  // Al
+  if (need_u) cta_load_async(b4, lds, a.ATs + ib + ol, n);  // Ar^T
+  cp_async_commit();
+  cp_async_wait<1>();
+  __syncthreads();
+  gemm_tn_mn(n, R, n, b0, lds, b1, lds, EpiS{b2, lds, n});  // W = Pr F
+  __syncthreads();
+  gemm_tn_mn(R, R, n, b1, lds, b2, lds, EpiSId{sb, lds, R});  // S = I + F' W
+  __syncthreads();
+  if (!chol_stack(sb, b1, b2, lds, R, n)) return false;  // b1 = Fh, b2 = V
+  cp_async_wait<0>();
+  __syncthreads();
+  if (need_u) {
+    gemm_tn_mn(R, n, n, b1, lds, b4, lds, EpiS{sb, lds, R});  // U' = Fh' Ar^T
+    __syncthreads();
+    if (need_psi)  // Psi' = Ar^T - V U' (in place), record slot 2
+      gemm_nn_mn(n, n, R, b2, lds, sb, lds, EpiSub{b4, b4, lds, n, rec ? rec + 2 * MS : nullptr, ldg});
+    if (rec)  // -Y' = -Fh U', record slot 3
+      gemm_nn_mn(n, n, R, b1, lds, sb, lds, EpiG{rec + 3 * MS, nullptr, ldg, n, nullptr, nullptr, 0, -1.f});
+    if (need_c) {
+      if (out_factor) {  // [U | F_r], zero beyond
+        for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
+          const int i = e / ldg, j = e - i * ldg;
+          Cd[(size_t)i * ldg + j] = j < re ? sb[j * lds + i] : (j < re + rl ? Cr[(size_t)i * ldg + j - re] : 0.f);
+        }
+      } else {  // U U' + C_r (dense C_r; a factored C_r is added at the end)
+        gemm_tn_mn(n, n, R, sb, lds, sb, lds, EpiG{Cd, rl == 255 ? Cr : nullptr, ldg, n, nullptr, nullptr, 0, 1.f});
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < R * ldg; e += blockDim.x) {  // V' -> sb
+    const int k = e / ldg, i = e - k * ldg;
+    sb[k * lds + i] = i < n ? b2[i * lds + k] : 0.f;
+  }
+  __syncthreads();
+  gemm_tn_mn(n, n, R, sb, lds, sb, lds, EpiSub{b0, b0, lds, n, nullptr, 0});  // Pm = Pr - V V'
+  __syncthreads();
+  if (rec) {
+    gemm_tn_mn(R, n, n, b2, lds, b3, lds, EpiS{sb, lds, R});  // T = V' Al
+    __syncthreads();
+    gemm_nn_mn(n, n, R, b1, lds, sb, lds, EpiSub{nullptr, b3, lds, n, rec, ldg});  // Ups' = Al - Fh T, slot 0
+    __syncthreads();
+  }
+  // X' = Pm Al (record slot 1), then P = Al' X' + Pl
+  gemm_tn_mn(n, n, n, b0, lds, b3, lds, EpiG{rec ? rec + MS : nullptr, nullptr, ldg, n, nullptr, b1, lds, 1.f});
+  __syncthreads();
+  gemm_tn_mn(n, n, n, b3, lds, b1, lds, EpiG{a.Ps + ib + od, a.Ps + ib + oe, ldg, n, nullptr, nullptr, 0, 1.f});
+  if (need_a)  // A = Psi Al (+ A^T)
+    gemm_tn_mn(n, n, n, b4, lds, b3, lds,
+               EpiG{a.As + ib + od, nullptr, ldg, n, (op.w & 4) ? nullptr : a.ATs + ib + od, nullptr, 0, 1.f});
+  if (need_c && !out_factor && rl != 255) {  // C += F_r F_r'
+    const int RL = round_up(rl, 4);
+    for (int e = threadIdx.x; e < RL * ldg; e += blockDim.x) {
+      const int k = e / ldg, i = e - k * ldg;
+      b2[k * lds + i] = i < n ? Cr[(size_t)i * ldg + k] : 0.f;
+    }
+    __syncthreads();
+    gemm_tn_mn(n, n, RL, b2, lds, b2, lds, EpiG{Cd, Cd, ldg, n, nullptr, nullptr, 0, 1.f});
+  }
+  return true;
+}
+
 template <int NP>
 __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_combine(CombineArgs a) {
   long long* trc = (g_comb_trace && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == gridDim.y / 2) ? g_comb_trace : nullptr;
@@ -311,6 +440,15 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   const size_t MS = (size_t)n * ldg;
   const size_t BS = (size_t)n * lds;
   extern __shared__ float sm[];
+  if (((op.w >> 8) & 0xFF) != 0xFF) {  // earlier C carried as a factor
+    float* recf = a.rec ? a.rec + (long long)inst * a.rec_inst_stride + (size_t)(a.op_base + blockIdx.x) * 4 * MS
+                        : nullptr;
+    const bool ok = cvf_combine_factored<NP>(a, op, inst, sm, recf);
+    if (!ok && threadIdx.x == 0)
+      raise_err(a.err ? a.err + inst : nullptr, GSLS_ERR_LOWRANK, a.op_base + blockIdx.x, -1, a.label);
+    CTRACE(5);
+    return;
+  }
   float* b0 = sm;
   float* b1 = b0 + BS;
   float* b2 = b1 + BS;
@@ -381,7 +519,9 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
 
 size_t combine_smem_bytes(int n) {
   const int NP = n <= 64 ? 64 : 80;
-  return (6 * (size_t)n * gj_lds(NP, n) + gjl_scratch_words(NP)) * sizeof(float);
+  const size_t dense = 6 * (size_t)n * gj_lds(NP, n) + gjl_scratch_words(NP);
+  const size_t factored = 6 * (size_t)ldg_of(n) * gj_lds(NP, n);  // cvf_combine_factored
+  return std::max(dense, factored) * sizeof(float);
 }
 
 int combine_threads(int n) {  // k_cvf_combine: 4*NP row threads + the inverse's panel warp, >= GEMM tiles
@@ -633,7 +773,7 @@ int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_l
   for (int l = 0; l < c->cvf.layers; ++l) {
     const int o0 = c->cvf_layer_off[l], o1 = c->cvf_layer_off[l + 1];
     CombineArgs a{n, L.cvf_ops + o0, o0, L.Ps, L.As, L.Cs, L.ATs, (long long)L.cvf_nslots * (long long)MS,
-                  L.cvf_rec, (long long)L.cvf_nops * 4 * (long long)MS, d_list, L.err, 1e-10f};
+                  L.cvf_rec, (long long)L.cvf_nops * 4 * (long long)MS, d_list, L.err, 1e-10f, 0};
     if (o1 == o0) continue;
     ProfScope ps(P_CVF_LQR, st, (double)(o1 - o0) * count);
     int rc = launch_combine(a, o1 - o0, count, st);
@@ -668,8 +808,14 @@ int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_l
 // ---------------------------------------------------------------------------
 // context
 
+int factor_rmax(int n) {
+  const char* e = getenv("GSLS_LOWRANK");
+  if (e && e[0] == '0') return 0;
+  return (n / 4) * 4;  // the output factor [U, F_r] must fit the slot's n x ldg storage
+}
+
 int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff, int kind,
-                const int** leaf_dead) {
+                const int** leaf_dead, const std::vector<int>* leaf_rank, int rmax) {
   std::vector<int4> h(p.ops.size() ? p.ops.size() : 1);
   // Dead-output flags in .w, from the last layer back (kind: PLAN_CVF / PLAN_CVF_REC /
   // PLAN_OTHER).  For a CVF combine (dst <- earlier (x) later) a reader needs, of its
@@ -704,9 +850,47 @@ int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, co
       }
     }
   }
-  if (leaf_dead) {  // per leaf slot (< p.length): bit 0 A dead, bit 1 A^T dead, bit 2 C dead
+  // C representation (CVF plans; lowrank.cuh): every slot's C is either a factor F F'
+  // (F: n x rank, rank <= rmax) or dense.  Leaves have the ranks given (m; 0 for the
+  // terminal element); a combine's C has rank <= rank C_earlier + rank C_later, so its
+  // output is a factor while both operands are and the sum stays <= rmax.  A combine
+  // whose earlier C is dense takes the dense path, which adds C_later as a dense matrix
+  // when it forms its own C: such a later slot is forced dense (its producer then writes
+  // the dense C), iterated to a fixed point.
+  //   .w bits 8-15: rank of the earlier operand's C factor (255: dense -> dense path)
+  //   .w bits 16-23: rank of the later operand's C factor (255: dense)
+  //   .w bit 3: the output C is stored as a factor
+  // Leaf flag bit 3: the leaf's C is stored as a factor.
+  std::vector<int> rep(ns, -1);
+  if (cvf && leaf_rank) {
+    std::vector<char> forced(ns, 0);
+    for (int iter = 0; iter < ns + 1; ++iter) {
+      for (int i = 0; i < p.length && i < ns; ++i) rep[i] = forced[i] ? -1 : (*leaf_rank)[i];
+      for (const ScanOp& q : p.ops) {
+        const int re = rep[q.earlier], rl = rep[q.later];
+        rep[q.dst] = (forced[q.dst] || re < 0 || rl < 0 || re + rl > rmax) ? -1 : re + rl;
+      }
+      bool changed = false;
+      for (size_t o = 0; o < p.ops.size(); ++o) {
+        const ScanOp& q = p.ops[o];
+        if (rep[q.earlier] < 0 && !(h[o].w & 2) && rep[q.later] >= 0 && !forced[q.later]) {
+          forced[q.later] = 1;
+          changed = true;
+        }
+      }
+      if (!changed) break;
+    }
+  }
+  if (cvf)
+    for (size_t o = 0; o < p.ops.size(); ++o) {
+      const ScanOp& q = p.ops[o];
+      const int re = rep[q.earlier], rl = rep[q.later];
+      h[o].w |= ((re < 0 ? 255 : re) << 8) | ((rl < 0 ? 255 : rl) << 16) | (rep[q.dst] >= 0 ? 8 : 0);
+    }
+  if (leaf_dead) {  // per leaf slot (< p.length): bit 0 A dead, bit 1 A^T dead, bit 2 C dead, bit 3 C factored
     std::vector<int> lf(std::max(p.length, 1), 0);
-    for (int i = 0; i < p.length && i < ns; ++i) lf[i] = (nA[i] ? 0 : 1) | (nAT[i] ? 0 : 2) | (nC[i] ? 0 : 4);
+    for (int i = 0; i < p.length && i < ns; ++i)
+      lf[i] = (nA[i] ? 0 : 1) | (nAT[i] ? 0 : 2) | (nC[i] ? 0 : 4) | (rep[i] >= 0 ? 8 : 0);
     int* dlf = (int*)dev_alloc(c, lf.size() * sizeof(int));
     if (!dlf) return GSLS_ERR_CUDA;
     GSLS_CUDA_CHECK(cudaMemcpy(dlf, lf.data(), lf.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -757,7 +941,17 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
 
   DevLqr& L = c->dev;
   L.n = d.nx; L.m = d.nu; L.c = d.nc; L.nf = d.nf; L.N = d.N; L.ldg = c->ldg; L.mtot = c->mtot;
-  int rc = upload_plan(c, c->cvf, &L.cvf_ops, &L.cvf_out, &L.cvf_loff, PLAN_CVF_REC);
+  // leaf C ranks: B R^-1 B' (m) at the stages, 0 at the terminal element (lqr.py:306-320)
+  std::vector<int> leaf_rank(d.N + 1, d.nu);
+  leaf_rank[d.N] = 0;
+  const int rmax = factor_rmax(d.nx);
+  int rc = upload_plan(c, c->cvf, &c->cvf_ops_v[1], &L.cvf_out, &L.cvf_loff, PLAN_CVF_REC, &c->cvf_leaf_v[1]);
+  if (!rc)
+    rc = upload_plan(c, c->cvf, &c->cvf_ops_v[0], &L.cvf_out, &L.cvf_loff, PLAN_CVF_REC, &c->cvf_leaf_v[0],
+                     rmax > 0 ? &leaf_rank : nullptr, rmax);
+  c->lqr_dense = false;
+  L.cvf_ops = c->cvf_ops_v[0];
+  L.cvf_leaf = c->cvf_leaf_v[0];
   if (!rc && d.N > 0) rc = upload_plan(c, c->cot, &L.cot_ops, &L.cot_out, &L.cot_loff, PLAN_OTHER);
   if (rc) { delete c; return rc; }
   L.cvf_nphys = compress_slots(c->cvf, c->cvf_phys);

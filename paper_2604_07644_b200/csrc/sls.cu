@@ -94,11 +94,23 @@ struct SlsState {
   ScanPlan cvf, mp;
   DevSls dev{};
   bool ready = false;
+  // CVF plan variants (lowrank.cuh): [0] factored combines where C has low rank, [1] dense
+  const int4* cvf_ops_v[2] = {nullptr, nullptr};
+  const int* leaf_v[2] = {nullptr, nullptr};
+  bool dense = false;
 };
 
 static SlsState* sls_of(Ctx* c) { return reinterpret_cast<SlsState*>(c->sls); }
 
 void sls_destroy(Ctx* c) { delete sls_of(c); c->sls = nullptr; }
+
+void sls_use_dense(Ctx* c) {
+  SlsState* s = sls_of(c);
+  if (!s) return;
+  s->dense = true;
+  s->dev.cvf_ops = s->cvf_ops_v[1];
+  s->dev.leaf_dead = s->leaf_v[1];
+}
 
 static int sls_init(Ctx* c) {
   if (c->sls) return GSLS_OK;
@@ -119,14 +131,24 @@ static int sls_init(Ctx* c) {
   S.cmax = std::max(1, std::max(d.nc, d.nf));
   s->cvf = merge_columns(N, true, S.j0, S.j1);
   s->mp = merge_columns(N, false, S.j0, S.j1);
-  int rc = upload_plan(c, s->cvf, &S.cvf_ops, &S.cvf_out, &S.cvf_loff, PLAN_CVF, &S.leaf_dead);
-  if (!rc) rc = upload_plan(c, s->mp, &S.mp_ops, &S.mp_out, &S.mp_loff, PLAN_OTHER);
-  if (rc) return rc;
-  S.cvf_nslots = s->cvf.nslots; S.cvf_nops = (int)s->cvf.ops.size(); S.cvf_layers = s->cvf.layers;
-  S.mp_nslots = s->mp.nslots; S.mp_nops = (int)s->mp.ops.size(); S.mp_layers = s->mp.layers;
   std::vector<int2> kj(S.ncell);
   for (int j = S.j0; j < S.j1; ++j)
     for (int k = j + 1; k <= N; ++k) kj[cell_of(N, k, j) - S.cell0] = make_int2(k, j);
+  // leaf C ranks: B Qu^-1 B' (m) on the stage cells, 0 on the terminal cells (sls.py:262-278)
+  std::vector<int> leaf_rank(S.ncell);
+  for (int i = 0; i < S.ncell; ++i) leaf_rank[i] = kj[i].x == N ? 0 : m;
+  const int rmax = factor_rmax(n);
+  int rc = upload_plan(c, s->cvf, &s->cvf_ops_v[1], &S.cvf_out, &S.cvf_loff, PLAN_CVF, &s->leaf_v[1]);
+  if (!rc)
+    rc = upload_plan(c, s->cvf, &s->cvf_ops_v[0], &S.cvf_out, &S.cvf_loff, PLAN_CVF, &s->leaf_v[0],
+                     rmax > 0 ? &leaf_rank : nullptr, rmax);
+  if (!rc) rc = upload_plan(c, s->mp, &S.mp_ops, &S.mp_out, &S.mp_loff, PLAN_OTHER);
+  if (rc) return rc;
+  s->dense = false;
+  S.cvf_ops = s->cvf_ops_v[0];
+  S.leaf_dead = s->leaf_v[0];
+  S.cvf_nslots = s->cvf.nslots; S.cvf_nops = (int)s->cvf.ops.size(); S.cvf_layers = s->cvf.layers;
+  S.mp_nslots = s->mp.nslots; S.mp_nops = (int)s->mp.ops.size(); S.mp_layers = s->mp.layers;
   int2* dkj = (int2*)dev_alloc(c, sizeof(int2) * S.ncell);
   if (!dkj) return GSLS_ERR_CUDA;
   GSLS_CUDA_CHECK(cudaMemcpy(dkj, kj.data(), sizeof(int2) * S.ncell, cudaMemcpyHostToDevice));
@@ -313,6 +335,10 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   __syncthreads();
   const float* Ak = qp.A + st * n * n;
   const int dead = S.leaf_dead[cell];  // parts of this leaf no combine reads (scan-plan analysis)
+  // C = B Qu^-1 B' stored as the factor B L^-T (Qu = L L', L^-1 left in the inverse's
+  // work area) when the plan carries it factored (lowrank.cuh)
+  const bool cfac = (dead & 8) != 0;
+  const double* Linv = wk + kMaxM * (kMaxM + 1);
   const int q4 = np >> 2;
   for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
     const int i = e / q4, j0 = (e - i * q4) << 2;
@@ -339,6 +365,12 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
       po[t] = in ? (float)(Qx[i * n + jj] - p4[t]) : 0.f;
       ao[t] = in ? (float)((double)Ak[i * n + jj] - a4[t]) : 0.f;
       co[t] = in ? (float)c4[t] : 0.f;
+      if (cfac) {
+        double f = 0.0;
+        if (jj < m)
+          for (int b = 0; b <= jj; ++b) f = fma(BT[b * np + i], Linv[jj * (kMaxM + 1) + b], f);
+        co[t] = (float)f;
+      }
       if (in && !(dead & 2)) ATd[(size_t)jj * ldg + i] = ao[t];
     }
     *reinterpret_cast<float4*>(Pd + (size_t)i * ldg + j0) = make_float4(po[0], po[1], po[2], po[3]);
@@ -753,7 +785,22 @@ int sls_set_costs(Ctx* c, const double* Qx, const double* Qu, const double* Qux,
   return GSLS_OK;
 }
 
+static int sls_synthesize_once(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st);
+
+// A factored combine that met an indefinite P (GSLS_ERR_LOWRANK) switches the tree to
+// dense combines; the synthesis is then re-run once.
 int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st, bool check) {
+  int rc = sls_synthesize_once(c, qp, E, st);
+  if (rc || !check) return rc;
+  rc = check_errors(c, st, "sls.synthesize");
+  if (rc == GSLS_ERR_LOWRANK) {
+    rc = sls_synthesize_once(c, qp, E, st);
+    if (!rc) rc = check_errors(c, st, "sls.synthesize");
+  }
+  return rc;
+}
+
+static int sls_synthesize_once(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st) {
   int rc = sls_init(c);
   if (rc) return rc;
   SlsState* s = sls_of(c);
@@ -771,7 +818,7 @@ int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st,
   for (int l = 0; l < s->cvf.layers; ++l) {
     const int o0 = s->cvf.layer_off[l], o1 = s->cvf.layer_off[l + 1];
     CombineArgs a{n, S.cvf_ops + o0, o0, S.Ps, S.As, S.Cs, S.ATs, (long long)S.cvf_nslots * (long long)MS, nullptr, 0,
-                  nullptr, S.err, 1e-10f};
+                  nullptr, S.err, 1e-10f, 1};
     if (o1 == o0) continue;
     ProfScope ps(P_SLS_CVF, st, (double)(o1 - o0) * B);
     if ((rc = launch_combine(a, o1 - o0, B, st))) return rc;
@@ -803,7 +850,7 @@ int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st,
     GSLS_CUDA_CHECK(cudaGetLastError());
   }
   S.have_response = 1;
-  return check ? check_errors(c, st, "sls.synthesize") : GSLS_OK;
+  return GSLS_OK;
 }
 
 static int sls_rownorms(Ctx* c, const gsls_qp_t* qp, cudaStream_t st) {
