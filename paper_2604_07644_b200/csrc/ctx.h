@@ -112,9 +112,9 @@ int matmul_threads(int n);
 enum { PLAN_CVF = 0, PLAN_CVF_REC = 1, PLAN_OTHER = 2 };  // upload_plan dead-output analysis
 int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff, int kind,
                 const int** leaf_dead = nullptr, const std::vector<int>* leaf_rank = nullptr, int rmax = 0);
-// Largest C-factor rank the factored combine carries for state dimension n (0: off).
-// GSLS_LOWRANK=0 disables the factored path (every combine dense).
-int factor_rmax(int n);
+// Largest C-factor rank the factored combine carries for state dimension n in the
+// LQR (tree 0) or SLS (tree 1) scan; 0: off.  GSLS_LOWRANK=0 / sls / lqr restricts it.
+int factor_rmax(int n, int tree);
 void sls_destroy(Ctx* c);
 
 void* dev_alloc(Ctx* c, size_t bytes);

@@ -31,14 +31,39 @@
 namespace gsls {
 
 // ---- generalized GEMMs (4x4 register tiles, float4 smem operands) ----------------
+//
+// Small outputs (an n x r or r x r product has only a few dozen 4x4 tiles) split K
+// over KS adjacent lanes so the whole CTA works; the KS partial tiles are summed
+// with a fixed butterfly of warp shuffles (deterministic), and the part-0 lane
+// runs the epilogue.
+
+__device__ inline int gemm_ks(int tiles, int K) {
+  int ks = 1;
+  while (ks < 8 && tiles * ks * 2 <= (int)blockDim.x && K >= 8 * ks) ks <<= 1;
+  return ks;
+}
+
+__device__ inline void ks_reduce(float (&acc)[4][4], int ks) {
+  for (int o = 1; o < ks; o <<= 1) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] += __shfl_xor_sync(0xffffffffu, acc[a][b], o);
+  }
+}
 
 // C[i][j] = sum_{k<K} At[k][i] B[k][j] for i < round_up(M,4), j < round_up(Nc,4).
 template <class Epi>
 __device__ inline void gemm_tn_mn(int M, int Nc, int K, const float* At, int lda, const float* B, int ldb,
                                   Epi epi) {
-  const int TM = (M + 3) >> 2, TN = (Nc + 3) >> 2;
-  for (int t = threadIdx.x; t < TM * TN; t += blockDim.x) {
-    const int ti = t / TN, tj = t - ti * TN;
+  const int TM = (M + 3) >> 2, TN = (Nc + 3) >> 2, tiles = TM * TN;
+  const int ks = gemm_ks(tiles, K);
+  const int work = tiles * ks;
+  for (int base = 0; base < work; base += blockDim.x) {
+    const int t = base + threadIdx.x;
+    const int tile = t / ks, part = t - tile * ks;
+    const bool valid = t < work;
+    const int ti = valid ? tile / TN : 0, tj = valid ? tile - ti * TN : 0;
     float acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -46,8 +71,9 @@ __device__ inline void gemm_tn_mn(int M, int Nc, int K, const float* At, int lda
       for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
     const float* pa = At + 4 * ti;
     const float* pb = B + 4 * tj;
+    const int kend = valid ? K : 0;
 #pragma unroll 4
-    for (int k = 0; k < K; ++k) {
+    for (int k = part; k < kend; k += ks) {
       const float4 a = *reinterpret_cast<const float4*>(pa + k * lda);
       const float4 b = *reinterpret_cast<const float4*>(pb + k * ldb);
       const float av[4] = {a.x, a.y, a.z, a.w};
@@ -59,7 +85,8 @@ __device__ inline void gemm_tn_mn(int M, int Nc, int K, const float* At, int lda
         acc[r][3] = fmaf(av[r], b.w, acc[r][3]);
       }
     }
-    epi(4 * ti, 4 * tj, acc);
+    if (ks > 1) ks_reduce(acc, ks);
+    if (valid && part == 0) epi(4 * ti, 4 * tj, acc);
   }
 }
 
@@ -68,9 +95,14 @@ __device__ inline void gemm_tn_mn(int M, int Nc, int K, const float* At, int lda
 template <class Epi>
 __device__ inline void gemm_nn_mn(int M, int Nc, int K, const float* A, int lda, const float* B, int ldb,
                                   Epi epi) {
-  const int TM = (M + 3) >> 2, TN = (Nc + 3) >> 2;
-  for (int t = threadIdx.x; t < TM * TN; t += blockDim.x) {
-    const int ti = t / TN, tj = t - ti * TN;
+  const int TM = (M + 3) >> 2, TN = (Nc + 3) >> 2, tiles = TM * TN;
+  const int ks = gemm_ks(tiles, K);
+  const int work = tiles * ks;
+  for (int base = 0; base < work; base += blockDim.x) {
+    const int t = base + threadIdx.x;
+    const int tile = t / ks, part = t - tile * ks;
+    const bool valid = t < work;
+    const int ti = valid ? tile / TN : 0, tj = valid ? tile - ti * TN : 0;
     float acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -78,8 +110,9 @@ __device__ inline void gemm_nn_mn(int M, int Nc, int K, const float* A, int lda,
       for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
     const float* pa = A + 4 * ti * lda;
     const float* pb = B + 4 * tj;
+    const int kend = valid ? K : 0;
 #pragma unroll 2
-    for (int k = 0; k < K; k += 4) {
+    for (int k = 4 * part; k < kend; k += 4 * ks) {
       float4 ar[4], bk[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) ar[r] = *reinterpret_cast<const float4*>(pa + r * lda + k);
@@ -97,7 +130,8 @@ __device__ inline void gemm_nn_mn(int M, int Nc, int K, const float* A, int lda,
         }
       }
     }
-    epi(4 * ti, 4 * tj, acc);
+    if (ks > 1) ks_reduce(acc, ks);
+    if (valid && part == 0) epi(4 * ti, 4 * tj, acc);
   }
 }
 
@@ -161,13 +195,17 @@ struct EpiG {
   float* D;
   int dld;
   float scale;  // 1 or -1
+  const float* sadd = nullptr;  // smem addend (ld dld), used instead of add when set
   __device__ void operator()(int i0, int j0, float (&acc)[4][4]) const {
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int i = i0 + r;
       if (i >= rows) break;
       float4 v = make_float4(scale * acc[r][0], scale * acc[r][1], scale * acc[r][2], scale * acc[r][3]);
-      if (add) {
+      if (sadd) {
+        const float4 a = *reinterpret_cast<const float4*>(sadd + i * dld + j0);
+        v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+      } else if (add) {
         const float4 a = *reinterpret_cast<const float4*>(add + (size_t)i * ld + j0);
         v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
       }
@@ -208,7 +246,7 @@ __device__ inline bool chol_stack(float* Sb, float* Fb, float* Wb, int lds, int 
     float li[4][4];  // Lp^-1 (lower)
     bool ok = true;
     {
-      float l[4][4] = {};
+      float l[4][4] = {}, rd[4];  // rd[c] = 1 / l[c][c]
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         float s = d[c][c];
@@ -218,6 +256,7 @@ __device__ inline bool chol_stack(float* Sb, float* Fb, float* Wb, int lds, int 
         ok = ok && (s >= 0.5f) && isfinite(s);
         const float rs = rsqrtf(fmaxf(s, 1e-30f));
         l[c][c] = s * rs;
+        rd[c] = rs;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           if (r > c) {
@@ -238,7 +277,7 @@ __device__ inline bool chol_stack(float* Sb, float* Fb, float* Wb, int lds, int 
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             if (q >= c && q < r) t = fmaf(-l[r][q], li[q][c], t);
-          li[r][c] = t / l[r][r];
+          li[r][c] = t * rd[r];
         }
       }
     }
@@ -261,12 +300,14 @@ __device__ inline bool chol_stack(float* Sb, float* Fb, float* Wb, int lds, int 
     }
     __syncthreads();
     // phase B: trailing update Z[i][t] -= sum_c z~[i][c] L[t][c] for t >= jb + 4
+    // consecutive threads take consecutive rows of one column group: the row loads are
+    // conflict-free (ld = 4 mod 8 words) and the group's L rows are broadcasts
     const int g0 = (jb >> 2) + 1, ng = (R >> 2) - g0;
     if (ng > 0) {
       const int rows_below = nrow - (jb + 4);
       for (int e = threadIdx.x; e < rows_below * ng; e += blockDim.x) {
-        const int ii = e / ng, g = g0 + (e - ii * ng);
-        const int i = jb + 4 + ii;
+        const int gg = e / rows_below, ii = e - gg * rows_below;
+        const int g = g0 + gg, i = jb + 4 + ii;
         if (i < R && 4 * g > i) continue;  // S: lower triangle (and diagonal blocks) only
         float* p = row(i);
         const float4 z = *reinterpret_cast<const float4*>(p + jb);

@@ -342,7 +342,8 @@ __device__ long long* g_comb_trace = nullptr;
 // Returns false (block-uniform) when S has a pivot below 0.5 (P_r indefinite).
 template <int NP>
 __device__ __forceinline__ bool cvf_combine_factored(const CombineArgs& a, const int4 op, int inst, float* sm,
-                                                     float* rec) {
+                                                     float* rec, long long* trc) {
+#define FTRACE(i) do { if (trc) trc[i] = clock64(); } while (0)
   const int n = a.n, ldg = ldg_of(n), lds = gj_lds(NP, n);
   const int re = (op.w >> 8) & 0xFF, rl = (op.w >> 16) & 0xFF;
   const int R = round_up(re, 4);
@@ -368,16 +369,20 @@ __device__ __forceinline__ bool cvf_combine_factored(const CombineArgs& a, const
   cp_async_commit();
   cta_load_async(b3, lds, a.As + ib + oe, n);  // Al
   if (need_u) cta_load_async(b4, lds, a.ATs + ib + ol, n);  // Ar^T
+  else cta_load_async(b4, lds, a.Ps + ib + oe, n);          // Pl (the P epilogue's addend)
   cp_async_commit();
   cp_async_wait<1>();
   __syncthreads();
+  FTRACE(8);
   gemm_tn_mn(n, R, n, b0, lds, b1, lds, EpiS{b2, lds, n});  // W = Pr F
   __syncthreads();
   gemm_tn_mn(R, R, n, b1, lds, b2, lds, EpiSId{sb, lds, R});  // S = I + F' W
   __syncthreads();
+  FTRACE(9);
   if (!chol_stack(sb, b1, b2, lds, R, n)) return false;  // b1 = Fh, b2 = V
   cp_async_wait<0>();
   __syncthreads();
+  FTRACE(10);
   if (need_u) {
     gemm_tn_mn(R, n, n, b1, lds, b4, lds, EpiS{sb, lds, R});  // U' = Fh' Ar^T
     __syncthreads();
@@ -386,10 +391,14 @@ __device__ __forceinline__ bool cvf_combine_factored(const CombineArgs& a, const
     if (rec)  // -Y' = -Fh U', record slot 3
       gemm_nn_mn(n, n, R, b1, lds, sb, lds, EpiG{rec + 3 * MS, nullptr, ldg, n, nullptr, nullptr, 0, -1.f});
     if (need_c) {
-      if (out_factor) {  // [U | F_r], zero beyond
-        for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
-          const int i = e / ldg, j = e - i * ldg;
-          Cd[(size_t)i * ldg + j] = j < re ? sb[j * lds + i] : (j < re + rl ? Cr[(size_t)i * ldg + j - re] : 0.f);
+      if (out_factor) {  // [U | F_r], zero beyond (ranks are multiples of 4: float4 columns)
+        const int q = ldg >> 2;
+        for (int e = threadIdx.x; e < n * q; e += blockDim.x) {
+          const int j = (e / n) << 2, i = e - (e / n) * n;  // consecutive threads: consecutive rows
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (j < re) v = make_float4(sb[j * lds + i], sb[(j + 1) * lds + i], sb[(j + 2) * lds + i], sb[(j + 3) * lds + i]);
+          else if (j < re + rl) v = *reinterpret_cast<const float4*>(Cr + (size_t)i * ldg + j - re);
+          *reinterpret_cast<float4*>(Cd + (size_t)i * ldg + j) = v;
         }
       } else {  // U U' + C_r (dense C_r; a factored C_r is added at the end)
         gemm_tn_mn(n, n, R, sb, lds, sb, lds, EpiG{Cd, rl == 255 ? Cr : nullptr, ldg, n, nullptr, nullptr, 0, 1.f});
@@ -397,6 +406,7 @@ __device__ __forceinline__ bool cvf_combine_factored(const CombineArgs& a, const
     }
     __syncthreads();
   }
+  FTRACE(11);
   for (int e = threadIdx.x; e < R * ldg; e += blockDim.x) {  // V' -> sb
     const int k = e / ldg, i = e - k * ldg;
     sb[k * lds + i] = i < n ? b2[i * lds + k] : 0.f;
@@ -407,17 +417,26 @@ __device__ __forceinline__ bool cvf_combine_factored(const CombineArgs& a, const
   if (rec) {
     gemm_tn_mn(R, n, n, b2, lds, b3, lds, EpiS{sb, lds, R});  // T = V' Al
     __syncthreads();
+    if (need_u) cta_load_async(b2, lds, a.Ps + ib + oe, n);  // Pl (V is dead)
+    cp_async_commit();
     gemm_nn_mn(n, n, R, b1, lds, sb, lds, EpiSub{nullptr, b3, lds, n, rec, ldg});  // Ups' = Al - Fh T, slot 0
     __syncthreads();
+  } else if (need_u) {
+    cta_load_async(b2, lds, a.Ps + ib + oe, n);  // Pl (V is dead)
+    cp_async_commit();
   }
+  const float* plb = need_u ? b2 : b4;
+  FTRACE(12);
   // X' = Pm Al (record slot 1), then P = Al' X' + Pl
   gemm_tn_mn(n, n, n, b0, lds, b3, lds, EpiG{rec ? rec + MS : nullptr, nullptr, ldg, n, nullptr, b1, lds, 1.f});
+  cp_async_wait<0>();
   __syncthreads();
-  gemm_tn_mn(n, n, n, b3, lds, b1, lds, EpiG{a.Ps + ib + od, a.Ps + ib + oe, ldg, n, nullptr, nullptr, 0, 1.f});
+  gemm_tn_mn(n, n, n, b3, lds, b1, lds, EpiG{a.Ps + ib + od, nullptr, ldg, n, nullptr, nullptr, lds, 1.f, plb});
   if (need_a)  // A = Psi Al (+ A^T)
     gemm_tn_mn(n, n, n, b4, lds, b3, lds,
                EpiG{a.As + ib + od, nullptr, ldg, n, (op.w & 4) ? nullptr : a.ATs + ib + od, nullptr, 0, 1.f});
   if (need_c && !out_factor && rl != 255) {  // C += F_r F_r'
+    __syncthreads();  // b2 may hold Pl, read by the P epilogue above
     const int RL = round_up(rl, 4);
     for (int e = threadIdx.x; e < RL * ldg; e += blockDim.x) {
       const int k = e / ldg, i = e - k * ldg;
@@ -426,6 +445,9 @@ __device__ __forceinline__ bool cvf_combine_factored(const CombineArgs& a, const
     __syncthreads();
     gemm_tn_mn(n, n, RL, b2, lds, b2, lds, EpiG{Cd, Cd, ldg, n, nullptr, nullptr, 0, 1.f});
   }
+  __syncthreads();
+  FTRACE(13);
+#undef FTRACE
   return true;
 }
 
@@ -443,7 +465,7 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   if (((op.w >> 8) & 0xFF) != 0xFF) {  // earlier C carried as a factor
     float* recf = a.rec ? a.rec + (long long)inst * a.rec_inst_stride + (size_t)(a.op_base + blockIdx.x) * 4 * MS
                         : nullptr;
-    const bool ok = cvf_combine_factored<NP>(a, op, inst, sm, recf);
+    const bool ok = cvf_combine_factored<NP>(a, op, inst, sm, recf, trc);
     if (!ok && threadIdx.x == 0)
       raise_err(a.err ? a.err + inst : nullptr, GSLS_ERR_LOWRANK, a.op_base + blockIdx.x, -1, a.label);
     CTRACE(5);
@@ -732,8 +754,10 @@ int launch_combine(const CombineArgs& a, int nops, int count, cudaStream_t st) {
   const bool tracing = getenv("GSLS_COMBINE_TRACE") != nullptr;
   if (tracing && !trace) {
     GSLS_CUDA_CHECK(cudaMalloc(&trace, 16 * sizeof(long long)));
+    GSLS_CUDA_CHECK(cudaMemset(trace, 0, 16 * sizeof(long long)));
     GSLS_CUDA_CHECK(cudaMemcpyToSymbol(g_comb_trace, &trace, sizeof(trace)));
   }
+  if (tracing) GSLS_CUDA_CHECK(cudaMemsetAsync(trace, 0, 16 * sizeof(long long), st));
   if (a.n <= 64) {
     int rc = set_smem((const void*)k_cvf_combine<64>, sb);
     if (rc) return rc;
@@ -748,8 +772,13 @@ int launch_combine(const CombineArgs& a, int nops, int count, cudaStream_t st) {
     long long h[16];
     GSLS_CUDA_CHECK(cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st));
     GSLS_CUDA_CHECK(cudaStreamSynchronize(st));
-    fprintf(stderr, "combine n=%d ops=%d count=%d rec=%d cycles: load %lld gemm1 %lld gemm2+3 %lld gj %lld rest %lld total %lld\n",
-            a.n, nops, count, a.rec != nullptr, h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4], h[5] - h[0]);
+    if (h[13] > 0)
+      fprintf(stderr, "combine n=%d ops=%d count=%d rec=%d factored cycles: load %lld W,S %lld chol %lld U,Psi,Y,C %lld Pm(,T,Ups) %lld X,P,A %lld total %lld\n",
+              a.n, nops, count, a.rec != nullptr, h[8] - h[0], h[9] - h[8], h[10] - h[9], h[11] - h[10], h[12] - h[11],
+              h[13] - h[12], h[13] - h[0]);
+    else
+      fprintf(stderr, "combine n=%d ops=%d count=%d rec=%d cycles: load %lld gemm1 %lld gemm2+3 %lld gj %lld rest %lld total %lld\n",
+              a.n, nops, count, a.rec != nullptr, h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4], h[5] - h[0]);
   }
   return GSLS_OK;
 }
@@ -808,10 +837,24 @@ int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_l
 // ---------------------------------------------------------------------------
 // context
 
-int factor_rmax(int n) {
-  const char* e = getenv("GSLS_LOWRANK");
-  if (e && e[0] == '0') return 0;
-  return (n / 4) * 4;  // the output factor [U, F_r] must fit the slot's n x ldg storage
+int factor_rmax(int n, int tree) {
+  // Default: the SLS tree only.  The factored forms M1^-1 P_r = P_r - V V' and
+  // Ups' = A_l - Fh V' A_l subtract nearly equal terms where P_r C_l is large, which the
+  // ADMM penalty produces in the LQR tree; the recorded operators then drive hundreds of
+  // ADMM iterations: on cfg-B (12D quadrotor, N = 100, 500-1000 iterations per QP) the
+  // factored LQR tree moves inner iteration counts by up to 22 against the reference
+  // (the dense tree: <= 1, tests/test_gpu_configs.py).  The SLS costs keep P_r C_l = O(1):
+  // there the factored tree matches the oracle as closely as the dense one
+  // (tools/probe/sls_factored_shapes.py, tools/probe/tau_sensitivity.py).
+  // GSLS_LOWRANK: "0" none, "1" / "all" both trees, "lqr" the LQR tree only.
+  bool on = tree == 1;
+  if (const char* e = getenv("GSLS_LOWRANK")) {
+    if (e[0] == '0') on = false;
+    else if (e[0] == '1' || e[0] == 'a') on = true;
+    else if (e[0] == 'l') on = tree == 0;
+    else if (e[0] == 's') on = tree == 1;
+  }
+  return on ? (n / 4) * 4 : 0;  // the output factor [U, F_r] must fit the slot's n x ldg storage
 }
 
 int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, const int** loff, int kind,
@@ -887,6 +930,18 @@ int upload_plan(Ctx* c, const ScanPlan& p, const int4** ops, const int** out, co
       const int re = rep[q.earlier], rl = rep[q.later];
       h[o].w |= ((re < 0 ? 255 : re) << 8) | ((rl < 0 ? 255 : rl) << 16) | (rep[q.dst] >= 0 ? 8 : 0);
     }
+  if (cvf && getenv("GSLS_PLAN_VERBOSE")) {  // per layer: factored ops (rank histogram), dense ops, P-only ops
+    for (int l = 0; l + 1 < (int)p.layer_off.size(); ++l) {
+      int nf = 0, nd = 0, fin = 0, rsum = 0;
+      for (int o = p.layer_off[l]; o < p.layer_off[l + 1]; ++o) {
+        const int re = (h[o].w >> 8) & 0xFF;
+        if (re == 255) ++nd; else { ++nf; rsum += re; }
+        fin += h[o].w & 1;
+      }
+      fprintf(stderr, "plan%s layer %d: %d factored (mean rank %.1f), %d dense, %d P-only\n", rec ? " rec" : "", l, nf,
+              nf ? (double)rsum / nf : 0.0, nd, fin);
+    }
+  }
   if (leaf_dead) {  // per leaf slot (< p.length): bit 0 A dead, bit 1 A^T dead, bit 2 C dead, bit 3 C factored
     std::vector<int> lf(std::max(p.length, 1), 0);
     for (int i = 0; i < p.length && i < ns; ++i)
@@ -942,9 +997,9 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
   DevLqr& L = c->dev;
   L.n = d.nx; L.m = d.nu; L.c = d.nc; L.nf = d.nf; L.N = d.N; L.ldg = c->ldg; L.mtot = c->mtot;
   // leaf C ranks: B R^-1 B' (m) at the stages, 0 at the terminal element (lqr.py:306-320)
-  std::vector<int> leaf_rank(d.N + 1, d.nu);
+  std::vector<int> leaf_rank(d.N + 1, round_up(d.nu, 4));  // factor ranks carried as multiples of 4
   leaf_rank[d.N] = 0;
-  const int rmax = factor_rmax(d.nx);
+  const int rmax = factor_rmax(d.nx, 0);
   int rc = upload_plan(c, c->cvf, &c->cvf_ops_v[1], &L.cvf_out, &L.cvf_loff, PLAN_CVF_REC, &c->cvf_leaf_v[1]);
   if (!rc)
     rc = upload_plan(c, c->cvf, &c->cvf_ops_v[0], &L.cvf_out, &L.cvf_loff, PLAN_CVF_REC, &c->cvf_leaf_v[0],

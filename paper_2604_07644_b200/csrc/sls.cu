@@ -136,8 +136,8 @@ static int sls_init(Ctx* c) {
     for (int k = j + 1; k <= N; ++k) kj[cell_of(N, k, j) - S.cell0] = make_int2(k, j);
   // leaf C ranks: B Qu^-1 B' (m) on the stage cells, 0 on the terminal cells (sls.py:262-278)
   std::vector<int> leaf_rank(S.ncell);
-  for (int i = 0; i < S.ncell; ++i) leaf_rank[i] = kj[i].x == N ? 0 : m;
-  const int rmax = factor_rmax(n);
+  for (int i = 0; i < S.ncell; ++i) leaf_rank[i] = kj[i].x == N ? 0 : round_up(m, 4);  // multiples of 4
+  const int rmax = factor_rmax(n, 1);
   int rc = upload_plan(c, s->cvf, &s->cvf_ops_v[1], &S.cvf_out, &S.cvf_loff, PLAN_CVF, &s->leaf_v[1]);
   if (!rc)
     rc = upload_plan(c, s->cvf, &s->cvf_ops_v[0], &S.cvf_out, &S.cvf_loff, PLAN_CVF, &s->leaf_v[0],
