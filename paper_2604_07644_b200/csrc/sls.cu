@@ -321,24 +321,27 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
       raise_err(S.err + inst, GSLS_ERR_SINGULAR_STAGE, k, j, GSLS_LABEL_QU);
   }
   __syncthreads();
+  const int dead = S.leaf_dead[cell];  // parts of this leaf no combine reads (scan-plan analysis)
+  // C = B Qu^-1 B' is stored as the factor F = B L^-T (Qu = L L', L^-1 left in the
+  // inverse's work area) when the plan carries it factored (lowrank.cuh): BQT then
+  // holds F' = L^-1 B' instead of (B Qu^-1)'
+  const bool cfac = (dead & 8) != 0;
+  const double* Linv = wk + kMaxM * (kMaxM + 1);
   for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
     const int a = e / np, i = e - a * np;
     double s1 = 0.0, s2 = 0.0;
     for (int b2 = 0; b2 < m; ++b2) {
       const double qi = Qi[b2 * m + a];  // Qi symmetric in exact arithmetic; use Qi^T consistently
       s1 = fma(qi, Qux[b2 * np + i], s1);
-      s2 = fma(qi, BT[b2 * np + i], s2);
+      if (!cfac) s2 = fma(qi, BT[b2 * np + i], s2);
     }
+    if (cfac)
+      for (int b2 = 0; b2 <= a; ++b2) s2 = fma(Linv[a * (kMaxM + 1) + b2], BT[b2 * np + i], s2);
     QQ[e] = s1;
     BQT[e] = s2;
   }
   __syncthreads();
   const float* Ak = qp.A + st * n * n;
-  const int dead = S.leaf_dead[cell];  // parts of this leaf no combine reads (scan-plan analysis)
-  // C = B Qu^-1 B' stored as the factor B L^-T (Qu = L L', L^-1 left in the inverse's
-  // work area) when the plan carries it factored (lowrank.cuh)
-  const bool cfac = (dead & 8) != 0;
-  const double* Linv = wk + kMaxM * (kMaxM + 1);
   const int q4 = np >> 2;
   for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
     const int i = e / q4, j0 = (e - i * q4) << 2;
@@ -354,7 +357,7 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
       for (int t = 0; t < 4; ++t) {
         p4[t] = fma(qx, qq[t], p4[t]);
         a4[t] = fma(bt, qq[t], a4[t]);
-        c4[t] = fma(bq, bb[t], c4[t]);
+        if (!cfac) c4[t] = fma(bq, bb[t], c4[t]);
       }
     }
     float po[4], ao[4], co[4];
@@ -365,12 +368,7 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
       po[t] = in ? (float)(Qx[i * n + jj] - p4[t]) : 0.f;
       ao[t] = in ? (float)((double)Ak[i * n + jj] - a4[t]) : 0.f;
       co[t] = in ? (float)c4[t] : 0.f;
-      if (cfac) {
-        double f = 0.0;
-        if (jj < m)
-          for (int b = 0; b <= jj; ++b) f = fma(BT[b * np + i], Linv[jj * (kMaxM + 1) + b], f);
-        co[t] = (float)f;
-      }
+      if (cfac) co[t] = jj < m ? (float)BQT[jj * np + i] : 0.f;
       if (in && !(dead & 2)) ATd[(size_t)jj * ldg + i] = ao[t];
     }
     *reinterpret_cast<float4*>(Pd + (size_t)i * ldg + j0) = make_float4(po[0], po[1], po[2], po[3]);
