@@ -122,6 +122,21 @@ def flops_cvf(n):
     return 50.0 / 3.0 * n ** 3          # 16 2/3 n^3 per CVF combine (matrix part)
 
 
+def flops_build(n, m, N):
+    """SURVEY §8d F_build: one LQR cache build (CVF tree + COT tree + per-stage gains)."""
+    return (W(N + 1) * (50.0 / 3.0 * n ** 3 + 8 * n * n) + W(N) * (2 * n ** 3 + 2 * n * n)
+            + N * (14 * n * n * m + 8 * n * m * m + 2 * m ** 3))
+
+
+def flops_sls(n, m, c, nf, N):
+    """SURVEY §8d F_SLS: one SLS synthesis + tightening (N(N-1) CVF combines at 18 2/3 n^3 with
+    the gains / closed loop, per-cell costs and row norms)."""
+    V = N * (N - 1) / 2
+    return (N * (N - 1) * 56.0 / 3.0 * n ** 3
+            + V * (2 * m ** 3 + 16 * n * n * m + 10 * n * m * m + 2 * m * n * n + 2 * c * (2 * n * n + m * m + 2 * n * m))
+            + 4 * N * nf * n * n)
+
+
 def bytes_replay_iter(n, m, c, nf, N):
     """SURVEY §8d B_iter: algorithmic bytes of one cached ADMM iteration (fp32 convention)."""
     return 4 * (4 * n * n * W(N + 1) + n * n * W(N) + N * (n * n + 2 * m * m + 3 * n * m + 2 * c * (n + m) + 5 * n
@@ -302,6 +317,196 @@ def latency(tag, steps=30, warmup=5):
             "e2e_p50": statistics.median(e2e), "phases_ms": phases}
 
 
+PHASE_GROUPS = {"sls": ("sls_assemble", "sls_leaf", "sls_cvf", "sls_gains", "sls_matprod", "sls_phiu", "sls_rownorm",
+                         "sls_small"),
+                "build": ("leaf", "cvf_lqr", "gains", "cot"),
+                "replay": ("replay",),
+                "other": ("linearize", "rti_misc")}
+
+
+def serialized_phases(eng, step, nat, lib, steps=2):
+    """Per-family device time of the batched step with both overlaps off (the SLS / first-build
+    side stream and the ADMM driver's rebuild side stream), so the families add up to the
+    serialized step; returns (families, serialized ms per step, builds per step)."""
+    import torch
+    ov = eng.overlap
+    eng.overlap = False
+    os.environ["GSLS_ADMM_SERIAL"] = "1"
+    try:
+        step()
+        torch.cuda.synchronize()
+        lib.gsls_prof_enable(1)
+        lib.gsls_prof_read(None, None, None, 0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        builds = 0
+        e0.record()
+        for _ in range(steps):
+            step()
+            builds += int(eng.stats.cache_builds.sum())
+        e1.record()
+        torch.cuda.synchronize()
+        lib.gsls_prof_enable(0)
+    finally:
+        eng.overlap = ov
+        os.environ.pop("GSLS_ADMM_SERIAL", None)
+    nfam = len(nat.PROF_FAMILIES)
+    pm, pu_, pl = np.zeros(nfam), np.zeros(nfam), np.zeros(nfam, np.int64)
+    lib.gsls_prof_read(pm.ctypes.data, pu_.ctypes.data, pl.ctypes.data, nfam)
+    fam = {k: (float(t) / steps, int(c) // steps) for k, t, c in zip(nat.PROF_FAMILIES, pm, pl) if c}
+    return fam, e0.elapsed_time(e1) / steps, builds / steps
+
+
+def phase_rooflines(fam, B, dims, iters_per_step, builds_per_step, fp32_peak, hbm_peak):
+    """SURVEY §8d per-phase rooflines on the serialized family times: SLS and LQR-build flop
+    against the FP32-SIMT peak, the cached ADMM iterations' bytes against HBM, and the
+    time-weighted whole-step fraction (the 'other' phases count with fraction 0)."""
+    n, m, c, nf, N = dims
+    out, tw, tt = {}, 0.0, 0.0
+    for ph, fams in PHASE_GROUPS.items():
+        t = sum(fam[f][0] for f in fams if f in fam)
+        if t <= 0:
+            continue
+        if ph == "sls":
+            work, unit, peak, bound = flops_sls(n, m, c, nf, N) * B / 1e12, "TFLOP/s", fp32_peak, "fp32-simt"
+        elif ph == "build":
+            work, unit, peak, bound = flops_build(n, m, N) * builds_per_step / 1e12, "TFLOP/s", fp32_peak, "fp32-simt"
+        elif ph == "replay":
+            work, unit, peak, bound = bytes_replay_iter(n, m, c, nf, N) * iters_per_step / 1e9, "GB/s", hbm_peak, "hbm"
+        else:
+            work, unit, peak, bound = None, None, None, "latency"
+        ach = work / (t / 1e3) if work is not None else None
+        frac = ach / peak if ach is not None else 0.0
+        out[ph] = {"ms_per_step": t, "bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": frac,
+                   "families": {f: {"ms": fam[f][0], "launches": fam[f][1]} for f in fams if f in fam}}
+        tw += t * frac
+        tt += t
+    out["time_weighted_frac"] = tw / tt if tt else None
+    return out
+
+
+def receding_horizon(tag, steps=200, warmup=10, seed=0):
+    """Closed-loop MPC at batch 1: each robust RTI step's u0 drives the plant (model.step plus a
+    bounded disturbance E w, |w| <= 1), the next step warm-starts from the shifted plan and the
+    engine-held duals.  Device time per step (CUDA events around RtiEngine.step) and the loop's
+    wall time per step (incl. the u0 read-back and the host plant step)."""
+    import torch
+    from paper_2604_07644_b200 import scenarios
+    from paper_2604_07644_b200.engine import RtiEngine
+    from paper_2604_07644_b200.sls import ragged_to_cells
+    wl = scenarios.rti_workload(tag)
+    m = wl.model
+    eng = RtiEngine(m, wl.N, 1, scenarios.our_settings()(m))
+    d = lambda a: torch.as_tensor(np.asarray(a), dtype=torch.float64, device="cuda").contiguous()  # noqa: E731
+    rng = np.random.default_rng(seed)
+    x = np.array(wl.xbar0, float)
+    px, pu = d(wl.prev_x[None]), d(wl.prev_u[None])
+    tc, tt = d(ragged_to_cells(wl.tau, wl.N, (m.nc,))[None]), d(wl.tau_term[None])
+    dev_ms, wall_ms, its = [], [], []
+    done = 0
+    try:
+        for k in range(warmup + steps):
+            t0 = time.perf_counter()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            xb = d(x[None])
+            e0.record()
+            if k == 0:
+                eng.step(xb, px, pu, tau=tc, tau_term=tt)
+            else:
+                eng.step(xb, px, pu)
+            e1.record()
+            u0 = eng.u0[0].cpu().numpy()
+            w = rng.standard_normal(m.nx)
+            w *= rng.random() ** (1.0 / m.nx) / np.linalg.norm(w)
+            x = np.asarray(m.step(x, u0), float) + np.asarray(m.disturbance(x), float) @ w
+            px, pu = eng.warm_x.clone(), eng.warm_u.clone()
+            if k >= warmup:
+                dev_ms.append(e0.elapsed_time(e1))
+                wall_ms.append(1e3 * (time.perf_counter() - t0))
+                its.append(int(eng.stats.iterations[0]))
+            done = k + 1
+            if not np.all(np.isfinite(x)):
+                break
+    except Exception as exc:  # noqa: BLE001 - reported, not hidden
+        return {"error": f"{type(exc).__name__}: {exc}", "steps_done": done}
+    if not dev_ms:
+        return {"error": "no timed steps", "steps_done": done}
+    return {"steps": len(dev_ms), "device_ms_p50": statistics.median(dev_ms),
+            "device_ms_p90": float(np.percentile(dev_ms, 90)), "device_ms_max": max(dev_ms),
+            "loop_wall_ms_p50": statistics.median(wall_ms), "admm_iterations_mean": float(np.mean(its)),
+            "admm_iterations_max": int(max(its)),
+            "disturbance": "x+ = f(x, u0) + E(x) w, w uniform in the unit ball (seed 0)"}
+
+
+def cpu_latency(tag, steps=5, warmup=1):
+    """Single-process CPU latency of one robust RTI step: the oracle (float64 numpy, the
+    reference's algorithm) with numpy's BLAS threads on all host cores."""
+    import oracle
+    from paper_2604_07644_b200 import scenarios
+    wl = scenarios.rti_workload(tag)
+    m = wl.model
+    rs = oracle_settings(m)
+    tau = oracle.sls.Duals.zero(wl.N, m.nc, m.nf, rs.eps)
+    tau.tau, tau.tau_term = wl.tau, wl.tau_term
+    prev = oracle.sqp.Trajectory(wl.prev_x, wl.prev_u, m.dt)
+    times = []
+    for k in range(warmup + steps):
+        t = time.perf_counter()
+        oracle.sls.rti_robust_step(m, wl.xbar0, prev, tau, rs)
+        if k >= warmup:
+            times.append(1e3 * (time.perf_counter() - t))
+    return {"p50_ms": statistics.median(times), "p90_ms": float(np.percentile(times, 90)), "steps": steps,
+            "cores": os.cpu_count(), "kind": "port",
+            "threads": "one process; numpy BLAS on all host cores (the reference's own executor threads engage only "
+                       "at >= 64 combines per layer, scan.py:118-120)"}
+
+
+def config_lines(reps=2):
+    """BASELINE configs B, C, E through the drop-in API (host numpy in and out), wall ms."""
+    import torch
+    from paper_2604_07644_b200 import admm, scenarios as S, sls, sqp
+    out = {}
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            t = time.perf_counter()
+            r = fn()
+            torch.cuda.synchronize()
+            ts.append(1e3 * (time.perf_counter() - t))
+        return r, min(ts)
+    try:
+        m = S.cfgb_model()
+        x0 = S.quad12_start()
+        xg, ug = S.hover_guess(m, x0, S.CFGB["N"])
+        st = sqp.SqpSettings(admm=admm.AdmmSettings(**S.CFGB["admm"]), **S.CFGB["sqp"])
+        r, ms = timed(lambda: sqp.solve_nmpc(m, x0, st, sqp.Trajectory(xg, ug, m.dt)))
+        out["cfgB_solve_nmpc"] = {"ms": ms, "N": S.CFGB["N"], "nx": m.nx, "nu": m.nu, "sqp_iterations": r.stats.iterations,
+                                  "admm_iterations": r.stats.admm_iterations, "converged": bool(r.stats.converged)}
+        mc = S.cfgc_model()
+        xg, ug = S.hover_guess(mc, x0, S.CFGC["N"])
+        stc = sqp.SqpSettings(admm=admm.AdmmSettings(**S.CFGC["admm"]), **S.CFGC["sqp"])
+        rs = sls.RobustSettings(sqp=stc, weights=sls.SlsWeights.identity(mc.nx, mc.nu), eps=S.CFGC["eps"],
+                                tol_h=S.CFGC["tol_h"], max_alternations=S.CFGC["max_alternations"])
+        r, ms = timed(lambda: sls.solve_robust(mc, x0, rs, initial=sqp.Trajectory(xg, ug, mc.dt)))
+        out["cfgC_solve_robust"] = {"ms": ms, "N": S.CFGC["N"], "alternations": r.stats.alternations,
+                                    "sqp_iterations": r.stats.sqp_iterations, "converged": bool(r.stats.converged)}
+        me = S.cfge_model()
+        N = S.CFGE["N"]
+        x, u = S.cfge_trajectory(me, N)
+        qp = sqp.linearize(me, sqp.Trajectory(x, u, me.dt), None, S.cfge_start(me))
+        ste = admm.AdmmSettings(**S.CFGE["admm"])
+        r, ms = timed(lambda: admm.solve_qp(qp, ste))
+        out["cfgE_solve_qp"] = {"ms": ms, "N": N, "nx": me.nx, "nu": me.nu,
+                                "variables": (N + 1) * me.nx + N * me.nu, "constraints": N * qp.nc + qp.nf,
+                                "admm_iterations": r.stats.iterations, "cache_builds": r.stats.cache_builds,
+                                "converged": bool(r.stats.converged)}
+    except Exception as exc:  # noqa: BLE001 - reported, not hidden
+        out["error"] = f"{type(exc).__name__}: {exc}"
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -434,8 +639,7 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel family ------------------------------------
-    fam = dict(zip(nat.PROF_FAMILIES, zip(pm, pu_, pl)))
+    # ---- per-phase rooflines on a serialized pass (families add up to the step) ----------
     clk = clocks.summary()
     sm_max = clk["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
     # FP32-SIMT peak: measured on a B200 of this pool (tools/micro/fp32peak.cu, committed result);
@@ -447,30 +651,45 @@ def run_ours(args):
     except (OSError, ValueError, KeyError):
         fp32_peak, fp32_how = 148 * 128 * 2 * sm_max * 1e6 / 1e12, "derived: 148 SMs x 128 FP32 FMA/clk x 2 x max SM clock"
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    phases = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[2] / args.steps} for k, v in fam.items()
-              if v[2]}
     total_iters = float(its_all.sum())
-    rl = {}
+    iters_per_step = total_iters / args.steps
+    fam = dict(zip(nat.PROF_FAMILIES, zip(pm, pu_, pl)))  # timed loop: (ms, units, launches)
+    fam_s, ms_serial, builds_per_step = serialized_phases(eng, lambda: step(dev), nat, lib)
+    dims = (n, mu, c, nf, N)
+    rl_phase = phase_rooflines(fam_s, B, dims, iters_per_step, builds_per_step, fp32_peak, hbm_peak)
     tr = ncu_traffic()
+    rl = {}
     for k in ("sls_cvf", "cvf_lqr"):
-        t_ms, units, nl = fam[k]
-        if nl:
+        if k in fam_s:
+            t_ms, nl = fam_s[k]
+            units = fam[k][1] / args.steps  # combines per step (the timed loop's unit count)
             ach = units * flops_cvf(n) / (t_ms / 1e3) / 1e12
-            rl[k] = {"bound": "fp32-simt", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
-                     "frac": ach / fp32_peak, "traffic": (tr.get(k) or {}).get("dram_bytes"),
+            rl[k] = {"bound": "fp32-simt", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s", "frac": ach / fp32_peak,
+                     "ms_per_step": t_ms, "traffic": (tr.get(k) or {}).get("dram_bytes"),
                      "traffic_launch": (tr.get(k) or {}).get("launch")}
-    t_ms, units, nl = fam["replay"]
-    if nl:
-        ach = total_iters * bytes_replay_iter(n, mu, c, nf, N) / (t_ms / 1e3) / 1e9
+    if "replay" in fam_s:
+        t_ms, nl = fam_s["replay"]
+        ach = iters_per_step * bytes_replay_iter(n, mu, c, nf, N) / (t_ms / 1e3) / 1e9
         rl["replay"] = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-                        "traffic": (tr.get("replay") or {}).get("dram_bytes"),
+                        "ms_per_step": t_ms, "traffic": (tr.get("replay") or {}).get("dram_bytes"),
                         "traffic_launch": (tr.get("replay") or {}).get("launch")}
-    dom = max(fam, key=lambda k: fam[k][0])
+    dom = max(fam_s, key=lambda k: fam_s[k][0])
     roof = dict(rl.get(dom, {}), kernel=dom,
-                peak_source=fp32_how if dom in ("sls_cvf", "cvf_lqr") else
-                "MEASURED_PEAKS.json hbm_gbs",
+                peak_source=fp32_how if dom in ("sls_cvf", "cvf_lqr") else "MEASURED_PEAKS.json hbm_gbs",
                 work=("units = combines per launch x batch; 16 2/3 n^3 flop per combine (SURVEY §8d)"
-                      if dom in ("sls_cvf", "cvf_lqr") else "B_iter x ADMM iterations (SURVEY §8d)"))
+                      if dom in ("sls_cvf", "cvf_lqr") else "B_iter x ADMM iterations (SURVEY §8d)"),
+                timing="serialized pass (side streams off), CUDA events per kernel family")
+    phases = {"serialized_ms_per_step": ms_serial, "families_sum_ms": sum(v[0] for v in fam_s.values()),
+              "overlapped_ms_per_step": ms_max / args.steps,
+              "families": {k: {"ms_per_step": v[0], "launches_per_step": v[1]} for k, v in fam_s.items()},
+              "lqr_builds_per_step": builds_per_step}
+
+    # ---- closed-loop latency, configs B / C / E ----------------------------------------
+    rh = {}
+    if not args.no_latency:
+        for tag in ("q61", "h75"):
+            rh[tag] = receding_horizon(tag, steps=args.rh_steps)
+    cfg_lines = config_lines() if not args.no_latency else {}
 
     # ---- CPU baseline (rank 0, N=1 only) -----------------------------------------
     cpu = None
@@ -485,6 +704,7 @@ def run_ours(args):
         cpu = {"value": len(res) / dt, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{cores} q61 scenarios, one oracle rti_robust_step each (single-threaded numpy per core)"}
         parity = parity_block(eng, res)
+        cpu["latency_q61"] = cpu_latency("q61")
 
     launches = int(pl.sum())
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -498,7 +718,8 @@ def run_ours(args):
            "latency_phases_ms": {k: v["phases_ms"] for k, v in lat.items()},
            "admm_iterations_mean": total_iters / its_all.numel(),
            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
-           "gpu_launches": launches, "roofline": roof, "roofline_by_kernel": rl, "phases": phases,
+           "gpu_launches": launches, "roofline": roof, "roofline_by_kernel": rl, "roofline_by_phase": rl_phase,
+           "phases": phases, "receding_horizon_b1": rh, "configs_drop_in": cfg_lines,
            "rollout": rollout_line,
            "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
            "cpu_baseline": cpu, "parity": parity}
@@ -516,6 +737,7 @@ def main():
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--rh-steps", type=int, default=200)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

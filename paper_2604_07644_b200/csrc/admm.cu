@@ -1770,6 +1770,10 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
   int cap = (B > sms) ? s->sigma : 0;
   if (capenv) cap = atoi(capenv);
   const bool verbose = getenv("GSLS_ADMM_VERBOSE") != nullptr;  // per-wave timing (diagnostics)
+  // GSLS_ADMM_SERIAL=1: rebuild waves on the calling stream before the replay of every live
+  // instance (no side-stream overlap), so per-family device times add up (bench phases)
+  const char* serenv = getenv("GSLS_ADMM_SERIAL");
+  const bool serial = serenv && serenv[0] == '1';
   cudaEvent_t ev[3] = {};
   if (verbose) for (auto& e : ev) cudaEventCreate(&e);
   int wave = 0;
@@ -1799,7 +1803,7 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
       for (int i : rebuild) builds[i]++;
       prebuilt = false;
       rc = replay_wave(list, c->d_inst_list, st);
-    } else if (nreb == cnt) {  // every live instance needs its (first or re-) build
+    } else if (nreb == cnt || serial) {  // every live instance needs its (first or re-) build
       GSLS_CUDA_CHECK(cudaMemcpyAsync(c->d_build_list, rebuild.data(), sizeof(int) * nreb, cudaMemcpyHostToDevice, st));
       if ((rc = build_cache(c, qp, state->rho, c->d_build_list, nreb, st))) return rc;
       for (int i : rebuild) builds[i]++;
