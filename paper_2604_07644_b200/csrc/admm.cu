@@ -21,6 +21,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "ctx.h"
 #include "prof.h"
 #include "cluster.cuh"
@@ -29,6 +31,17 @@ namespace gsls {
 
 int check_errors(Ctx* c, cudaStream_t st, const char* what);
 void set_error(int code, int inst, int where, int aux, int label, const char* msg);
+
+// Whole-GPU replay of ONE large instance (vectors too large for shared memory, e.g.
+// cfg-E: 75D, N = 2047): the instance's vectors live once in global memory (L2) and
+// every CTA of a cooperative grid owns a share of each phase, exactly as the ranks
+// of a cluster do; puts are plain global stores and phases end with a grid barrier.
+struct GridCl {
+  unsigned rank, cs;
+  __device__ void put(double* p, double v) const { *p = v; }
+  __device__ void put_mask(double* p, double v, unsigned) const { *p = v; }
+  __device__ void sync() const { cooperative_groups::this_grid().sync(); }
+};
 
 enum { MODE_LQR = 0, MODE_ADMM = 1 };
 enum { ST_DONE = 0, ST_REBUILD = 1, ST_CONTINUE = 2, ST_BUILD_ERR = 3 };  // per-instance exit status of a replay launch
@@ -346,8 +359,8 @@ __device__ inline unsigned long long gtimer() {
   return t;
 }
 
-template <class Desc>
-__device__ void mv_round(int ntask, int n, int ldg, double* part, const Cl& cl, Desc desc,
+template <class Comm, class Desc>
+__device__ void mv_round(int ntask, int n, int ldg, double* part, const Comm& cl, Desc desc,
                          unsigned long long* dbg = nullptr) {
   auto D = [&](int j) { if (dbg && threadIdx.x == 0) dbg[j] = clock64(); };
   D(0);
@@ -433,29 +446,35 @@ __device__ inline void gdotc(int cs, int total, int len, int gt, int gs, Term te
   else gdot<G>(total, len, gt, gs, term, out);
 }
 
+// GRID: one instance over a cooperative grid (GridCl, rank = blockIdx.x); otherwise one
+// instance per cluster (Cl, rank = cluster rank), blockIdx.y = instance.
+template <bool GRID>
 __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
+  using Comm = typename std::conditional<GRID, GridCl, Cl>::type;
   const DevLqr& L = a.L;
   const int inst = a.list ? a.list[blockIdx.y] : (int)blockIdx.y;
   if (a.mode == MODE_ADMM && L.err[inst].key != 0) {  // its (re)build raised: the host driver decides
-    if (cluster_rank() == 0 && threadIdx.x == 0) a.status[inst] = ST_BUILD_ERR;
+    if ((GRID ? blockIdx.x : cluster_rank()) == 0 && threadIdx.x == 0) a.status[inst] = ST_BUILD_ERR;
     return;
   }
   const int n = L.n, m = L.m, c = L.c, nf = L.nf, N = L.N, ldg = L.ldg, mtot = L.mtot;
   const size_t MS = (size_t)n * ldg;
   const int tid = threadIdx.x, nthr = blockDim.x;
-  Cl cl;
-  cl.rank = cluster_rank();
-  cl.cs = cluster_size();
+  Comm cl;
+  cl.rank = GRID ? blockIdx.x : cluster_rank();
+  cl.cs = GRID ? gridDim.x : cluster_size();
   const int rank = (int)cl.rank, cs = (int)cl.cs;
-  const int gt = rank * nthr + tid, gs = cs * nthr;  // cluster-wide thread index / stride
+  const int gt = rank * nthr + tid, gs = cs * nthr;  // cluster- (grid-) wide thread index / stride
   const VecLayout V = vec_layout(n, m, N, mtot, L.cvf_nslots, L.cot_nslots, a.max_layer, L.cvf_nops, L.cot_nops,
                                  L.cvf_layers, L.cot_layers);
   extern __shared__ double smem[];
   double* vs = a.gscratch ? a.gscratch + (size_t)inst * a.scratch_floats : smem;
   double *pv = vs + V.pv, *bv = vs + V.bv, *cb = vs + V.cb;
   double *z = vs + V.z, *lam = vs + V.lam, *y = vs + V.y;
-  double *rhat = vs + V.rhat, *om = vs + V.om, *kf = vs + V.kf, *du = vs + V.du, *red = vs + V.red;
-  double *part = vs + V.part, *redall = vs + V.redall;
+  double *rhat = vs + V.rhat, *om = vs + V.om, *kf = vs + V.kf, *du = vs + V.du;
+  double *red = GRID ? smem : vs + V.red;                   // per-CTA scratch
+  double *part = GRID ? smem + 64 : vs + V.part;            // per-CTA split-K partials
+  double* redall = vs + V.redall;
   __shared__ int s_flag;  // 0 continue, 1 done, 2 rebuild
   __shared__ double s_rho;
 
@@ -484,19 +503,30 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
   const int warp = tid >> 5, lane = tid & 31, nwarp = nthr >> 5;
 
   double* w = vs + V.w;
-  // the scan plans, copied to shared memory (every op / layer lookup is on a phase's critical path)
-  int4* s_cvf_ops = reinterpret_cast<int4*>(vs + V.plan);
-  int4* s_cot_ops = s_cvf_ops + L.cvf_nops;
-  int* s_cvf_loff = reinterpret_cast<int*>(s_cot_ops + L.cot_nops);
-  int* s_cot_loff = s_cvf_loff + L.cvf_layers + 1;
-  int* s_cvf_out = s_cot_loff + L.cot_layers + 1;
-  int* s_cot_out = s_cvf_out + N + 1;
-  for (int i = tid; i < L.cvf_nops; i += nthr) s_cvf_ops[i] = L.cvf_ops[i];
-  for (int i = tid; i < L.cot_nops; i += nthr) s_cot_ops[i] = L.cot_ops[i];
-  for (int i = tid; i <= L.cvf_layers; i += nthr) s_cvf_loff[i] = L.cvf_loff[i];
-  for (int i = tid; i <= L.cot_layers; i += nthr) s_cot_loff[i] = (N > 0) ? L.cot_loff[i] : 0;
-  for (int i = tid; i <= N; i += nthr) s_cvf_out[i] = L.cvf_out[i];
-  for (int i = tid; i < N; i += nthr) s_cot_out[i] = L.cot_out[i];
+  // the scan plans, copied to shared memory (every op / layer lookup is on a phase's critical
+  // path); a GRID launch (one large instance) reads them from global memory instead
+  const int4* s_cvf_ops = L.cvf_ops;
+  const int4* s_cot_ops = L.cot_ops;
+  const int* s_cvf_loff = L.cvf_loff;
+  const int* s_cot_loff = L.cot_loff;
+  const int* s_cvf_out = L.cvf_out;
+  const int* s_cot_out = L.cot_out;
+  if (!GRID) {
+    int4* p_cvf_ops = reinterpret_cast<int4*>(vs + V.plan);
+    int4* p_cot_ops = p_cvf_ops + L.cvf_nops;
+    int* p_cvf_loff = reinterpret_cast<int*>(p_cot_ops + L.cot_nops);
+    int* p_cot_loff = p_cvf_loff + L.cvf_layers + 1;
+    int* p_cvf_out = p_cot_loff + L.cot_layers + 1;
+    int* p_cot_out = p_cvf_out + N + 1;
+    for (int i = tid; i < L.cvf_nops; i += nthr) p_cvf_ops[i] = L.cvf_ops[i];
+    for (int i = tid; i < L.cot_nops; i += nthr) p_cot_ops[i] = L.cot_ops[i];
+    for (int i = tid; i <= L.cvf_layers; i += nthr) p_cvf_loff[i] = L.cvf_loff[i];
+    for (int i = tid; i <= L.cot_layers; i += nthr) p_cot_loff[i] = (N > 0) ? L.cot_loff[i] : 0;
+    for (int i = tid; i <= N; i += nthr) p_cvf_out[i] = L.cvf_out[i];
+    for (int i = tid; i < N; i += nthr) p_cot_out[i] = L.cot_out[i];
+    s_cvf_ops = p_cvf_ops; s_cot_ops = p_cot_ops; s_cvf_loff = p_cvf_loff; s_cot_loff = p_cot_loff;
+    s_cvf_out = p_cvf_out; s_cot_out = p_cot_out;
+  }
   __syncthreads();
   // dx_k lives in the COT outputs (k >= 1) or dx0
   auto dxp = [&](int k) -> const double* { return k == 0 ? dx0 : cb + (size_t)s_cot_out[k - 1] * n; };
@@ -510,7 +540,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
     const double* zg = a.state.z + (size_t)inst * mtot;
     const double* lg = a.state.lam + (size_t)inst * mtot;
     const double* yg = a.state.y + (size_t)inst * mtot;
-    for (int e = tid; e < mtot; e += nthr) {
+    for (int e = GRID ? gt : tid; e < mtot; e += GRID ? gs : nthr) {  // GRID: shared copy, one writer
       z[e] = zg[e]; lam[e] = lg[e]; y[e] = yg[e];
       w[e] = yg[e] - zg[e];
     }
@@ -522,9 +552,10 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
   unsigned* cvf_mask = reinterpret_cast<unsigned*>(vs + V.masks);
   unsigned* cot_mask = cvf_mask + L.cvf_nslots;
   auto srank = [&](int k) { return k % cs; };
-  for (int i = tid; i < L.cvf_nslots + L.cot_nslots; i += nthr) cvf_mask[i] = 0u;
+  if (!GRID)
+    for (int i = tid; i < L.cvf_nslots + L.cot_nslots; i += nthr) cvf_mask[i] = 0u;
   __syncthreads();
-  if (cs > 1) {
+  if (!GRID && cs > 1) {
     for (int lay = 0; lay < L.cvf_layers; ++lay) {  // half-ops (p, b) h = 2 oi + which on rank h / per
       const int o0 = s_cvf_loff[lay], nh = 2 * (s_cvf_loff[lay + 1] - o0), per = (nh + cs - 1) / cs;
       for (int h = tid; h < nh; h += nthr) {
@@ -1547,28 +1578,45 @@ static int launch_replay(Ctx* c, ReplayArgs& a, int count, cudaStream_t st) {
   }
   static bool attrs_set = false;
   if (!attrs_set) {
-    GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_replay<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(kReplaySmemMax)));
-    GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_replay, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attrs_set = true;
   }
-  // One CTA per instance.  Cluster launches of the ADMM loop go to k_admm_staged; this
-  // kernel's cluster mode (DSMEM replicas) is kept for GSLS_REPLAY_CLUSTER experiments only:
-  // it reproduces the reference at cs <= 2 but not at cs >= 4 (open issue).
-  const char* force_cs = getenv("GSLS_REPLAY_LEGACY_CLUSTER");
-  const int cs = (a.mode == MODE_ADMM && force_cs) ? replay_cluster(c, count, sb, (const void*)k_replay) : 1;
+  // Vectors too large for shared memory (long horizons, e.g. cfg-E at N = 2047): each
+  // instance runs over the whole GPU as a cooperative grid (k_replay<true>), instances in
+  // turn.  GSLS_REPLAY_GRID=0 keeps one CTA per instance (diagnostics).
+  const char* genv = getenv("GSLS_REPLAY_GRID");
+  if (c->d_scratch && !(genv && genv[0] == '0')) {
+    const size_t gsb = (64 + kReplayThreads) * sizeof(double);
+    static int per_sm = 0, sms = 0;
+    if (!per_sm) {
+      int dev = 0;
+      GSLS_CUDA_CHECK(cudaGetDevice(&dev));
+      GSLS_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      GSLS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_replay<true>, kReplayThreads, gsb));
+      if (per_sm < 1) per_sm = 1;
+    }
+    const int grid = per_sm * sms;
+    ProfScope ps(P_REPLAY, st, (double)count);
+    for (int i = 0; i < count; ++i) {
+      ReplayArgs ai = a;
+      ai.list = (a.list ? a.list : c->d_inst_all) + i;
+      ai.trace = nullptr;
+      void* args[] = {&ai};
+      GSLS_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_replay<true>, dim3(grid, 1), dim3(kReplayThreads), args,
+                                                  gsb, st));
+    }
+    GSLS_CUDA_CHECK(cudaGetLastError());
+    return GSLS_OK;
+  }
+  // One CTA per instance (cluster launches of the ADMM loop go to k_admm_staged).
   cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.gridDim = dim3(cs, count);
+  cfg.gridDim = dim3(1, count);
   cfg.blockDim = dim3(kReplayThreads);
   cfg.dynamicSmemBytes = sb;
   cfg.stream = st;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.attrs = nullptr;
+  cfg.numAttrs = 0;
   static unsigned long long* trace = nullptr;
   const bool tracing = getenv("GSLS_REPLAY_TRACE") != nullptr;
   if (tracing && !trace) GSLS_CUDA_CHECK(cudaMalloc(&trace, 256 * sizeof(unsigned long long)));
@@ -1576,14 +1624,14 @@ static int launch_replay(Ctx* c, ReplayArgs& a, int count, cudaStream_t st) {
   if (tracing) GSLS_CUDA_CHECK(cudaMemsetAsync(trace, 0, 256 * sizeof(unsigned long long), st));
   {
     ProfScope ps(P_REPLAY, st, (double)count);
-    GSLS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_replay, a));
+    GSLS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_replay<false>, a));
     GSLS_CUDA_CHECK(cudaGetLastError());
   }
   if (tracing) {
     unsigned long long h[256];
     GSLS_CUDA_CHECK(cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st));
     GSLS_CUDA_CHECK(cudaStreamSynchronize(st));
-    fprintf(stderr, "replay trace cs=%d count=%d:", cs, count);
+    fprintf(stderr, "replay trace count=%d:", count);
     for (unsigned long long i = 2; i <= h[0]; ++i) fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
     fprintf(stderr, " | first iteration %.2f us | mv_round layer 3:", h[0] > 1 ? (h[h[0]] - h[1]) * 1e-3 : 0.0);
     for (int j = 1; j < 5; ++j) fprintf(stderr, " %llu", h[200 + j] - h[200 + j - 1]);
