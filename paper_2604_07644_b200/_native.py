@@ -18,6 +18,7 @@ c_void_p = ctypes.c_void_p
 
 # status codes (gsls_status_t)
 OK, ERR_ARG, ERR_CUDA, ERR_SINGULAR, ERR_ILL, ERR_CACHE, ERR_NONFINITE, ERR_TOO_LARGE, ERR_NO_DEVICE = range(9)
+ERR_LOWRANK = 9  # internal: a factored combine met an indefinite P; the scan re-runs dense (include/gsls.h)
 
 
 class Dims(ctypes.Structure):

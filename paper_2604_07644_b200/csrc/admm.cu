@@ -63,6 +63,7 @@ struct ReplayArgs {
   unsigned long long* trace;  // GSLS_REPLAY_TRACE: phase timestamps of the first iteration (rank 0)
   int prefetch;               // k_replay: bulk-prefetch the next tree layer's records into L2
   int cap;                    // ADMM: pause (ST_CONTINUE) an undecided instance at this iteration (0: none)
+  const int* count;           // device-side instance count (graph-captured loop); nullptr: grid-sized
 };
 
 constexpr int kReplayThreads = 512;
@@ -452,6 +453,7 @@ template <bool GRID>
 __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
   using Comm = typename std::conditional<GRID, GridCl, Cl>::type;
   const DevLqr& L = a.L;
+  if (!GRID && a.count && (int)blockIdx.y >= *a.count) return;
   const int inst = a.list ? a.list[blockIdx.y] : (int)blockIdx.y;
   if (a.mode == MODE_ADMM && L.err[inst].key != 0) {  // its (re)build raised: the host driver decides
     if ((GRID ? blockIdx.x : cluster_rank()) == 0 && threadIdx.x == 0) a.status[inst] = ST_BUILD_ERR;
@@ -1065,6 +1067,7 @@ struct ItemEpi {
 
 __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a, int R, int max_items) {
   const DevLqr& L = a.L;
+  if (a.count && (int)blockIdx.y >= *a.count) return;
   const int inst = a.list ? a.list[blockIdx.y] : (int)blockIdx.y;
   if (L.err[inst].key != 0) {  // its (re)build raised: the host driver decides
     if (cluster_rank() == 0 && threadIdx.x == 0) a.status[inst] = ST_BUILD_ERR;
@@ -1786,12 +1789,121 @@ int ctx_export(Ctx* c, float* K, double* k, float* P, double* p, cudaStream_t st
   return GSLS_OK;
 }
 
+// ---- graph-captured ADMM loop ---------------------------------------------------
+// Under stream capture (one MPC step recorded as a CUDA graph) the host-driven wave
+// loop below cannot run: it reads each wave's exit status back.  The captured form is a
+// conditional WHILE node whose body is [count builds | cache build of the build list |
+// replay of the live list | decide], all sized for the whole batch and guarded by the
+// device-side counts (d_counts[0] live, [1] build); `decide` keeps the instances that
+// committed a rho change, in index order, and re-arms the loop while any is left.
+__global__ void k_loop_init(int* live, int* build, int* counts, int B, int prebuilt, int32_t* cache_builds) {
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    live[i] = i;
+    build[i] = i;
+    cache_builds[i] = prebuilt ? 1 : 0;
+  }
+  if (threadIdx.x == 0) {
+    counts[0] = B;
+    counts[1] = prebuilt ? 0 : B;
+  }
+}
+
+__global__ void k_loop_count_builds(const int* build, const int* counts, int32_t* cache_builds) {
+  for (int i = threadIdx.x; i < counts[1]; i += blockDim.x) cache_builds[build[i]] += 1;
+}
+
+__global__ void k_loop_decide(const int32_t* status, int* live, int* build, int* counts,
+                              cudaGraphConditionalHandle h) {
+  if (threadIdx.x != 0) return;
+  int cnt = 0;
+  const int nl = counts[0];
+  for (int i = 0; i < nl; ++i) {
+    const int inst = live[i];
+    if (status[inst] == ST_REBUILD) build[cnt++] = inst;
+  }
+  for (int i = 0; i < cnt; ++i) live[i] = build[i];
+  counts[0] = cnt;
+  counts[1] = cnt;
+  cudaGraphSetConditional(h, cnt > 0 ? 1u : 0u);
+}
+
+static int admm_solve_captured(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_admm_state_t* state,
+                               gsls_admm_stats_t* stats, double* dx, double* du, cudaStream_t st) {
+  const int B = c->dims.batch;
+  if (c->d_scratch) {
+    set_error(GSLS_ERR_ARG, -1, 0, 0, 0, "graph capture needs the shared-memory replay (N too large)");
+    return GSLS_ERR_ARG;
+  }
+  GSLS_CUDA_CHECK(cudaMemsetAsync(stats->iterations, 0, sizeof(int32_t) * B, st));
+  GSLS_CUDA_CHECK(cudaMemsetAsync(stats->converged, 0, sizeof(int32_t) * B, st));
+  GSLS_CUDA_CHECK(cudaMemsetAsync(stats->rho_changes, 0, sizeof(int32_t) * B, st));
+  const bool prebuilt = c->admm_prebuilt;
+  c->admm_prebuilt = false;
+  c->cache_valid = false;
+  k_loop_init<<<1, 256, 0, st>>>(c->d_inst_list, c->d_build_list, c->d_counts, B, prebuilt ? 1 : 0,
+                                 stats->cache_builds);
+  GSLS_CUDA_CHECK(cudaGetLastError());
+  cudaStreamCaptureStatus cst;
+  cudaGraph_t graph = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  GSLS_CUDA_CHECK(cudaStreamGetCaptureInfo(st, &cst, nullptr, &graph, &deps, &ndeps));
+  cudaGraphConditionalHandle h;
+  GSLS_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  GSLS_CUDA_CHECK(cudaGraphAddNode(&node, graph, deps, ndeps, &cp));
+  GSLS_CUDA_CHECK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cudaStream_t bs = c->body_stream;
+  GSLS_CUDA_CHECK(cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  int rc = GSLS_OK;
+  k_loop_count_builds<<<1, 256, 0, bs>>>(c->d_build_list, c->d_counts, stats->cache_builds);
+  GSLS_CUDA_CHECK(cudaGetLastError());
+  c->dev.build_count = c->d_counts + 1;
+  rc = build_cache(c, qp, state->rho, c->d_build_list, B, bs);
+  c->dev.build_count = nullptr;
+  if (!rc) {
+    ReplayArgs a{};
+    a.qp = *qp;
+    a.mode = MODE_ADMM;
+    a.set = *s;
+    a.state = *state;
+    a.stats = *stats;
+    a.status = c->d_status;
+    a.dx = dx; a.du = du;
+    a.list = c->d_inst_list;
+    a.count = c->d_counts;
+    a.cap = 0;
+    rc = launch_admm_staged(c, a, B, bs);
+    if (rc == GSLS_ERR_TOO_LARGE) rc = launch_replay(c, a, B, bs);
+  }
+  if (!rc) {
+    k_loop_decide<<<1, 32, 0, bs>>>(c->d_status, c->d_inst_list, c->d_build_list, c->d_counts, h);
+    if (cudaGetLastError() != cudaSuccess) rc = GSLS_ERR_CUDA;
+  }
+  cudaGraph_t done = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(bs, &done);
+  if (rc) return rc;
+  GSLS_CUDA_CHECK(ec);
+  return GSLS_OK;
+}
+
 int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_admm_state_t* state,
                gsls_admm_stats_t* stats, double* dx, double* du, cudaStream_t st) {
   const int B = c->dims.batch;
   if (s->sigma < 2 || s->max_iter < 1 || !(s->rho0 > 0) || !(s->tol_primal > 0) || !(s->tol_dual > 0)) {
     set_error(GSLS_ERR_ARG, -1, 0, 0, 0, "invalid ADMM settings");
     return GSLS_ERR_ARG;
+  }
+  {
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    GSLS_CUDA_CHECK(cudaStreamIsCapturing(st, &cst));
+    if (cst == cudaStreamCaptureStatusActive) return admm_solve_captured(c, qp, s, state, stats, dx, du, st);
   }
   GSLS_CUDA_CHECK(cudaMemsetAsync(stats->iterations, 0, sizeof(int32_t) * B, st));
   GSLS_CUDA_CHECK(cudaMemsetAsync(stats->converged, 0, sizeof(int32_t) * B, st));

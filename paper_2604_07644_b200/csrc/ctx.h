@@ -56,6 +56,9 @@ struct DevLqr {
   int cvf_nphys, cot_nphys;
   double *pb0, *kk0;
   ErrSlot* err;          // [batch]
+  // device-side instance count of a build launched over the whole batch (graph-captured
+  // ADMM loop): CTAs with blockIdx.y >= *build_count exit at once; nullptr: host-sized grid
+  const int* build_count;
 };
 
 struct Ctx {
@@ -75,6 +78,8 @@ struct Ctx {
   cudaStream_t side = nullptr;  // ADMM driver: rebuild + replay of the rebuilt instances, beside the others
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int32_t* d_status = nullptr; // [batch] per-instance ADMM exit status
+  int* d_counts = nullptr;     // [2] graph-captured ADMM loop: replay / build instance counts
+  cudaStream_t body_stream = nullptr;  // capture stream of the captured loop's body graph
   double* d_scratch = nullptr; // global fallback for replay vectors
   size_t scratch_floats = 0;   // per instance (doubles)
   int generation = -1;         // cache stamp (single-generation API); -1 = none
@@ -105,6 +110,7 @@ struct CombineArgs {
   ErrSlot* err;
   float rel_tol;
   int label;                   // GSLS_ERR_LOWRANK label: 0 LQR tree, 1 SLS tree
+  const int* count = nullptr;  // device-side instance count (graph-captured loop), see DevLqr
 };
 int launch_combine(const CombineArgs& a, int nops, int count, cudaStream_t st);
 int combine_threads(int n);

@@ -133,6 +133,7 @@ __device__ inline int inst_of(const int* list) { return list ? list[blockIdx.y] 
 // terms; only the result is rounded to the float32 scan storage.
 __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const double* rho_arr,
                                                    const int* list) {
+  if (L.build_count && (int)blockIdx.y >= *L.build_count) return;
   const int inst = inst_of(list);
   const int k = blockIdx.x;
   const int n = L.n, m = L.m, c = L.c, nf = L.nf, N = L.N, ldg = L.ldg;
@@ -456,6 +457,7 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   long long* trc = (g_comb_trace && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == gridDim.y / 2) ? g_comb_trace : nullptr;
 #define CTRACE(i) do { if (trc) trc[i] = clock64(); } while (0)
   CTRACE(0);
+  if (a.count && (int)blockIdx.y >= *a.count) return;
   const int inst = inst_of(a.list);
   const int4 op = a.ops[blockIdx.x];
   const int n = a.n, ldg = ldg_of(n), lds = gj_lds(NP, n);  // >= lds_of(n): the inverse's column tiles fit a row
@@ -561,6 +563,7 @@ int matmul_threads(int n) {
 
 // Gains, closed loop and COT leaves per stage (lqr.py:398-404, :349-356), in float64.
 __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const double* rho_arr, const int* list) {
+  if (L.build_count && (int)blockIdx.y >= *L.build_count) return;
   const int inst = inst_of(list);
   const int k = blockIdx.x;
   const int n = L.n, m = L.m, N = L.N, ldg = L.ldg, c = L.c;
@@ -708,6 +711,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
 
 // COT combine: A = A_later A_earlier (+ transpose); records A_later column-major.
 __global__ void __launch_bounds__(512) k_cot_combine(DevLqr L, const int4* ops, int op_base, const int* list) {
+  if (L.build_count && (int)blockIdx.y >= *L.build_count) return;
   const int inst = inst_of(list);
   const int4 op = ops[blockIdx.x];
   const int n = L.n, ldg = L.ldg, lds = lds_of(n);
@@ -802,7 +806,7 @@ int build_cache(Ctx* c, const gsls_qp_t* qp, const double* d_rho, const int* d_l
   for (int l = 0; l < c->cvf.layers; ++l) {
     const int o0 = c->cvf_layer_off[l], o1 = c->cvf_layer_off[l + 1];
     CombineArgs a{n, L.cvf_ops + o0, o0, L.Ps, L.As, L.Cs, L.ATs, (long long)L.cvf_nslots * (long long)MS,
-                  L.cvf_rec, (long long)L.cvf_nops * 4 * (long long)MS, d_list, L.err, 1e-10f, 0};
+                  L.cvf_rec, (long long)L.cvf_nops * 4 * (long long)MS, d_list, L.err, 1e-10f, 0, L.build_count};
     if (o1 == o0) continue;
     ProfScope ps(P_CVF_LQR, st, (double)(o1 - o0) * count);
     int rc = launch_combine(a, o1 - o0, count, st);
@@ -1059,11 +1063,13 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
   c->d_inst_list = (int*)dev_alloc(c, B * sizeof(int));
   c->d_build_list = (int*)dev_alloc(c, B * sizeof(int));
   c->d_status = (int32_t*)dev_alloc(c, B * sizeof(int32_t));
+  c->d_counts = (int*)dev_alloc(c, 4 * sizeof(int));
+  cudaStreamCreateWithFlags(&c->body_stream, cudaStreamNonBlocking);
   c->scratch_floats = replay_smem_floats(c);  // doubles
   if (c->scratch_floats * 8 > kReplaySmemMax) c->d_scratch = (double*)dev_alloc(c, B * c->scratch_floats * 8);
   bool fail = !L.Ps || !L.As || !L.Cs || !L.ATs || !L.cotAT || !L.cvf_rec || !L.cotA || !L.cot_rec || !L.Rhat || !L.Shat || !L.Shat64 || !L.Rinv ||
               !L.Gamma || !L.K || !L.cvec || !L.v0 || !L.last_k || !L.last_p || !L.err || !L.X23 || !L.pb0 || !L.XK || !L.kk0 ||
-              !L.Bcm || !L.ZD || !c->d_inst_all || !c->d_inst_list || !c->d_build_list || !c->d_status ||
+              !L.Bcm || !L.ZD || !c->d_inst_all || !c->d_inst_list || !c->d_build_list || !c->d_status || !c->d_counts ||
               (c->scratch_floats * 8 > kReplaySmemMax && !c->d_scratch);
   if (fail) {
     for (void* p : c->allocs) cudaFree(p);
@@ -1082,6 +1088,7 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
 void ctx_destroy(Ctx* c) {
   if (!c) return;
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->body_stream) cudaStreamDestroy(c->body_stream);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->sls) sls_destroy(c);

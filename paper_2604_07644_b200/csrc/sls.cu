@@ -790,6 +790,9 @@ static int sls_synthesize_once(Ctx* c, const gsls_qp_t* qp, const float* E, cuda
 int sls_synthesize(Ctx* c, const gsls_qp_t* qp, const float* E, cudaStream_t st, bool check) {
   int rc = sls_synthesize_once(c, qp, E, st);
   if (rc || !check) return rc;
+  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+  GSLS_CUDA_CHECK(cudaStreamIsCapturing(st, &cst));
+  if (cst != cudaStreamCaptureStatusNone) return GSLS_OK;  // captured step: errors are read after the graph
   rc = check_errors(c, st, "sls.synthesize");
   if (rc == GSLS_ERR_LOWRANK) {
     rc = sls_synthesize_once(c, qp, E, st);

@@ -147,6 +147,13 @@ class RtiEngine:
         (B,n), (B,N+1,n), (B,N,m); ``tau``/``tau_term`` (cell layout) override the
         engine-held duals; ``use_tau=False`` forces the unweighted synthesis."""
         ctx, lib, qp, S = self.ctx, self.ctx.lib, self.qp, stream_ptr()
+        n, m, c, nf, N = self.dims
+        for name, t, shape in (("xbar0", xbar0, (self.B, n)), ("prev_x", prev_x, (self.B, N + 1, n)),
+                               ("prev_u", prev_u, (self.B, N, m)), ("tau", tau, (self.B, self.ncell, c)),
+                               ("tau_term", tau_term, (self.B, N, nf))):
+            if t is not None and (tuple(t.shape) != shape or t.dtype != F64 or not t.is_cuda or not t.is_contiguous()):
+                raise ValueError(f"{name} must be a contiguous float64 CUDA tensor of shape {shape}, "
+                                 f"got {tuple(t.shape)} {t.dtype} contiguous={t.is_contiguous()}")
         qs = qp.cstruct()
         linearize_into(ctx, self.dm, qp, prev_x, prev_u, xbar0=xbar0, E=self.E,
                        write_weights=not self._weights_written)
@@ -198,6 +205,10 @@ class RtiEngine:
                   "rti_apply")
         return self
 
+    def capture(self, xbar0=None, prev_x=None, prev_u=None) -> "CapturedStep":
+        """Record one step of this engine as a CUDA graph (see CapturedStep)."""
+        return CapturedStep(self, xbar0, prev_x, prev_u)
+
     # -- views ---------------------------------------------------------------------
     def lam_split(self):
         n, m, c, nf, N = self.dims
@@ -213,3 +224,66 @@ class RtiEngine:
         nat.check(self.ctx.lib.gsls_sls_export(self.ctx.handle, phix.data_ptr(), phiu.data_ptr(),
                                                gains.data_ptr(), stream_ptr()), "sls export")
         return phix, phiu, gains
+
+
+class CapturedStep:
+    """One MPC step of an ``RtiEngine`` recorded as a single CUDA graph.
+
+    The graph holds the whole step: linearization, the SLS chain (and the ADMM's first
+    factorization on a forked branch), the ADMM QP as a conditional WHILE node over
+    [rebuild | persistent replay | decide] (csrc/admm.cu admm_solve_captured), duals and
+    the plan update.  A replay issues one graph launch and no host synchronization;
+    ``check()`` reads the error records afterwards (one D2H copy), raising as the eager
+    step would.  Inputs are copied into static device buffers; the engine-held duals
+    carry over between steps as in the eager receding-horizon loop.
+
+    A step whose factored SLS combine met an indefinite P (GSLS_ERR_LOWRANK) switched the
+    context to dense combines: the recorded graph is then stale, so ``check()`` re-runs the
+    step eagerly and re-records the graph.
+    """
+
+    def __init__(self, eng: RtiEngine, xbar0=None, prev_x=None, prev_u=None):
+        n, m, c, nf, N = eng.dims
+        dev = eng.qp.QN.device
+        self.eng = eng
+        z = lambda *s: torch.zeros(s, dtype=F64, device=dev)  # noqa: E731
+        self.xbar0, self.prev_x, self.prev_u = z(eng.B, n), z(eng.B, N + 1, n), z(eng.B, N, m)
+        if xbar0 is not None:
+            self._load(xbar0, prev_x, prev_u)
+        self._record()
+
+    def _load(self, xbar0, prev_x, prev_u):
+        self.xbar0.copy_(xbar0, non_blocking=True)
+        self.prev_x.copy_(prev_x, non_blocking=True)
+        self.prev_u.copy_(prev_u, non_blocking=True)
+
+    def _record(self):
+        eng = self.eng
+        if eng.robust and not eng.tau_valid:
+            raise RuntimeError("capture after one eager robust step (the duals tau must be valid)")
+        s = torch.cuda.Stream(device=self.xbar0.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):  # warm-up on the capture stream: lazy allocations / attributes
+            eng.step(self.xbar0, self.prev_x, self.prev_u)
+        s.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=s, capture_error_mode="relaxed"):
+            eng.step(self.xbar0, self.prev_x, self.prev_u)
+        torch.cuda.current_stream().wait_stream(s)
+
+    def __call__(self, xbar0=None, prev_x=None, prev_u=None) -> RtiEngine:
+        if xbar0 is not None:
+            self._load(xbar0, prev_x, prev_u)
+        self.graph.replay()
+        return self.eng
+
+    def check(self):
+        """Raise the step's error, if any (synchronizes)."""
+        eng = self.eng
+        rc = eng.ctx.lib.gsls_ctx_check(eng.ctx.handle, stream_ptr())
+        if rc == nat.ERR_LOWRANK:  # the context now runs dense combines: re-run eagerly, re-record
+            eng.step(self.xbar0, self.prev_x, self.prev_u)
+            nat.check(eng.ctx.lib.gsls_ctx_check(eng.ctx.handle, stream_ptr()), "graph step")
+            self._record()
+            return
+        nat.check(rc, "graph step")
