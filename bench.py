@@ -288,6 +288,26 @@ def latency(tag, steps=30, warmup=5):
         if i >= warmup:
             times.append(e0.elapsed_time(e1))
     its = int(eng.stats.iterations[0])
+    # the same step recorded as one CUDA graph (RtiEngine.capture): one launch, no host sync;
+    # its duals carry over from step to step (the engine-held tau), as in closed loop
+    graph = {}
+    try:
+        cap = eng.capture(xb, px, pu)
+        g_times = []
+        for i in range(warmup + steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            cap()
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= warmup:
+                g_times.append(e0.elapsed_time(e1))
+        cap.check()
+        graph = {"p50": statistics.median(g_times), "p90": float(np.percentile(g_times, 90)),
+                 "admm_iterations": int(eng.stats.iterations[0]), "graph_launches_per_step": 1}
+    except Exception as exc:  # noqa: BLE001 - reported, not hidden
+        graph = {"error": f"{type(exc).__name__}: {exc}"}
     # per-kernel-family breakdown of the same step (separate, profiled pass)
     from paper_2604_07644_b200 import _native as nat
     lib = nat.load()
@@ -314,7 +334,7 @@ def latency(tag, steps=30, warmup=5):
             e2e.append(1e3 * (time.perf_counter() - t))
     del eng
     return {"p50": statistics.median(times), "p90": float(np.percentile(times, 90)), "admm_iterations": its,
-            "e2e_p50": statistics.median(e2e), "phases_ms": phases}
+            "e2e_p50": statistics.median(e2e), "phases_ms": phases, "graph": graph}
 
 
 PHASE_GROUPS = {"sls": ("sls_assemble", "sls_leaf", "sls_cvf", "sls_gains", "sls_matprod", "sls_phiu", "sls_rownorm",
@@ -384,7 +404,7 @@ def phase_rooflines(fam, B, dims, iters_per_step, builds_per_step, fp32_peak, hb
     return out
 
 
-def receding_horizon(tag, steps=200, warmup=10, seed=0):
+def receding_horizon(tag, steps=200, warmup=10, seed=0, graph=False):
     """Closed-loop MPC at batch 1: each robust RTI step's u0 drives the plant (model.step plus a
     bounded disturbance E w, |w| <= 1), the next step warm-starts from the shifted plan and the
     engine-held duals.  Device time per step (CUDA events around RtiEngine.step) and the loop's
@@ -403,17 +423,24 @@ def receding_horizon(tag, steps=200, warmup=10, seed=0):
     tc, tt = d(ragged_to_cells(wl.tau, wl.N, (m.nc,))[None]), d(wl.tau_term[None])
     dev_ms, wall_ms, its = [], [], []
     done = 0
+    cap = None
     try:
         for k in range(warmup + steps):
             t0 = time.perf_counter()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             xb = d(x[None])
+            if graph and k == 1:  # record after the first (tau-seeding) eager step
+                cap = eng.capture(xb, px, pu)
             e0.record()
             if k == 0:
                 eng.step(xb, px, pu, tau=tc, tau_term=tt)
+            elif cap is not None:
+                cap(xb, px, pu)
             else:
                 eng.step(xb, px, pu)
             e1.record()
+            if cap is not None:
+                cap.check()
             u0 = eng.u0[0].cpu().numpy()
             w = rng.standard_normal(m.nx)
             w *= rng.random() ** (1.0 / m.nx) / np.linalg.norm(w)
@@ -433,7 +460,7 @@ def receding_horizon(tag, steps=200, warmup=10, seed=0):
     return {"steps": len(dev_ms), "device_ms_p50": statistics.median(dev_ms),
             "device_ms_p90": float(np.percentile(dev_ms, 90)), "device_ms_max": max(dev_ms),
             "loop_wall_ms_p50": statistics.median(wall_ms), "admm_iterations_mean": float(np.mean(its)),
-            "admm_iterations_max": int(max(its)),
+            "admm_iterations_max": int(max(its)), "mode": "CUDA graph replay (one launch per step)" if graph else "eager",
             "disturbance": "x+ = f(x, u0) + E(x) w, w uniform in the unit ball (seed 0)"}
 
 
@@ -689,6 +716,7 @@ def run_ours(args):
     if not args.no_latency:
         for tag in ("q61", "h75"):
             rh[tag] = receding_horizon(tag, steps=args.rh_steps)
+            rh[tag + "_graph"] = receding_horizon(tag, steps=args.rh_steps, graph=True)
     cfg_lines = config_lines() if not args.no_latency else {}
 
     # ---- CPU baseline (rank 0, N=1 only) -----------------------------------------
@@ -715,6 +743,7 @@ def run_ours(args):
            "latency_ms_p90": {k: v["p90"] for k, v in lat.items()},
            "latency_e2e_ms_p50": {k: v["e2e_p50"] for k, v in lat.items()},
            "latency_admm_iterations": {k: v["admm_iterations"] for k, v in lat.items()},
+           "latency_graph_ms": {k: v["graph"] for k, v in lat.items()},
            "latency_phases_ms": {k: v["phases_ms"] for k, v in lat.items()},
            "admm_iterations_mean": total_iters / its_all.numel(),
            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
