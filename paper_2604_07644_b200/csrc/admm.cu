@@ -1539,7 +1539,10 @@ static int replay_cluster(Ctx* c, int count, size_t smem_bytes, const void* kern
   }
   int want = 16;
   if (const char* e = getenv("GSLS_REPLAY_CLUSTER")) want = std::max(1, std::min(16, atoi(e)));
-  for (int cs = want; cs >= 2; cs >>= 1) {
+  // any size up to 16 (the staged kernel's ownership is k mod cs / ceil(ops / cs)): the
+  // ADMM tail's few remaining instances spread over every SM (e.g. 49 instances x 3)
+  const char* p2 = getenv("GSLS_REPLAY_CLUSTER_POW2");
+  for (int cs = want; cs >= 2; cs = (p2 && p2[0] == '1') ? cs >> 1 : cs - 1) {
     if ((long long)count * cs > sms) continue;
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
