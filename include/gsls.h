@@ -223,6 +223,11 @@ int gsls_sls_import_response(gsls_ctx* ctx, const float* phix, const float* phiu
 /* SlsResponse export (sls.py:51-92): Phi_x (B,ncell,nx,nx), Phi_u and gains
  * (B,ncell,nu,nx) (zero on terminal cells), float32; any may be NULL. */
 int gsls_sls_export(gsls_ctx* ctx, float* phix, float* phiu, float* gains, void* stream);
+/* sls.sls_cost (sls.py:344-358) of the response held by ctx: cost (B,) float64 =
+ * sum over cells of tr(Phi' W Phi) = ||L' Phi||_F^2 (W = L L': Qbar for Phi^x at k < N,
+ * QbarN at k = N, Rbar for Phi^u); weights nx x nx / nu x nu float64 device arrays. */
+int gsls_sls_cost(gsls_ctx* ctx, const double* Qbar, const double* Rbar, const double* QbarN, double* cost,
+                  void* stream);
 
 /* ---- SQP linearization (sqp.py:105-147) ----------------------------------- */
 enum { GSLS_MODEL_DUBINS = 1, GSLS_MODEL_PLANAR_QUAD = 2, GSLS_MODEL_PENDULUM = 3,

@@ -103,6 +103,7 @@ _SIGS = {
                        + [c_void_p] * 5, ctypes.c_int),
     "gsls_sls_import_response": ([c_void_p] * 4, ctypes.c_int),
     "gsls_sls_export": ([c_void_p] * 5, ctypes.c_int),
+    "gsls_sls_cost": ([c_void_p] * 6, ctypes.c_int),
     "gsls_linearize": ([c_void_p, ctypes.POINTER(LinArgs), ctypes.POINTER(Qp), c_void_p, c_void_p], ctypes.c_int),
     "gsls_traj_eval": ([c_void_p, ctypes.POINTER(LinArgs), c_void_p, c_void_p], ctypes.c_int),
     "gsls_apply_tightening": ([c_void_p] * 6, ctypes.c_int),

@@ -39,6 +39,7 @@ int rti_apply(Ctx* c, const double* px, const double* pu, const double* dx, cons
               double* plan_u, double* warm_x, double* warm_u, double* u0, const double* Qw, const double* Rw,
               const double* QNw, const double* xref, const double* uref, double* cost, cudaStream_t st);
 int sls_export(Ctx* c, float* phix, float* phiu, float* gains, cudaStream_t st);
+int sls_cost(Ctx* c, const double* Qbar, const double* Rbar, const double* QbarN, double* cost, cudaStream_t st);
 int rollout(Ctx* c, const gsls_rollout_args_t* in, const gsls_rollout_out_t* out, cudaStream_t st);
 int sls_set_columns(Ctx* c, int j0, int j1);
 }  // namespace gsls
@@ -209,6 +210,12 @@ int gsls_sls_import_response(gsls_ctx* ctx, const float* phix, const float* phiu
 int gsls_sls_export(gsls_ctx* ctx, float* phix, float* phiu, float* gains, void* stream) {
   if (!ctx) return fail_null("ctx");
   return sls_export(ctx->impl, phix, phiu, gains, (cudaStream_t)stream);
+}
+
+int gsls_sls_cost(gsls_ctx* ctx, const double* Qbar, const double* Rbar, const double* QbarN, double* cost,
+                  void* stream) {
+  if (!ctx || !Qbar || !Rbar || !QbarN || !cost) return fail_null("argument");
+  return sls_cost(ctx->impl, Qbar, Rbar, QbarN, cost, (cudaStream_t)stream);
 }
 
 int gsls_linearize(gsls_ctx* ctx, const gsls_linearize_args_t* args, const gsls_qp_t* out, float* E, void* stream) {

@@ -98,6 +98,7 @@ struct SlsState {
   const int4* cvf_ops_v[2] = {nullptr, nullptr};
   const int* leaf_v[2] = {nullptr, nullptr};
   bool dense = false;
+  double* cost_cells = nullptr;  // sls_cost: per (instance, cell) terms
 };
 
 static SlsState* sls_of(Ctx* c) { return reinterpret_cast<SlsState*>(c->sls); }
@@ -899,6 +900,85 @@ int sls_duals(Ctx* c, const gsls_qp_t* qp, const double* lam, double eps, int us
   if (S.have_response && !reuse_rownorms && (rc = sls_rownorms(c, qp, st))) return rc;
   ProfScope ps(P_SLS_SMALL, st, (double)c->dims.batch);
   k_sls_duals<<<c->dims.batch, 256, 0, st>>>(S, lam, eps, tau, tau_term, beta, beta_term);
+  GSLS_CUDA_CHECK(cudaGetLastError());
+  return GSLS_OK;
+}
+
+// sls.sls_cost (sls.py:344-358): sum over the response's cells of ||L' Phi||_F^2 with
+// W = L L' the cell's weight (Qbar for Phi^x_{k,j}, k < N; QbarN at k = N; Rbar for
+// Phi^u), i.e. tr(Phi' W Phi).  One CTA per (cell, instance) writes the cell's term in
+// float64 (Phi read from the synthesis storage); a second pass sums each instance's
+// cells in cell order (deterministic).
+__global__ void __launch_bounds__(256) k_sls_cost_cells(DevSls S, const double* Qbar, const double* Rbar,
+                                                        const double* QbarN, double* cells) {
+  const int cell = blockIdx.x, inst = blockIdx.y;
+  const int n = S.n, m = S.m, ldg = S.ldg, N = S.N;
+  const int k = S.cell_kj[cell].x;
+  const size_t cb = (size_t)inst * S.ncell + cell;
+  extern __shared__ double smc[];
+  double* W = smc;            // n x n
+  double* F = W + n * n;      // n x n   Phi^x (then Phi^u rows in the first m rows)
+  double* red = F + n * n;    // 32
+  const float* px = S.Ms + ((size_t)inst * S.mp_nslots + S.mp_out[cell]) * n * ldg;
+  const double* Wx = (k < N) ? Qbar : QbarN;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    W[e] = Wx[e];
+    F[e] = (double)px[(e / n) * ldg + e % n];
+  }
+  __syncthreads();
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {  // (a, c): Phi[a][c] (W Phi)[a][c]
+    const int a = e / n, cc = e - a * n;
+    double t = 0.0;
+    for (int b = 0; b < n; ++b) t = fma(W[a * n + b], F[b * n + cc], t);
+    acc = fma(F[e], t, acc);
+  }
+  if (k < N) {  // Phi^u_{k,j} (m x n) with Rbar
+    __syncthreads();
+    const float* pu = S.Phiu + cb * m * n;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) W[e] = Rbar[e];
+    for (int e = threadIdx.x; e < m * n; e += blockDim.x) F[e] = (double)pu[e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+      const int a = e / n, cc = e - a * n;
+      double t = 0.0;
+      for (int b = 0; b < m; ++b) t = fma(W[a * m + b], F[b * n + cc], t);
+      acc = fma(F[e], t, acc);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) sum += red[w];
+    cells[cb] = sum;
+  }
+}
+
+__global__ void k_sls_cost_sum(const double* cells, int ncell, int B, double* cost) {
+  const int inst = blockIdx.x * blockDim.x + threadIdx.x;
+  if (inst >= B) return;
+  double s = 0.0;
+  for (int i = 0; i < ncell; ++i) s += cells[(size_t)inst * ncell + i];
+  cost[inst] = s;
+}
+
+int sls_cost(Ctx* c, const double* Qbar, const double* Rbar, const double* QbarN, double* cost, cudaStream_t st) {
+  int rc = sls_init(c);
+  if (rc) return rc;
+  SlsState* s = sls_of(c);
+  DevSls& S = s->dev;
+  const int B = c->dims.batch;
+  if (!s->cost_cells) {
+    s->cost_cells = (double*)dev_alloc(c, (size_t)B * S.ncell * sizeof(double));
+    if (!s->cost_cells) return GSLS_ERR_CUDA;
+  }
+  const size_t sb = (2 * (size_t)S.n * S.n + 32) * sizeof(double);
+  if ((rc = smem_attr((const void*)k_sls_cost_cells, sb))) return rc;
+  k_sls_cost_cells<<<dim3(S.ncell, B), 256, sb, st>>>(S, Qbar, Rbar, QbarN, s->cost_cells);
+  GSLS_CUDA_CHECK(cudaGetLastError());
+  k_sls_cost_sum<<<(B + 127) / 128, 128, 0, st>>>(s->cost_cells, S.ncell, B, cost);
   GSLS_CUDA_CHECK(cudaGetLastError());
   return GSLS_OK;
 }

@@ -187,41 +187,54 @@ def sample_disturbance(kind: str, n_x: int, horizon: int, seed, rows: np.ndarray
 
 
 def adversarial_rows(model, traj, constraint_row: int | None = None, max_lookahead: int = 4) -> np.ndarray:
-    """rollout.py:126-166: per-stage pushes (C_{k+m} A_{k+m-1} ... A_{k+1} E_k)^T."""
-    N = traj.N
-    rows = np.zeros((N, model.nx))
+    """Per-stage push directions toward the nearest constraint boundary (rollout.py:126-166).
+
+    Row k is the first nonzero (C_t A_{t-1} ... A_{k+1} E_k)^T over the look-ahead stages
+    t = k+1 .. min(k + max_lookahead, N), where C_t is the state part of stage t's most
+    violated constraint (or ``constraint_row``).  The model's Jacobians are evaluated once
+    per stage along the trajectory (t = 1 .. N, with u_{N-1} at t = N) and every stage's
+    window is one pass of running products over them.
+    """
+    N, nx = traj.N, model.nx
+    x, u = np.asarray(traj.x, float), np.asarray(traj.u, float)
+    ut = lambda t: u[min(t, N - 1)]  # noqa: E731
+    push = [None] * (N + 1)  # push[t]: the selected state row of stage t's constraints, or None
+    for t in range(1, N + 1):
+        C, _ = model.stage_constraint_jacobians(x[t], ut(t))
+        C = np.asarray(C, float)
+        if not C.shape[0]:
+            continue
+        if constraint_row is not None:
+            push[t] = C[constraint_row]
+            continue
+        live = np.flatnonzero(np.abs(C).sum(axis=1) > 1e-12)
+        if live.size:
+            g = np.asarray(model.stage_constraints(x[t], ut(t)), float)
+            push[t] = C[live[np.argmax(g[live])]]
+    A = [None] + [np.asarray(model.jacobians(x[t], ut(t))[0], float) for t in range(1, N)]
+    rows = np.zeros((N, nx))
     for k in range(N):
-        E = model.disturbance(traj.x[k])
-        prop = np.eye(model.nx)
-        for m in range(1, max_lookahead + 1):
-            idx_k = min(k + m, N)
-            xk, uk = traj.x[idx_k], traj.u[min(idx_k, N - 1)]
-            C, _ = model.stage_constraint_jacobians(xk, uk)
-            if C.shape[0]:
-                if constraint_row is None:
-                    g = model.stage_constraints(xk, uk)
-                    state_rows = np.where(np.abs(C).sum(axis=1) > 1e-12)[0]
-                    idx = state_rows[np.argmax(g[state_rows])] if state_rows.size else None
-                else:
-                    idx = constraint_row
-                if idx is not None:
-                    cand = (C[idx] @ prop @ E).T
-                    if np.linalg.norm(cand) > 1e-9:
-                        rows[k] = cand
-                        break
-            if idx_k >= N:
-                break
-            A, _ = model.jacobians(traj.x[idx_k], traj.u[min(idx_k, N - 1)])
-            prop = A @ prop
+        E = np.asarray(model.disturbance(x[k]), float)
+        c_row = None  # C_t A_{t-1} ... A_{k+1}, built right to left
+        for t in range(k + 1, min(k + max_lookahead, N) + 1):
+            c_row = None if push[t] is None else push[t].copy()
+            if c_row is not None:
+                for s in range(t - 1, k, -1):
+                    c_row = c_row @ A[s]
+                cand = c_row @ E
+                if np.linalg.norm(cand) > 1e-9:
+                    rows[k] = cand
+                    break
     return rows
 
 
 def superposition_check(traj, response: SlsResponse, w: np.ndarray, realized_x: np.ndarray) -> float:
-    """rollout.py:169-180: worst |x_k - x_nom_k - sum_j Phi^x_{k,j} w_j|."""
-    worst = 0.0
-    for k in range(1, traj.N + 1):
-        pred = np.zeros(traj.x.shape[1])
-        for j in range(k):
-            pred += response.phi_x(k, j) @ w[j]
-        worst = max(worst, float(np.abs(realized_x[k] - traj.x[k] - pred).max()))
-    return worst
+    """Worst |x_k - x_nom_k - sum_{j<k} Phi^x_{k,j} w_j| (rollout.py:169-180), all k at once:
+    the response's lower-triangular blocks contracted with the disturbance sequence."""
+    N = traj.N
+    w = np.asarray(w, float)
+    off = np.asarray(realized_x, float)[1:] - np.asarray(traj.x, float)[1:]
+    pred = np.zeros_like(off)
+    for j in range(N):  # column j feeds stages k = j+1 .. N
+        pred[j:] += np.einsum("kab,b->ka", response.Phi_x[j], w[j])
+    return float(np.abs(off - pred).max()) if N else 0.0

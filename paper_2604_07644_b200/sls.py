@@ -390,21 +390,25 @@ def synthesize_tighten_columns(A, B, E, costs: SlsCosts, C, D, CN, columns, exec
     return h[0], hf[0], phix, phiu
 
 
-def sls_cost(response: SlsResponse, weights: SlsWeights) -> float:
-    """Weighted Frobenius energy of the response maps (sls.py:344-358), on the device."""
-    dev = torch.device("cuda", torch.cuda.current_device())
-    Lq, Lr, Ln = (torch.linalg.cholesky(to_dev(np.asarray(w, float), F64))
-                  for w in (weights.Qbar, weights.Rbar, weights.QbarN))
-    total = torch.zeros((), dtype=F64, device=dev)
-    for j in range(response.N):
-        px = to_dev(response.Phi_x[j], F64)
-        if px.shape[0] > 1:
-            total += ((Lq.T @ px[:-1]) ** 2).sum()
-        total += ((Ln.T @ px[-1]) ** 2).sum()
-        pu = response.Phi_u[j]
-        if len(pu):
-            total += ((Lr.T @ to_dev(pu, F64)) ** 2).sum()
-    return float(total)
+def sls_cost(response: SlsResponse, weights: SlsWeights, executor=None) -> float:
+    """Weighted Frobenius energy of the response maps (sls.py:344-358), computed by
+    gsls_sls_cost on the device response (a host response is loaded first): the sum over
+    cells of ||L' Phi||_F^2 = tr(Phi' W Phi).  The weights must be positive definite, as
+    the reference's Cholesky factors require (np.linalg.LinAlgError otherwise)."""
+    W = [np.asarray(w, float) for w in (weights.Qbar, weights.Rbar, weights.QbarN)]
+    for w in W:
+        np.linalg.cholesky(w)  # the reference's factorization: same error on an indefinite weight
+    N, nx, nu = response.N, response.nx, response.nu
+    if N == 0:
+        return 0.0
+    tok = getattr(response, "_tok", None)
+    ws = tok[0] if tok is not None and tok[1] == tok[0].resp_ver else _ws(nx, nu, 1, 1, N, executor)
+    _ensure_response(ws, response)
+    Qb, Rb, QbN = (to_dev(w, F64).contiguous() for w in W)
+    out = torch.zeros(1, dtype=F64, device=Qb.device)
+    nat.check(ws.ctx.lib.gsls_sls_cost(ws.ctx.handle, Qb.data_ptr(), Rb.data_ptr(), QbN.data_ptr(), out.data_ptr(),
+                                       stream_ptr()), "sls_cost")
+    return float(out[0])
 
 
 # --- robust loops ------------------------------------------------------------------------
