@@ -51,6 +51,9 @@ def main():
     its = eng.stats.iterations.cpu().numpy()
     print(f"B={B} {a.tag}: wall {wall:.2f} ms/step (serialized streams); ADMM iterations mean {its.mean():.1f} "
           f"max {its.max()} sum {its.sum()}; rho changes {eng.stats.rho_changes.cpu().numpy().sum()}")
+    q = np.percentile(its, [10, 50, 90, 99])
+    print(f"  iterations p10/p50/p90/p99 {q.tolist()}; histogram (25-wide bins): "
+          f"{np.bincount(its // 25).tolist()}")
     tot = 0.0
     for k, v, c in zip(nat.PROF_FAMILIES, ms, nl):
         if c:
