@@ -106,12 +106,41 @@ def measured_peaks():
         return {}
 
 
+def _admm_max_iter():
+    from paper_2604_07644_b200 import scenarios
+    return scenarios.ADMM["max_iter"]
+
+
+def makespan_block(its_all, fam_s, iters_per_step, B, b_iter, hbm_peak, max_iter):
+    """ADMM load balance: the per-instance iteration spread of the timed
+    batch against the replay's device time, and the replay time the same total iteration
+    count would take at the bulk waves' measured bandwidth (ncu, profiles/rNN/traffic.json)
+    -- the excess is the long-running instances' tail (latency-bound clusters)."""
+    it = its_all.flatten().cpu().numpy()
+    q = np.percentile(it, [50, 90, 99])
+    out = {"mean": float(it.mean()), "p50": float(q[0]), "p90": float(q[1]), "p99": float(q[2]),
+           "max": float(it.max()), "at_max_iter_fraction": float((it >= max_iter).mean()),
+           "iterations_in_instances_beyond_p90": float(it[it > q[1]].sum() / max(it.sum(), 1.0))}
+    rep = fam_s.get("replay")
+    tr = ncu_traffic().get("replay") or {}
+    if rep and tr.get("duration_ms") and tr.get("units"):
+        bulk_gbs = tr["units"] * b_iter / (tr["duration_ms"] / 1e3) / 1e9  # algorithmic, first (full) wave
+        at_bulk_ms = iters_per_step * b_iter / (bulk_gbs * 1e9) * 1e3
+        out.update({"replay_ms_per_step": rep[0], "bulk_wave_gbs": bulk_gbs,
+                    "replay_ms_at_bulk_bandwidth": at_bulk_ms, "tail_excess_ms": rep[0] - at_bulk_ms})
+    return out
+
+
 def ncu_traffic():
     """DRAM bytes per launch of the roofline kernels from the committed ncu capture."""
     try:
-        return json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic.json")))
+        for rnd in ("r02", "r01"):  # the latest round's captures
+            f = os.path.join(ROOT, "profiles", rnd, "traffic.json")
+            if os.path.exists(f):
+                return json.load(open(f))
     except Exception:
-        return {}
+        pass
+    return {}
 
 
 def W(L):
@@ -746,6 +775,8 @@ def run_ours(args):
            "latency_graph_ms": {k: v["graph"] for k, v in lat.items()},
            "latency_phases_ms": {k: v["phases_ms"] for k, v in lat.items()},
            "admm_iterations_mean": total_iters / its_all.numel(),
+           "admm_makespan": makespan_block(its_all, fam_s, iters_per_step, B, bytes_replay_iter(n, mu, c, nf, N),
+                                           hbm_peak, max_iter=_admm_max_iter()),
            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
            "gpu_launches": launches, "roofline": roof, "roofline_by_kernel": rl, "roofline_by_phase": rl_phase,
            "phases": phases, "receding_horizon_b1": rh, "configs_drop_in": cfg_lines,

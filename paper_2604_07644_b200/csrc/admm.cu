@@ -96,7 +96,7 @@ __host__ __device__ inline VecLayout vec_layout(int n, int m, int N, int mtot, i
   v.part = take(kReplayThreads);     // split-K partial sums (kReplayThreads / 32 warps x 32 rows)
   v.redall = take(2 * kMaxCluster);  // per-rank partial maxima of the residuals
   v.masks = take((s_cvf + s_cot + 1) / 2 + 1);  // consumer-rank masks per slot (uint32)
-  v.plan = take(2 * (nops_cvf + nops_cot) + (lay_cvf + lay_cot + 2 + 2 * N + 2) / 2 + 2);  // scan plan copy
+  v.plan = take(2 * (nops_cvf + nops_cot) + (2 * lay_cvf + lay_cot + 2 + 2 * N + 2) / 2 + 2);  // scan plan copy
   v.total = o;
   return v;
 }
@@ -513,6 +513,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
   const int* s_cot_loff = L.cot_loff;
   const int* s_cvf_out = L.cvf_out;
   const int* s_cot_out = L.cot_out;
+  const int* s_cvf_blive = L.cvf_blive;
   if (!GRID) {
     int4* p_cvf_ops = reinterpret_cast<int4*>(vs + V.plan);
     int4* p_cot_ops = p_cvf_ops + L.cvf_nops;
@@ -520,6 +521,8 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
     int* p_cot_loff = p_cvf_loff + L.cvf_layers + 1;
     int* p_cvf_out = p_cot_loff + L.cot_layers + 1;
     int* p_cot_out = p_cvf_out + N + 1;
+    int* p_cvf_blive = p_cot_out + N;
+    for (int i = tid; i < L.cvf_layers; i += nthr) p_cvf_blive[i] = L.cvf_blive[i];
     for (int i = tid; i < L.cvf_nops; i += nthr) p_cvf_ops[i] = L.cvf_ops[i];
     for (int i = tid; i < L.cot_nops; i += nthr) p_cot_ops[i] = L.cot_ops[i];
     for (int i = tid; i <= L.cvf_layers; i += nthr) p_cvf_loff[i] = L.cvf_loff[i];
@@ -527,7 +530,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
     for (int i = tid; i <= N; i += nthr) p_cvf_out[i] = L.cvf_out[i];
     for (int i = tid; i < N; i += nthr) p_cot_out[i] = L.cot_out[i];
     s_cvf_ops = p_cvf_ops; s_cot_ops = p_cot_ops; s_cvf_loff = p_cvf_loff; s_cot_loff = p_cot_loff;
-    s_cvf_out = p_cvf_out; s_cot_out = p_cot_out;
+    s_cvf_out = p_cvf_out; s_cot_out = p_cot_out; s_cvf_blive = p_cvf_blive;
   }
   __syncthreads();
   // dx_k lives in the COT outputs (k >= 1) or dx0
@@ -558,12 +561,12 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
     for (int i = tid; i < L.cvf_nslots + L.cot_nslots; i += nthr) cvf_mask[i] = 0u;
   __syncthreads();
   if (!GRID && cs > 1) {
-    for (int lay = 0; lay < L.cvf_layers; ++lay) {  // half-ops (p, b) h = 2 oi + which on rank h / per
-      const int o0 = s_cvf_loff[lay], nh = 2 * (s_cvf_loff[lay + 1] - o0), per = (nh + cs - 1) / cs;
-      for (int h = tid; h < nh; h += nthr) {
-        const int4 op = s_cvf_ops[o0 + (h >> 1)];
-        atomicOr(cvf_mask + op.y, 1u << (h / per));
-        atomicOr(cvf_mask + op.z, 1u << (h / per));
+    for (int lay = 0; lay < L.cvf_layers; ++lay) {  // op oi (both halves) on rank oi / per
+      const int o0 = s_cvf_loff[lay], no = s_cvf_loff[lay + 1] - o0, per = (no + cs - 1) / cs;
+      for (int oi = tid; oi < no; oi += nthr) {
+        const int4 op = s_cvf_ops[o0 + oi];
+        atomicOr(cvf_mask + op.y, 1u << (oi / per));
+        atomicOr(cvf_mask + op.z, 1u << (oi / per));
       }
     }
     for (int p = tid; p <= N; p += nthr) atomicOr(cvf_mask + s_cvf_out[p], 1u << srank(max(p - 1, 0)));
@@ -667,19 +670,28 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay(ReplayArgs a) {
       if (tid == 0 && lay + 1 < L.cvf_layers && a.prefetch) {  // next layer's records -> L2 during this round
         const int p0 = s_cvf_loff[lay + 1], pn = s_cvf_loff[lay + 2] - p0, pp = (pn + cs - 1) / cs;
         const int plo = min(pn, rank * pp), pnl = min(pn, plo + pp) - plo;
-        if (pnl > 0) prefetch_l2_range(cvf_rec + (size_t)(p0 + plo) * 4 * MS, (size_t)pnl * 4 * MS * sizeof(float));
+        // ops with a live b: all four operators (contiguous); the rest: [Ups X] only
+        const int pl = max(0, min(plo + pnl, s_cvf_blive[lay + 1]) - plo);
+        if (pl > 0) prefetch_l2_range(cvf_rec + (size_t)(p0 + plo) * 4 * MS, (size_t)pl * 4 * MS * sizeof(float));
+        for (int q = plo + pl; q < plo + pnl; ++q)
+          prefetch_l2_range(cvf_rec + (size_t)(p0 + q) * 4 * MS, (size_t)2 * MS * sizeof(float));
       }
       if (no == 0) continue;
       const int per = (no + cs - 1) / cs;
       const int lo = min(no, rank * per), nl = min(no, lo + per) - lo;
       if (nl > 0) {
         // p = p_earlier + Ups p_later + X b_earlier, b = b_later + Psi b_earlier - Y p_later
-        // (lqr.py:242-246 with the recorded X = Ups Pr, -Y = -Psi Cl): one round per layer
-        mv_round(2 * nl, n, ldg, part, cl, [&](int ti) {
-          const int oi = lo + (ti >> 1);
+        // (lqr.py:242-246 with the recorded X = Ups Pr, -Y = -Psi Cl): one round per layer.
+        // Tasks [0, nl): the p halves; [nl, nl + nb): the b halves of the ops whose result
+        // a later op reads (the layer's first s_cvf_blive[lay] ops; the b of the scan's
+        // final outputs is never read, plan.h partition_unread_last)
+        const int nb = max(0, min(lo + nl, s_cvf_blive[lay]) - lo);
+        mv_round(nl + nb, n, ldg, part, cl, [&](int ti) {
+          const bool bh = ti >= nl;
+          const int oi = lo + (bh ? ti - nl : ti);
           const int4 op = s_cvf_ops[o0 + oi];
           const float* rec = cvf_rec + (size_t)(o0 + oi) * 4 * MS;
-          if ((ti & 1) == 0)
+          if (!bh)
             return MvTask{rec + 0 * MS, pv + op.z * n, pv + op.y * n, 1.0, pv + op.x * n, cvf_mask[op.x],
                           rec + 1 * MS, bv + op.y * n, 1.0};
           return MvTask{rec + 2 * MS, bv + op.y * n, bv + op.z * n, 1.0, bv + op.x * n, cvf_mask[op.x],
@@ -1016,7 +1028,7 @@ __host__ __device__ inline StagedLayout staged_layout(const DevLqr& L, int max_l
   S.red = take(64 * 8, 16);
   S.redall = take(2 * kMaxCluster * 8, 16);
   S.masks = take((L.cvf_nslots + L.cot_nslots) * 4, 16);
-  S.ops = take((L.cvf_nops + L.cot_nops) * 16 + (L.cvf_layers + L.cot_layers + 2 + 2 * N + 2) * 4, 16);
+  S.ops = take((L.cvf_nops + L.cot_nops) * 16 + (2 * L.cvf_layers + L.cot_layers + 2 + 2 * N + 2) * 4, 16);
   S.phys = take((L.cvf_nslots + L.cot_nslots) * 4, 16);
   S.max_items = max_items;
   S.items = take(S.max_items * (int)sizeof(ItemDesc), 16);
@@ -1103,6 +1115,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   int* s_cot_loff = s_cvf_loff + L.cvf_layers + 1;
   int* s_cvf_out = s_cot_loff + L.cot_layers + 1;
   int* s_cot_out = s_cvf_out + N + 1;
+  int* s_cvf_blive = s_cot_out + N;
   int* cvf_phys = reinterpret_cast<int*>(smb + SL.phys);
   int* cot_phys = cvf_phys + L.cvf_nslots;
   ItemDesc* desc = reinterpret_cast<ItemDesc*>(smb + SL.items);
@@ -1119,6 +1132,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   for (int i = tid; i <= L.cot_layers; i += nthr) s_cot_loff[i] = (N > 0) ? L.cot_loff[i] : 0;
   for (int i = tid; i <= N; i += nthr) s_cvf_out[i] = L.cvf_out[i];
   for (int i = tid; i < N; i += nthr) s_cot_out[i] = L.cot_out[i];
+  for (int i = tid; i < L.cvf_layers; i += nthr) s_cvf_blive[i] = L.cvf_blive[i];
   for (int i = tid; i < L.cvf_nslots; i += nthr) cvf_phys[i] = L.cvf_phys[i];
   for (int i = tid; i < L.cot_nslots; i += nthr) cot_phys[i] = L.cot_phys[i];
   for (int i = tid; i < L.cvf_nslots + L.cot_nslots; i += nthr) cvf_mask[i] = 0u;
@@ -1126,10 +1140,11 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   __syncthreads();
   auto srank = [&](int k) { return k % cs; };
   if (cs > 1) {
-    for (int lay = 0; lay < L.cvf_layers; ++lay) {  // half-ops (p, b) h = 2 oi + which on rank h / per
-      const int o0 = s_cvf_loff[lay], nh = 2 * (s_cvf_loff[lay + 1] - o0), per = (nh + cs - 1) / cs;
+    for (int lay = 0; lay < L.cvf_layers; ++lay) {  // half-op h on rank h / per (cvf_half)
+      const int o0 = s_cvf_loff[lay], no = s_cvf_loff[lay + 1] - o0, nh = no + s_cvf_blive[lay];
+      const int per = (nh + cs - 1) / cs;
       for (int h = tid; h < nh; h += nthr) {
-        const int4 op = s_cvf_ops[o0 + (h >> 1)];
+        const int4 op = s_cvf_ops[o0 + (h < no ? h : h - no)];
         atomicOr(cvf_mask + op.y, 1u << (h / per));
         atomicOr(cvf_mask + op.z, 1u << (h / per));
       }
@@ -1153,11 +1168,14 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
     phase_off[ph++] = ni;
     for (int k = rank; k < N; k += cs) add(IT_P1, 0, k);
     for (int lay = 0; lay < L.cvf_layers; ++lay) {
-      // half-ops: p = p_e + [Ups X] [p_l; b_e] (which 0), b = b_l + [Psi -Y] [b_e; p_l] (which 1)
-      const int o0 = s_cvf_loff[lay], nh = 2 * (s_cvf_loff[lay + 1] - o0), per = (nh + cs - 1) / cs;
+      // half-ops: p = p_e + [Ups X] [p_l; b_e] (which 0) for every op (h < no), then
+      // b = b_l + [Psi -Y] [b_e; p_l] (which 1) for the layer's first s_cvf_blive ops (the
+      // others' results are read by no later op, so their b is dead)
+      const int o0 = s_cvf_loff[lay], no = s_cvf_loff[lay + 1] - o0, nh = no + s_cvf_blive[lay];
+      const int per = (nh + cs - 1) / cs;
       const int lo = min(nh, rank * per), hi = min(nh, lo + per);
       phase_off[ph++] = ni;
-      for (int h = lo; h < hi; ++h) add(IT_CVF1, h & 1, o0 + (h >> 1));
+      for (int h = lo; h < hi; ++h) add(IT_CVF1, h < no ? 0 : 1, o0 + (h < no ? h : h - no));
     }
     phase_off[ph++] = ni;
     for (int k = rank; k < N; k += cs) add(IT_FF1, 0, k);

@@ -20,6 +20,8 @@ struct DevLqr {
   const int* cvf_out;
   const int* cvf_loff;   // layer offsets (cvf_layers + 1)
   const int* cvf_leaf;   // per leaf: bit 3 = C stored as a factor (upload_plan)
+  const int* cvf_blive;  // per layer: ops whose result a later op reads (first in the layer;
+                         // the rest have a dead b: no [Psi -Y] record, no b replay)
   int cvf_nslots, cvf_nops, cvf_layers;
   // COT plan (forward scan over N elements)
   const int4* cot_ops;

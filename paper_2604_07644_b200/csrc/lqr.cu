@@ -360,7 +360,7 @@ __device__ __forceinline__ bool cvf_combine_factored(const CombineArgs& a, const
   const size_t oe = (size_t)op.y * MS, ol = (size_t)op.z * MS, od = (size_t)op.x * MS;
   const bool need_a = !(op.w & 1);                // A (A^T unless bit 2) live
   const bool need_c = !(op.w & 2);                // C live
-  const bool need_psi = rec != nullptr || need_a;
+  const bool need_psi = need_a;                   // (a recorded op with bit 0 is never read: no b half)
   const bool need_u = need_psi || need_c;
   const bool out_factor = (op.w & 8) != 0;
   const float* Cr = a.Cs + ib + ol;
@@ -389,7 +389,7 @@ __device__ __forceinline__ bool cvf_combine_factored(const CombineArgs& a, const
     __syncthreads();
     if (need_psi)  // Psi' = Ar^T - V U' (in place), record slot 2
       gemm_nn_mn(n, n, R, b2, lds, sb, lds, EpiSub{b4, b4, lds, n, rec ? rec + 2 * MS : nullptr, ldg});
-    if (rec)  // -Y' = -Fh U', record slot 3
+    if (rec && need_psi)  // -Y' = -Fh U', record slot 3
       gemm_nn_mn(n, n, R, b1, lds, sb, lds, EpiG{rec + 3 * MS, nullptr, ldg, n, nullptr, nullptr, 0, -1.f});
     if (need_c) {
       if (out_factor) {  // [U | F_r], zero beyond (ranks are multiples of 4: float4 columns)
@@ -485,9 +485,11 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   float* rec = a.rec ? a.rec + (long long)inst * a.rec_inst_stride + (size_t)(a.op_base + blockIdx.x) * 4 * MS
                      : nullptr;
 
-  // fin: an unrecorded combine whose output's A, A^T and C are all dead (plan .w bit 0):
-  // only P is formed, so Ar^T, W2, Psi, A and C are skipped (4 of 8 GEMMs)
-  const bool fin = (op.w & 1) && rec == nullptr;
+  // fin: the output's A, A^T and C are all dead (plan .w bit 0): only P is formed, so
+  // Ar^T, W2, Psi, A and C are skipped (4 of 8 GEMMs).  A recorded op with bit 0 is one
+  // whose result no later op reads (recorded readers always need A^T), so its b half
+  // is never replayed either (partition_unread_last): only Ups and X are recorded.
+  const bool fin = (op.w & 1);
   cta_load_async(b0, lds, a.Ps + ib + ol, n);   // Pr (= Pr^T)
   cta_load_async(b1, lds, a.Cs + ib + oe, n);   // Cl (= Cl^T)
   cp_async_commit();
@@ -516,7 +518,7 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   CTRACE(4);
   if (rec) {
     gemm_tn(n, b1, b3, lds, EpiGlobal{rec + 0 * MS, nullptr, ldg, n, nullptr});  // Ups^T = Minv^T Al
-    gemm_tn(n, b1, b0, lds, EpiGlobalNeg{rec + 3 * MS, ldg, n});  // -Y^T = -Minv^T W2
+    if (!fin) gemm_tn(n, b1, b0, lds, EpiGlobalNeg{rec + 3 * MS, ldg, n});  // -Y^T = -Minv^T W2
     __syncthreads();
   }
   gemm_tn(n, b2, b5, lds, EpiSmem{b1, lds, n, false});  // V = Minv W1 = X^T (over Minv)
@@ -530,10 +532,6 @@ __global__ void __launch_bounds__(NP == 64 ? 288 : 416, NP == 64 ? 2 : 1) k_cvf_
   gemm_tn(n, b2, b4, lds, EpiSmem{b5, lds, n, false});  // Psi^T = Minv Ar^T (over W1)
   __syncthreads();
   if (rec) cta_store(rec + 2 * MS, b5, lds, n);          // Psi record
-  if (op.w & 1) {  // recorded combine whose A, C no later layer reads
-    CTRACE(5);
-    return;
-  }
   gemm_tn(n, b5, b3, lds, EpiGlobal{a.As + ib + od, nullptr, ldg, n, (op.w & 4) ? nullptr : a.ATs + ib + od});  // A = Psi Al (+ A^T)
   if (!(op.w & 2)) gemm_tn(n, b5, b0, lds, EpiGlobal{a.Cs + ib + od, a.Cs + ib + ol, ldg, n, nullptr});  // C = Psi W2 + Cr
   __syncthreads();
@@ -989,6 +987,7 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
   c->ldg = ldg_of(d.nx);
   c->mtot = d.N * d.nc + d.nf;
   c->cvf = make_scan_plan(d.N + 1, true);
+  const std::vector<int> cvf_blive = partition_unread_last(c->cvf);
   c->cot = d.N > 0 ? make_scan_plan(d.N, false) : ScanPlan{};
   c->cvf_layer_off = c->cvf.layer_off;
   c->cot_layer_off = c->cot.layer_off;
@@ -1024,6 +1023,13 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
                                  cudaMemcpyHostToDevice));
     L.cvf_phys = dp;
     L.cot_phys = dp + c->cvf_phys.size();
+  }
+  {
+    int* db = (int*)dev_alloc(c, (cvf_blive.size() + 1) * sizeof(int));
+    if (!db) { delete c; return GSLS_ERR_CUDA; }
+    if (!cvf_blive.empty())
+      GSLS_CUDA_CHECK(cudaMemcpy(db, cvf_blive.data(), cvf_blive.size() * sizeof(int), cudaMemcpyHostToDevice));
+    L.cvf_blive = db;
   }
   L.cvf_nslots = c->cvf.nslots;
   L.cvf_nops = (int)c->cvf.ops.size();

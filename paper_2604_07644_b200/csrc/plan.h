@@ -107,6 +107,27 @@ inline ScanPlan make_scan_plan(int length, bool reverse, const std::vector<char>
   return pl;
 }
 
+// Within every layer, moves the ops whose result no later op reads (the scan's
+// final outputs, read only through out[]) behind the others, keeping both groups in
+// order; ops of one layer are independent, so the values are unchanged.  Returns the
+// per-layer count of ops whose result is read again.  The CVF replay uses it: of a
+// combine's affine outputs (p, b), b is read only by later combines, so the
+// unread ops skip their b half ([Psi -Y], half the op's replay operator bytes).
+inline std::vector<int> partition_unread_last(ScanPlan& p) {
+  std::vector<char> rd(std::max(p.nslots, 1), 0);
+  for (const ScanOp& q : p.ops) {
+    if (q.earlier >= 0) rd[q.earlier] = 1;
+    if (q.later >= 0) rd[q.later] = 1;
+  }
+  std::vector<int> live(p.layers, 0);
+  for (int l = 0; l < p.layers; ++l) {
+    auto b = p.ops.begin() + p.layer_off[l], e = p.ops.begin() + p.layer_off[l + 1];
+    auto mid = std::stable_partition(b, e, [&](const ScanOp& q) { return rd[q.dst] != 0; });
+    live[l] = (int)(mid - b);
+  }
+  return live;
+}
+
 // Physical slots for the replay vectors: interval colouring of slot lifetimes.
 // Leaves are defined at time 0; the ops of layer l read their operands and
 // define their result at time l + 1 (a result may not share storage with
