@@ -302,6 +302,45 @@ int gsls_rti_apply(gsls_ctx* ctx, const double* prev_x, const double* prev_u, co
                    const double* Rw, const double* QNw, const double* xref, const double* uref, double* cost,
                    void* stream);
 
+/* ---- one MPC step for the whole batch (the metric's unit of work) ------------
+ * Replaces sls.rti_robust_step (sls.py:500-525) for every instance of the
+ * context when robust = 1, sqp.rti_step (sqp.py:272-302) when robust = 0:
+ * linearize at (lin.x, lin.u) = (prev_x, prev_u) with lin.xbar0; [robust: SLS
+ * costs with the duals tau / tau_term when use_tau (else unweighted),
+ * synthesize, tighten into h / hf, f -= h]; admm.solve_qp from a cold state
+ * (state reset to rho0) or the given one (warm_admm); [robust: compute_duals
+ * into tau, tau_term, beta, beta_term for the next step]; plan / warm start / u0
+ * / tracking cost.  The ADMM's first factorization runs on the context's side
+ * stream concurrently with the SLS chain unless no_overlap.  Capturable into a
+ * CUDA graph.  All pointers are device buffers of the layouts above; `qp` is the
+ * QP workspace the step writes.  E_in (B,N,nx,nx) or NULL overrides the
+ * disturbance maps after the linearization. */
+typedef struct {
+  gsls_linearize_args_t lin;      /* model, x = prev_x, u = prev_u, xbar0, weights     */
+  const gsls_qp_t* qp;            /* QP workspace (written)                             */
+  float* E;                       /* (B,N,nx,nx) disturbance maps (written)             */
+  const float* E_in;              /* or NULL                                            */
+  int32_t robust, use_tau, warm_admm, no_overlap;
+  const float *Qbar, *Rbar, *QbarN;  /* SLS weights (nx,nx) (nu,nu) (nx,nx)            */
+  double *tau, *tau_term, *beta, *beta_term;  /* cell-layout duals, in / out           */
+  double eps;                     /* compute_duals epsilon                              */
+  gsls_admm_settings_t admm;
+  gsls_admm_state_t state;
+  gsls_admm_stats_t stats;
+  double *h, *hf;                 /* tightenings (B,N,nc), (B,nf)                       */
+  double *dx, *du;                /* QP solution (B,N+1,nx), (B,N,nu)                   */
+  double *plan_x, *plan_u, *warm_x, *warm_u, *u0;
+  double* cost;                   /* (B) tracking cost of the plan, or NULL             */
+} gsls_rti_step_args_t;
+
+int gsls_rti_step(gsls_ctx* ctx, const gsls_rti_step_args_t* args, void* stream);
+
+/* The per-instance result record a multi-GPU batch exchanges (one all-gather per
+ * step, dist.py): rec (B, nu + 4) float64 = u0, ADMM iterations, converged, rho
+ * changes, cost (0 when cost is NULL). */
+int gsls_rti_pack_results(gsls_ctx* ctx, const double* u0, const gsls_admm_stats_t* stats, const double* cost,
+                          double* rec, void* stream);
+
 /* ---- profiling (bench.py roofline evidence) -----------------------------
  * When enabled, every kernel launch records a CUDA event pair on its stream.
  * gsls_prof_read synchronizes and returns, per kernel family (order:

@@ -57,6 +57,16 @@ class LinArgs(ctypes.Structure):
                 ("E_const", c_void_p), ("write_weights", ctypes.c_int32)]
 
 
+class RtiStepArgs(ctypes.Structure):
+    """gsls_rti_step_args_t (include/gsls.h)."""
+    _fields_ = ([("lin", LinArgs), ("qp", ctypes.POINTER(Qp)), ("E", c_void_p), ("E_in", c_void_p)]
+                + [(k, ctypes.c_int32) for k in ("robust", "use_tau", "warm_admm", "no_overlap")]
+                + [(k, c_void_p) for k in ("Qbar", "Rbar", "QbarN", "tau", "tau_term", "beta", "beta_term")]
+                + [("eps", ctypes.c_double), ("admm", AdmmSettings), ("state", AdmmState), ("stats", AdmmStats)]
+                + [(k, c_void_p) for k in ("h", "hf", "dx", "du", "plan_x", "plan_u", "warm_x", "warm_u", "u0",
+                                           "cost")])
+
+
 class RolloutArgs(ctypes.Structure):
     _fields_ = [("model_id", ctypes.c_int32), ("params", c_void_p), ("cons_offset", ctypes.c_int32),
                 ("x", c_void_p), ("u", c_void_p), ("phi_u", c_void_p), ("E", c_void_p), ("E_pinv", c_void_p),
@@ -110,6 +120,9 @@ _SIGS = {
     "gsls_prof_enable": ([ctypes.c_int32], ctypes.c_int),
     "gsls_prof_read": ([c_void_p, c_void_p, c_void_p, ctypes.c_int32], ctypes.c_int),
     "gsls_rti_apply": ([c_void_p] * 17, ctypes.c_int),
+    "gsls_rti_step": ([c_void_p, ctypes.POINTER(RtiStepArgs), c_void_p], ctypes.c_int),
+    "gsls_rti_pack_results": ([c_void_p, c_void_p, ctypes.POINTER(AdmmStats), c_void_p, c_void_p, c_void_p],
+                              ctypes.c_int),
     "gsls_rollout": ([c_void_p, ctypes.POINTER(RolloutArgs), ctypes.POINTER(RolloutOut), c_void_p], ctypes.c_int),
 }
 

@@ -42,6 +42,9 @@ int sls_export(Ctx* c, float* phix, float* phiu, float* gains, cudaStream_t st);
 int sls_cost(Ctx* c, const double* Qbar, const double* Rbar, const double* QbarN, double* cost, cudaStream_t st);
 int rollout(Ctx* c, const gsls_rollout_args_t* in, const gsls_rollout_out_t* out, cudaStream_t st);
 int sls_set_columns(Ctx* c, int j0, int j1);
+int rti_step(Ctx* c, const gsls_rti_step_args_t* a, cudaStream_t st);
+int rti_pack_results(Ctx* c, const double* u0, const gsls_admm_stats_t* stats, const double* cost, double* rec,
+                     cudaStream_t st);
 }  // namespace gsls
 
 using namespace gsls;
@@ -263,6 +266,35 @@ int gsls_rollout(gsls_ctx* ctx, const gsls_rollout_args_t* args, const gsls_roll
   if (rc == GSLS_ERR_ARG) set_error(rc, -1, 0, 0, 0, "model / dimension mismatch");
   if (rc == GSLS_ERR_TOO_LARGE) set_error(rc, -1, 0, 0, 0, "rollout too large");
   return rc;
+}
+
+int gsls_rti_step(gsls_ctx* ctx, const gsls_rti_step_args_t* args, void* stream) {
+  if (!ctx || !args) return fail_null("argument");
+  const gsls_linearize_args_t& l = args->lin;
+  if (!l.params || !l.x || !l.u || !l.Qw || !l.Rw || !l.QNw || !l.xref || !l.uref) return fail_null("lin argument");
+  if (!args->qp || !args->dx || !args->du || !args->plan_x || !args->plan_u || !args->warm_x || !args->warm_u ||
+      !args->u0)
+    return fail_null("step output");
+  const gsls_admm_state_t& a = args->state;
+  const gsls_admm_stats_t& t = args->stats;
+  if (!a.z || !a.lam || !a.y || !a.rho || !a.r_primal || !a.r_dual || !a.generation || !a.iteration)
+    return fail_null("ADMM state");
+  if (!t.iterations || !t.converged || !t.rho_changes || !t.cache_builds) return fail_null("ADMM stats");
+  const gsls_admm_settings_t& st = args->admm;
+  if (st.sigma < 2 || st.max_iter < 1 || !(st.rho0 > 0) || !(st.tol_primal > 0) || !(st.tol_dual > 0)) {
+    set_error(GSLS_ERR_ARG, -1, 0, 0, 0, "invalid ADMM settings");
+    return GSLS_ERR_ARG;
+  }
+  int rc = rti_step(ctx->impl, args, (cudaStream_t)stream);
+  if (rc == GSLS_ERR_ARG) set_error(rc, -1, 0, 0, 0, "model / dimension mismatch");
+  return rc;
+}
+
+int gsls_rti_pack_results(gsls_ctx* ctx, const double* u0, const gsls_admm_stats_t* stats, const double* cost,
+                          double* rec, void* stream) {
+  if (!ctx || !u0 || !stats || !stats->iterations || !stats->converged || !stats->rho_changes || !rec)
+    return fail_null("argument");
+  return rti_pack_results(ctx->impl, u0, stats, cost, rec, (cudaStream_t)stream);
 }
 
 }  // extern "C"

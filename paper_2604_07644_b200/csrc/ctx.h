@@ -79,6 +79,8 @@ struct Ctx {
   int* d_build_list = nullptr; // scratch list (batch): instances of a cache rebuild
   cudaStream_t side = nullptr;  // ADMM driver: rebuild + replay of the rebuilt instances, beside the others
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t step_side = nullptr;  // gsls_rti_step: the ADMM's first build beside the SLS chain
+  cudaEvent_t step_fork = nullptr, step_join = nullptr;
   int32_t* d_status = nullptr; // [batch] per-instance ADMM exit status
   int* d_counts = nullptr;     // [2] graph-captured ADMM loop: replay / build instance counts
   cudaStream_t body_stream = nullptr;  // capture stream of the captured loop's body graph

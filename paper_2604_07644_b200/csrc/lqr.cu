@@ -1097,6 +1097,9 @@ void ctx_destroy(Ctx* c) {
   if (c->body_stream) cudaStreamDestroy(c->body_stream);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->step_side) cudaStreamDestroy(c->step_side);
+  if (c->step_fork) cudaEventDestroy(c->step_fork);
+  if (c->step_join) cudaEventDestroy(c->step_join);
   if (c->sls) sls_destroy(c);
   for (void* p : c->allocs) cudaFree(p);
   delete c;

@@ -58,8 +58,18 @@ def pack_results(u0: torch.Tensor, iterations: torch.Tensor, converged: torch.Te
 
 
 def pack_engine(engine, out: torch.Tensor | None = None) -> torch.Tensor:
-    s = engine.stats
-    return pack_results(engine.u0, s.iterations, s.converged, s.rho_changes, engine.cost, out)
+    """The engine's record through the C ABI (gsls_rti_pack_results, one kernel)."""
+    import ctypes
+    from . import _native as nat
+    from .device import stream_ptr
+    if out is None:
+        out = torch.empty(engine.B, engine.u0.shape[1] + len(RESULT_FIELDS), dtype=torch.float64,
+                          device=engine.u0.device)
+    ss = engine.stats.cstruct()
+    nat.check(engine.ctx.lib.gsls_rti_pack_results(engine.ctx.handle, engine.u0.data_ptr(), ctypes.byref(ss),
+                                                   engine.cost.data_ptr(), out.data_ptr(), stream_ptr()),
+              "pack results")
+    return out
 
 
 def gather_results(local: torch.Tensor, world: int, out: torch.Tensor | None = None,

@@ -127,19 +127,10 @@ class RtiEngine:
         self.cost = d(batch)
         self._weights_written = False
         self.launches_per_step = 0
-        # side stream for the ADMM's first cache build, overlapped with the SLS synthesis
+        # the ADMM's first cache build runs on the context's side stream, overlapped with the
+        # SLS synthesis (csrc/rti.cu); GSLS_OVERLAP=0 serializes it (phase timing)
         import os
         self.overlap = robust and os.environ.get("GSLS_OVERLAP", "1") != "0"
-        self.side = torch.cuda.Stream(device=dev) if self.overlap else None
-
-    # -- pieces ------------------------------------------------------------------
-    def _reset_admm(self, warm: DeviceAdmmState | None = None):
-        st = self.state
-        if warm is None:
-            st.z.zero_(); st.lam.zero_(); st.y.zero_()
-            st.rho.fill_(float(self.admm_settings.rho0))
-            st.generation.zero_(); st.iteration.zero_()
-            st.r_primal.fill_(np.inf); st.r_dual.fill_(np.inf)
 
     def step(self, xbar0: torch.Tensor, prev_x: torch.Tensor, prev_u: torch.Tensor, tau=None, tau_term=None,
              use_tau: bool | None = None, E: torch.Tensor | None = None, warm_admm: bool = False):
@@ -154,24 +145,19 @@ class RtiEngine:
             if t is not None and (tuple(t.shape) != shape or t.dtype != F64 or not t.is_cuda or not t.is_contiguous()):
                 raise ValueError(f"{name} must be a contiguous float64 CUDA tensor of shape {shape}, "
                                  f"got {tuple(t.shape)} {t.dtype} contiguous={t.is_contiguous()}")
+        # the whole step is one C-ABI call (csrc/rti.cu): linearize -> [SLS chain, with the
+        # ADMM's first factorization on the context's side stream] -> ADMM -> duals -> plan
+        a = nat.RtiStepArgs()
+        dm = self.dm
+        a.lin.model_id, a.lin.params, a.lin.cons_offset = dm.model_id, dm.params.data_ptr(), dm.cons_offset
+        a.lin.x, a.lin.u, a.lin.h, a.lin.hf, a.lin.xbar0 = prev_x.data_ptr(), prev_u.data_ptr(), None, None, _p(xbar0)
+        a.lin.Qw, a.lin.Rw, a.lin.QNw = dm.Qw.data_ptr(), dm.Rw.data_ptr(), dm.QNw.data_ptr()
+        a.lin.xref, a.lin.uref, a.lin.E_const = dm.xref.data_ptr(), dm.uref.data_ptr(), dm.E.data_ptr()
+        a.lin.write_weights = int(not self._weights_written)
         qs = qp.cstruct()
-        linearize_into(ctx, self.dm, qp, prev_x, prev_u, xbar0=xbar0, E=self.E,
-                       write_weights=not self._weights_written)
-        self._weights_written = True
-        if E is not None:
-            self.E.copy_(E)
-        if not warm_admm:
-            self._reset_admm()
-        prebuilt = False
-        if self.robust and self.overlap:
-            # The ADMM's first factorization depends on A, B, Q, R, S, C, D and rho only, not on
-            # the tightened offsets f: build it on a side stream while the SLS synthesis runs.
-            main = torch.cuda.current_stream()
-            self.side.wait_stream(main)
-            with torch.cuda.stream(self.side):
-                nat.check(lib.gsls_admm_build_cache(ctx.handle, ctypes.byref(qs), self.state.rho.data_ptr(),
-                                                    self.side.cuda_stream), "admm build")
-            prebuilt = True
+        a.qp = ctypes.pointer(qs)
+        a.E, a.E_in = self.E.data_ptr(), _p(E)
+        a.robust, a.warm_admm, a.no_overlap = int(self.robust), int(warm_admm), int(not self.overlap)
         if self.robust:
             if tau is not None:
                 self.tau.copy_(tau)
@@ -179,30 +165,21 @@ class RtiEngine:
                 self.tau_valid = True
             if use_tau is None:
                 use_tau = self.tau_valid
-            nat.check(lib.gsls_sls_assemble(ctx.handle, ctypes.byref(qs), _p(self.tau) if use_tau else None,
-                                            _p(self.tau_term) if use_tau else None, self.Qbar.data_ptr(),
-                                            self.Rbar.data_ptr(), self.QbarN.data_ptr(), 0, S), "assemble_costs")
-            nat.check(lib.gsls_sls_synthesize(ctx.handle, ctypes.byref(qs), self.E.data_ptr(), S), "synthesize")
-            nat.check(lib.gsls_sls_tighten(ctx.handle, ctypes.byref(qs), _p(self.h), _p(self.hf), S), "tighten")
-            nat.check(lib.gsls_apply_tightening(ctx.handle, _p(qp.f), _p(qp.fN), _p(self.h), _p(self.hf), S),
-                      "apply_tightening")
-        if prebuilt:
-            torch.cuda.current_stream().wait_stream(self.side)
-        sa, ss, st = self.state.cstruct(), self.stats.cstruct(), self.admm_settings.cstruct()
-        nat.check(lib.gsls_admm_solve_qp(ctx.handle, ctypes.byref(qs), ctypes.byref(st), ctypes.byref(sa),
-                                         ctypes.byref(ss), self.dx.data_ptr(), _p(self.du), S), "admm.solve_qp")
+            a.use_tau = int(bool(use_tau))
+            a.Qbar, a.Rbar, a.QbarN = self.Qbar.data_ptr(), self.Rbar.data_ptr(), self.QbarN.data_ptr()
+            a.tau, a.tau_term, a.beta, a.beta_term = (_p(t) for t in (self.tau, self.tau_term, self.beta,
+                                                                      self.beta_term))
+            a.eps = float(self.settings.eps)
+            a.h, a.hf = _p(self.h), _p(self.hf)
+        a.admm, a.state, a.stats = self.admm_settings.cstruct(), self.state.cstruct(), self.stats.cstruct()
+        a.dx, a.du = self.dx.data_ptr(), _p(self.du)
+        a.plan_x, a.plan_u, a.warm_x, a.warm_u = (t.data_ptr() for t in (self.plan_x, self.plan_u, self.warm_x,
+                                                                          self.warm_u))
+        a.u0, a.cost = self.u0.data_ptr(), self.cost.data_ptr()
+        nat.check(lib.gsls_rti_step(ctx.handle, ctypes.byref(a), S), "rti step")
+        self._weights_written = True
         if self.robust:
-            eps = float(self.settings.eps)
-            nat.check(lib.gsls_sls_duals(ctx.handle, ctypes.byref(qs), self.state.lam.data_ptr(), eps, 1, 1,
-                                         _p(self.tau), _p(self.tau_term), _p(self.beta), _p(self.beta_term), S),
-                      "compute_duals")
             self.tau_valid = True
-        nat.check(lib.gsls_rti_apply(ctx.handle, prev_x.data_ptr(), prev_u.data_ptr(), self.dx.data_ptr(),
-                                     self.du.data_ptr(), self.plan_x.data_ptr(), self.plan_u.data_ptr(),
-                                     self.warm_x.data_ptr(), self.warm_u.data_ptr(), self.u0.data_ptr(),
-                                     self.dm.Qw.data_ptr(), self.dm.Rw.data_ptr(), self.dm.QNw.data_ptr(),
-                                     self.dm.xref.data_ptr(), self.dm.uref.data_ptr(), self.cost.data_ptr(), S),
-                  "rti_apply")
         return self
 
     def capture(self, xbar0=None, prev_x=None, prev_u=None) -> "CapturedStep":

@@ -56,6 +56,18 @@ def test_lqr_matches_riccati_oracle(gs):
         assert rel(getattr(sol, fld), getattr(ref, fld)) <= TOL
 
 
+@pytest.mark.parametrize("nx", [63, 65, 66, 67, 68, 76, 80])
+def test_lqr_combine_sizes_64_to_80(gs, nx):
+    """The k_cvf_combine<80> Gauss-Jordan column tiles (gj.cuh, NP = 80: 5 columns per
+    row thread) at the state sizes where lds_of(n) and the tile width disagree, and the
+    64-wide kernel's upper edge, against the float64 scan oracle."""
+    lqr, _ = gs
+    qp = P.random_ltv_qp(np.random.default_rng(nx), nx, 7, 9)
+    sol, ref = lqr.solve(qp), olqr.solve(qp)
+    for fld in ("dx", "du", "K", "k"):
+        assert rel(getattr(sol, fld), getattr(ref, fld)) <= TOL, fld
+
+
 def test_lqr_scalar_analytic_and_terminal_only(gs):
     lqr, _ = gs
     sol = lqr.solve(P.scalar_qp())

@@ -32,6 +32,40 @@ def test_library_built_and_exports_header():
     assert _native.load(require_device=False).gsls_version() == 1
 
 
+ABI_STRUCTS = {  # C typedef (include/gsls.h) -> the ctypes mirror the Python shim passes
+    "gsls_dims_t": _native.Dims, "gsls_error_t": _native.Error, "gsls_qp_t": _native.Qp,
+    "gsls_admm_settings_t": _native.AdmmSettings, "gsls_admm_state_t": _native.AdmmState,
+    "gsls_admm_stats_t": _native.AdmmStats, "gsls_linearize_args_t": _native.LinArgs,
+    "gsls_rollout_args_t": _native.RolloutArgs, "gsls_rollout_out_t": _native.RolloutOut,
+    "gsls_rti_step_args_t": _native.RtiStepArgs,
+}
+
+
+def test_abi_struct_layouts_match_header(tmp_path):
+    """Every struct the C ABI takes has the same size and field offsets in C (gcc on
+    include/gsls.h) as in its ctypes mirror."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "gsls.h"', "int main(void) {"]
+    for cname, py in ABI_STRUCTS.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'  printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(line.rsplit(" ", 1) for line in subprocess.run([str(exe)], check=True, capture_output=True,
+                                                                   text=True).stdout.splitlines())
+    for cname, py in ABI_STRUCTS.items():
+        assert int(got[f"{cname} size"]) == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert int(got[f"{cname} {f}"]) == getattr(py, f).offset, (cname, f)
+
+
 @pytest.mark.parametrize("length", [1, 2, 3, 8, 17, 26, 51, 100, 1000])
 @pytest.mark.parametrize("reverse", [False, True])
 def test_plan_matches_reference_tree(length, reverse):
