@@ -976,7 +976,8 @@ constexpr int kTraceIter = 5;  // GSLS_REPLAY_TRACE samples this ADMM iteration 
 
 struct StagedLayout {
   // byte offsets into dynamic shared memory
-  int ring, pv, bv, cb, t1, t2, z, lam, y, w, kf, dx0, part, red, redall, masks, ops, phys, items, phase, mbar, total;
+  int ring, pv, bv, cb, t1, t2, z, lam, y, w, kf, dx0, part, red, redall, masks, ops, phys, items, gseq, phase, mbar,
+      total;
   int slot;  // bytes per ring slot
   int R;     // ring slots
   int max_items, nphase;
@@ -1005,7 +1006,15 @@ __host__ __device__ inline int stage_slot_bytes(int n, int m, int c, int ld2n, i
   return ((b * 4 + 127) / 128) * 128;
 }
 
-__host__ __device__ inline StagedLayout staged_layout(const DevLqr& L, int max_layer, int R, int max_items) {
+__host__ __device__ inline int staged_part_tasks(const DevLqr& L, int G) {  // partial tasks per group half
+  const int W = (kReplayThreads / 32) / G;
+  int rows = 2 * L.n;
+  rows = rows > L.c ? rows : L.c;
+  const int rb = (rows + 31) / 32;
+  return W > rb ? W : rb;
+}
+
+__host__ __device__ inline StagedLayout staged_layout(const DevLqr& L, int max_layer, int R, int max_items, int G) {
   StagedLayout S{};
   const int n = L.n, m = L.m, N = L.N;
   int o = 0;
@@ -1024,7 +1033,11 @@ __host__ __device__ inline StagedLayout staged_layout(const DevLqr& L, int max_l
   S.w = take(L.mtot * 8, 16);
   S.kf = take(N * m * 8, 16);
   S.dx0 = take(n * 8, 16);
-  S.part = take(2 * kReplayThreads * 8, 16);  // two halves x 16 (row block, slice) tasks x 32 rows
+  {  // per item group: two halves x max(W, row blocks) (row block, slice) tasks x 32 rows; also
+     // holds the setup's item list (<= kReplayThreads int2)
+    const int pb = G * 2 * staged_part_tasks(L, G) * 32 * 8;
+    S.part = take(pb > 2 * kReplayThreads * 8 ? pb : 2 * kReplayThreads * 8, 16);
+  }
   S.red = take(64 * 8, 16);
   S.redall = take(2 * kMaxCluster * 8, 16);
   S.masks = take((L.cvf_nslots + L.cot_nslots) * 4, 16);
@@ -1032,6 +1045,7 @@ __host__ __device__ inline StagedLayout staged_layout(const DevLqr& L, int max_l
   S.phys = take((L.cvf_nslots + L.cot_nslots) * 4, 16);
   S.max_items = max_items;
   S.items = take(S.max_items * (int)sizeof(ItemDesc), 16);
+  S.gseq = take((S.max_items + 2 * 8 + 2) * 4, 16);  // per-group item sequences + offsets (<= 8 groups)
   S.nphase = L.cvf_layers + L.cot_layers + 5;
   S.phase = take((S.nphase + 1) * 4, 16);
   S.mbar = take(R * 8, 8);
@@ -1077,6 +1091,8 @@ struct ItemEpi {
   int e0;              // E_G: first stacked constraint row of the stage
 };
 
+// G item groups (compile-time: the index arithmetic of the hot loop folds for each size)
+template <int G>
 __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a, int R, int max_items) {
   const DevLqr& L = a.L;
   if (a.count && (int)blockIdx.y >= *a.count) return;
@@ -1092,7 +1108,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   cl.rank = cluster_rank();
   cl.cs = cluster_size();
   const int rank = (int)cl.rank, cs = (int)cl.cs;
-  const StagedLayout SL = staged_layout(L, a.max_layer, R, max_items);
+  const StagedLayout SL = staged_layout(L, a.max_layer, R, max_items, G);
   extern __shared__ __align__(128) unsigned char smb[];
   unsigned char* ring = smb + SL.ring;
   double* pv = reinterpret_cast<double*>(smb + SL.pv);
@@ -1121,6 +1137,8 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   ItemDesc* desc = reinterpret_cast<ItemDesc*>(smb + SL.items);
   int2* items = reinterpret_cast<int2*>(smb + SL.part);  // setup only: (kind | which << 8 | loc << 16, index)
   int* phase_off = reinterpret_cast<int*>(smb + SL.phase);
+  int* gseq = reinterpret_cast<int*>(smb + SL.gseq);  // [P] items in group consumption order
+  int* goff = gseq + max_items;                        // [G + 1] group offsets into gseq
   uint64_t* full = reinterpret_cast<uint64_t*>(smb + SL.mbar);
   __shared__ int s_flag, s_nitems;
   __shared__ double s_rho;
@@ -1191,6 +1209,14 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
     for (int k = rank; k < N; k += cs) add(IT_G, 0, k);
     phase_off[ph] = ni;
     s_nitems = ni;
+    // group g consumes the items j of every phase with (j - phase start) = g (mod G), in order
+    int o = 0;
+    for (int g = 0; g < G; ++g) {
+      goff[g] = o;
+      for (int q = 0; q < ph; ++q)
+        for (int jj = phase_off[q] + g; jj < phase_off[q + 1]; jj += G) gseq[o++] = jj;
+    }
+    goff[G] = o;
   }
   // fence: mbarrier inits visible to the async proxy before the first bulk copy
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1270,8 +1296,9 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
           break;
       }
       const int RB = (d.rows + 31) >> 5;
-      int kslog = 4;  // KS = 16 / RB (power of two): one partial half holds <= 16 (row block, slice) tasks
-      while (kslog > 0 && (RB << kslog) > 16) --kslog;
+      const int Wg = (nthr >> 5) / G;  // warps of an item group
+      int kslog = 0;  // KS = W / RB (power of two): one group's partial half holds <= max(W, RB) tasks
+      while ((1 << (kslog + 1)) <= Wg && (RB << (kslog + 1)) <= Wg) ++kslog;  // (rows = 0: KS = W)
       const int KS = 1 << kslog, K = d.K1 + d.K2;
       d.kslog = kslog;
       d.kc = (((K + KS - 1) / KS) + 3) & ~3;
@@ -1279,14 +1306,19 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
     }
   }
   __syncthreads();
-  int pi = 0, pslot = 0;  // producer (thread 0): next item (mod P), slot to fill
-  auto issue = [&]() {
-    if (tid != nthr - 32 || P == 0) return;  // last warp: off the epilogue rows (tid < rows)
-    bulk_load(ring + (size_t)pslot * SL.slot, desc[pi].src, desc[pi].bytes, full + pslot);
-    if (++pi == P) pi = 0;
-    if (++pslot == R) pslot = 0;
-  };
-  for (int i = 0; i < R; ++i) issue();
+  // Ring schedule: group g owns slots g, g + G, ... (Rg = R / G of them) and consumes its
+  // item sequence gseq[goff[g] ..] in order, so every slot has one consumer that waits on
+  // its phases in order (no mbarrier parity aliasing between groups).  The group's t-th
+  // item of this launch sits in slot g + G (t mod Rg); after reading it the group refills
+  // the slot with its item t + Rg.
+  const int W = (nthr >> 5) / G, grp = warp / W, wg = warp - grp * W, gtid = tid - grp * W * 32, gsz = W * 32;
+  const int Rg = R / G, g0 = goff[grp], Pg = goff[grp + 1] - g0;
+  const int issuer = gsz - 32;  // the group's last warp: off the epilogue's first rows
+  if (gtid == issuer && Pg > 0)
+    for (int t = 0; t < Rg; ++t) {
+      const int jj = gseq[g0 + t % Pg], sl = grp + G * t;
+      bulk_load(ring + (size_t)sl * SL.slot, desc[jj].src, desc[jj].bytes, full + sl);
+    }
 
   double rho = a.state.rho[inst];
   int it = a.stats.iterations[inst];
@@ -1304,33 +1336,35 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   }
   cl.sync();  // every replica exists before the first remote store
 
-  int cslot = 0, cpar = 0, ph2 = 0;  // consumer: slot, mbarrier parity, partial-sum half
+  // Item groups: G groups of W warps take the items of a phase round-robin, each group with
+  // its own named barrier, ring slots and partial-sum halves, so up to G items are in flight
+  // per CTA (small clusters hold many items per rank and phase; G = 1 at 16-CTA clusters).
+  const int PT = staged_part_tasks(L, G) * 32;  // doubles per group half
+  int half = 0, gi = 0, gpar = 0, gpos = 0;  // partial half; ring position (0 .. Rg-1), parity; sequence position
   const int nph = L.cvf_layers + L.cot_layers + 4;  // P1, CVF layers, FF1, FF2, COT layers, G
   const int ph_ff1 = L.cvf_layers + 1, ph_g = nph - 1;
 
   int tr_it = 0;
   for (;;) {
     double rp = 0.0, rdz = 0.0;
-    int j = 0;
     if (a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == kTraceIter) a.trace[250] = clock64();
     for (int ph = 0; ph < nph; ++ph) {
       // ---- the phase's items: one matvec each, read from the ring ------------------------
-      for (; j < phase_off[ph + 1]; ++j) {
-        const bool tq = a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == kTraceIter && j < 20;
-        long long q0 = tq ? clock64() : 0, q1 = 0, q2 = 0, q3 = 0, q4 = 0;
+      for (int j = phase_off[ph] + grp; j < phase_off[ph + 1]; j += G) {
         const ItemDesc& d = desc[j];
         const int rows = d.rows, ld = d.ld, K1 = d.K1, kind = d.kind;
         const double* x1 = reinterpret_cast<const double*>(smb + d.x1);
         const double* x2 = reinterpret_cast<const double*>(smb + (d.x2 < 0 ? d.x1 : d.x2));
-        double pre_v = 0.0;
-        if (tid < rows && d.pre) pre_v = d.pre[tid] + (d.pre2 ? v0[tid] : 0.0);
-        mbar_wait(full + cslot, (unsigned)cpar);
-        if (tq) q1 = clock64();
-        const float* M = reinterpret_cast<const float*>(ring + (size_t)cslot * SL.slot);
-        double* pt = part + ph2 * kReplayThreads;
+        double pre_v = 0.0;  // global addend of this thread's first row, loaded before the wait
+        if (gtid < rows && d.pre) pre_v = d.pre[gtid] + (d.pre2 ? v0[gtid] : 0.0);
+        const int slot = grp + G * gi;
+        mbar_wait(full + slot, (unsigned)gpar);
+        const float* M = reinterpret_cast<const float*>(ring + (size_t)slot * SL.slot);
+        double* pt = part + (size_t)(2 * grp + half) * PT;
         const int kslog = d.kslog, KS = 1 << kslog, kc = d.kc, K = K1 + d.K2;
-        if (warp < (((rows + 31) >> 5) << kslog)) {
-          const int rb = warp >> kslog, ks = warp & (KS - 1);
+        const int ntask = ((rows + 31) >> 5) << kslog;
+        for (int t = wg; t < ntask; t += W) {
+          const int rb = t >> kslog, ks = t & (KS - 1);
           const int rq = lane & 7, gq = lane >> 3;
           const int row0 = rb * 32 + 4 * rq;
           const int k0 = ks * kc, k1 = min(K, k0 + kc);
@@ -1357,28 +1391,25 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
             a3 += __shfl_xor_sync(0xffffffffu, a3, o);
           }
           if (gq == 0) {
-            double* pp = pt + (warp << 5) + 4 * rq;  // (rb * KS + ks) * 32
+            double* pp = pt + (t << 5) + 4 * rq;  // (rb * KS + ks) * 32
             pp[0] = a0; pp[1] = a1; pp[2] = a2; pp[3] = a3;
           }
         }
-        // One barrier per item: the slot is refilled right after it and the partial
-        // sums alternate halves, so this epilogue overlaps the next item.
-        if (tq) q2 = clock64();
-        __syncthreads();
-        if (tq) q3 = clock64();
-        issue();
-        if (tq) q4 = clock64();
-        if (++cslot == R) { cslot = 0; cpar ^= 1; }
-        ph2 ^= 1;
-        if (tq) {
-          a.trace[100 + 5 * j] = q1 - q0; a.trace[101 + 5 * j] = q2 - q1; a.trace[102 + 5 * j] = q3 - q2;
-          a.trace[103 + 5 * j] = q4 - q3;
+        // One (group) barrier per item: the slot is refilled right after it and the partial
+        // sums alternate halves, so this epilogue overlaps the group's next item.
+        if (G == 1) __syncthreads();
+        else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(gsz) : "memory");
+        if (gtid == issuer) {  // the group's item Rg positions on (its sequence wraps per iteration)
+          const int jn = gseq[g0 + (gpos + Rg) % Pg];
+          bulk_load(ring + (size_t)slot * SL.slot, desc[jn].src, desc[jn].bytes, full + slot);
         }
-        if (tid < rows) {
-          const double* pr = pt + (((tid >> 5) << kslog) << 5) + (tid & 31);
+        if (++gpos == Pg) gpos = 0;
+        if (++gi == Rg) { gi = 0; gpar ^= 1; }
+        half ^= 1;
+        auto epi = [&](int i, double pv_) {
+          const double* pr = pt + (((i >> 5) << kslog) << 5) + (i & 31);
           double sum = 0.0;
           for (int ks = 0; ks < KS; ++ks) sum += pr[ks << 5];
-          const int i = tid;
           double* dst = reinterpret_cast<double*>(smb + d.dst);
           switch (kind) {
             case IT_CVF1:
@@ -1386,14 +1417,14 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
               cl.put_mask(dst + i, reinterpret_cast<const double*>(smb + d.add)[i] + d.sgn * sum, d.mask);
               break;
             case IT_P1:
-              cl.put_mask(i < n ? dst + i : reinterpret_cast<double*>(smb + d.dst2) + (i - n), pre_v + sum, d.mask);
+              cl.put_mask(i < n ? dst + i : reinterpret_cast<double*>(smb + d.dst2) + (i - n), pv_ + sum, d.mask);
               break;
-            case IT_FF1: dst[i] = pre_v + sum; break;
-            case IT_FF2: cl.put_mask(dst + i, pre_v + sum, d.mask); break;
+            case IT_FF1: dst[i] = pv_ + sum; break;
+            case IT_FF2: cl.put_mask(dst + i, pv_ + sum, d.mask); break;
             default: {  // z = min(G + y, f); lam += rho (G - z); y = lam / rho (admm.py:130-135)
               const int e = d.e0 + i;
               const double zo = z[e];
-              const double zn = fmin(sum + y[e], pre_v);
+              const double zn = fmin(sum + y[e], pv_);
               const double ln = lam[e] + rho * (sum - zn);
               const double yn = ln / rho;
               lam[e] = ln;
@@ -1404,7 +1435,10 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
               rdz = fmax(rdz, fabs(zn - zo));
             }
           }
-        }
+        };
+        if (gtid < rows) epi(gtid, pre_v);
+        for (int i = gtid + gsz; i < rows; i += gsz)  // rows beyond the group (P1 items of n > 64 at W = 4)
+          epi(i, d.pre ? d.pre[i] + (d.pre2 ? v0[i] : 0.0) : 0.0);
       }
       // ---- phase boundary -----------------------------------------------------------
       if (a.trace && tid == 0 && rank == 0 && blockIdx.y == 0 && tr_it == kTraceIter && 2 * ph + 1 < 250)
@@ -1500,11 +1534,12 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
     if (flag == 0) continue;
 
     // ---- exit: drain the in-flight bulk copies, write back what this rank owns -------
-    if (P > 0)  // the R in-flight copies land in slots cslot, cslot + 1, ... in order
-      for (int q = 0, sl = cslot, pa = cpar; q < R; ++q) {
-        mbar_wait(full + sl, (unsigned)pa);
-        if (++sl == R) { sl = 0; pa ^= 1; }
+    if (Pg > 0)  // the group's Rg in-flight copies land in its next ring positions, in order
+      for (int q = 0, sl = gi, pa = gpar; q < Rg; ++q) {
+        mbar_wait(full + grp + G * sl, (unsigned)pa);
+        if (++sl == Rg) { sl = 0; pa ^= 1; }
       }
+    __syncthreads();
     const double rho_new = s_rho;
     auto owns_row = [&](int e) { return srank(e < N * c ? e / c : N) == rank; };
     double* zg = a.state.z + (size_t)inst * mtot;
@@ -1677,13 +1712,21 @@ static int launch_admm_staged(Ctx* c, ReplayArgs& a, int count, cudaStream_t st)
   const size_t limit = 227 * 1024 - 1024;
   static bool attrs_set = false;
   if (!attrs_set) {
-    GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_admm_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)limit));
-    GSLS_CUDA_CHECK(cudaFuncSetAttribute((const void*)k_admm_staged, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    for (const void* k : {(const void*)k_admm_staged<1>, (const void*)k_admm_staged<2>, (const void*)k_admm_staged<4>}) {
+      GSLS_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit));
+      GSLS_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
     attrs_set = true;
   }
   // items per rank bound for the largest cluster this batch can use (fewer ranks -> more items)
-  const int cs0 = replay_cluster(c, count, limit, (const void*)k_admm_staged);  // occupancy at the largest footprint
+  const int cs0 = replay_cluster(c, count, limit, (const void*)k_admm_staged<1>);  // occupancy at the largest footprint
+  // item groups (k_admm_staged): small clusters hold many items per rank and phase, so up to
+  // 4 items run concurrently there; 16-CTA clusters (batch-1 latency) hold 1-2 per phase
+  // (measured, q61 / h75: 4 groups of 4 warps on clusters <= 4 cut the B = 1024 ADMM tail
+  // waves 1.66 -> 0.94 ms; at 16-CTA clusters 2 groups are fastest for batch-1 latency)
+  int G = cs0 <= 4 ? 4 : 2;
+  if (const char* ge = getenv("GSLS_STAGED_GROUPS")) G = std::max(1, std::min(8, atoi(ge)));
+  G = G >= 4 ? 4 : (G >= 2 ? 2 : 1);  // groups of 4 / 8 / 16 warps (ring slots per group >= 2)
   const int Nn = c->dims.N;
   auto cdiv = [](int x, int y) { return (x + y - 1) / y; };
   int max_items = 4 * cdiv(Nn, cs0) + 8;
@@ -1692,14 +1735,21 @@ static int launch_admm_staged(Ctx* c, ReplayArgs& a, int count, cudaStream_t st)
   if (max_items > kReplayThreads) return GSLS_ERR_TOO_LARGE;  // setup list lives in the partial buffer
   int R = 0;
   size_t sb = 0;
-  for (int r = 8; r >= 2; --r) {
-    const StagedLayout SL = staged_layout(c->dev, a.max_layer, r, max_items);
-    if ((size_t)SL.total <= limit) { R = r; sb = SL.total; break; }
+  int min_rg = 1;
+  if (const char* e = getenv("GSLS_STAGED_MIN_RG")) min_rg = std::max(1, atoi(e));
+  for (;;) {  // R: the largest multiple of G (ring slots per group) that fits, >= min_rg per group if G > 1
+    for (int r = 8; r >= 2; --r) {
+      if (r % G || (G > 1 && r / G < min_rg)) continue;
+      const StagedLayout SL = staged_layout(c->dev, a.max_layer, r, max_items, G);
+      if ((size_t)SL.total <= limit) { R = r; sb = SL.total; break; }
+    }
+    if (R || G == 1) break;
+    G >>= 1;
   }
   if (R == 0) return GSLS_ERR_TOO_LARGE;
   const int cs = cs0;
   if (getenv("GSLS_REPLAY_VERBOSE"))
-    fprintf(stderr, "staged replay: count=%d cs=%d R=%d max_items=%d smem=%zu\n", count, cs, R, max_items, sb);
+    fprintf(stderr, "staged replay: count=%d cs=%d R=%d G=%d max_items=%d smem=%zu\n", count, cs, R, G, max_items, sb);
   // One CTA per instance (large batches): k_replay's layer-parallel rounds keep more
   // matrices in flight than the one-item-at-a-time stream; GSLS_REPLAY_STAGED=1 forces it.
   const char* force = getenv("GSLS_REPLAY_STAGED");
@@ -1723,7 +1773,9 @@ static int launch_admm_staged(Ctx* c, ReplayArgs& a, int count, cudaStream_t st)
   if (tracing) GSLS_CUDA_CHECK(cudaMemsetAsync(trace, 0, 256 * sizeof(unsigned long long), st));
   {
     ProfScope ps(P_REPLAY, st, (double)count);
-    GSLS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_admm_staged, a, R, max_items));
+    if (G == 4) GSLS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_admm_staged<4>, a, R, max_items));
+    else if (G == 2) GSLS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_admm_staged<2>, a, R, max_items));
+    else GSLS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_admm_staged<1>, a, R, max_items));
     GSLS_CUDA_CHECK(cudaGetLastError());
   }
   if (tracing) {
