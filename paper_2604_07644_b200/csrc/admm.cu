@@ -1340,7 +1340,8 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   // its own named barrier, ring slots and partial-sum halves, so up to G items are in flight
   // per CTA (small clusters hold many items per rank and phase; G = 1 at 16-CTA clusters).
   const int PT = staged_part_tasks(L, G) * 32;  // doubles per group half
-  int half = 0, gi = 0, gpar = 0, gpos = 0;  // partial half; ring position (0 .. Rg-1), parity; sequence position
+  // partial half; ring position (0 .. Rg-1) and parity; sequence position of the next refill
+  int half = 0, gi = 0, gpar = 0, rpos = Pg > 0 ? Rg % Pg : 0;
   const int nph = L.cvf_layers + L.cot_layers + 4;  // P1, CVF layers, FF1, FF2, COT layers, G
   const int ph_ff1 = L.cvf_layers + 1, ph_g = nph - 1;
 
@@ -1363,7 +1364,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
         double* pt = part + (size_t)(2 * grp + half) * PT;
         const int kslog = d.kslog, KS = 1 << kslog, kc = d.kc, K = K1 + d.K2;
         const int ntask = ((rows + 31) >> 5) << kslog;
-        for (int t = wg; t < ntask; t += W) {
+        for (int t = wg; t < ntask; t += (G == 1 ? ntask : W)) {  // G = 1: ntask <= 16 warps, one task each
           const int rb = t >> kslog, ks = t & (KS - 1);
           const int rq = lane & 7, gq = lane >> 3;
           const int row0 = rb * 32 + 4 * rq;
@@ -1400,10 +1401,10 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
         if (G == 1) __syncthreads();
         else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(gsz) : "memory");
         if (gtid == issuer) {  // the group's item Rg positions on (its sequence wraps per iteration)
-          const int jn = gseq[g0 + (gpos + Rg) % Pg];
+          const int jn = gseq[g0 + rpos];
           bulk_load(ring + (size_t)slot * SL.slot, desc[jn].src, desc[jn].bytes, full + slot);
         }
-        if (++gpos == Pg) gpos = 0;
+        if (++rpos == Pg) rpos = 0;
         if (++gi == Rg) { gi = 0; gpar ^= 1; }
         half ^= 1;
         auto epi = [&](int i, double pv_) {
@@ -1437,7 +1438,8 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
           }
         };
         if (gtid < rows) epi(gtid, pre_v);
-        for (int i = gtid + gsz; i < rows; i += gsz)  // rows beyond the group (P1 items of n > 64 at W = 4)
+        if (G > 1)
+          for (int i = gtid + gsz; i < rows; i += gsz)  // rows beyond the group (P1 items of n > 64 at W = 4)
           epi(i, d.pre ? d.pre[i] + (d.pre2 ? v0[i] : 0.0) : 0.0);
       }
       // ---- phase boundary -----------------------------------------------------------
