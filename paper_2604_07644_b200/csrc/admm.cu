@@ -1027,9 +1027,7 @@ __host__ __device__ inline StagedLayout staged_layout(const DevLqr& L, int max_l
   S.cb = take(L.cot_nphys * n * 8, 16);
   S.t1 = take(0, 16);  // (unused since the one-round CVF replay)
   S.t2 = take(0, 16);
-  S.z = take(L.mtot * 8, 16);
-  S.lam = take(L.mtot * 8, 16);
-  S.y = take(L.mtot * 8, 16);
+  S.z = S.lam = S.y = -1;  // z, lam, y stay in global memory (only their owner rows' G epilogue touches them)
   S.w = take(L.mtot * 8, 16);
   S.kf = take(N * m * 8, 16);
   S.dx0 = take(n * 8, 16);
@@ -1114,9 +1112,12 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   double* pv = reinterpret_cast<double*>(smb + SL.pv);
   double* bv = reinterpret_cast<double*>(smb + SL.bv);
   double* cb = reinterpret_cast<double*>(smb + SL.cb);
-  double* z = reinterpret_cast<double*>(smb + SL.z);
-  double* lam = reinterpret_cast<double*>(smb + SL.lam);
-  double* y = reinterpret_cast<double*>(smb + SL.y);
+  // z, lam, y of the constraint rows live in global memory: a row is read and written only by
+  // its owning rank's G epilogue, once per iteration, with the reads issued before the item's
+  // wait (shared memory holds w = y - z, the vector the matvecs read)
+  double* z = a.state.z + (size_t)inst * L.mtot;
+  double* lam = a.state.lam + (size_t)inst * L.mtot;
+  double* y = a.state.y + (size_t)inst * L.mtot;
   double* w = reinterpret_cast<double*>(smb + SL.w);
   double* kf = reinterpret_cast<double*>(smb + SL.kf);
   double* dx0s = reinterpret_cast<double*>(smb + SL.dx0);
@@ -1323,15 +1324,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
   double rho = a.state.rho[inst];
   int it = a.stats.iterations[inst];
   {
-    const double* zg = a.state.z + (size_t)inst * mtot;
-    const double* lg = a.state.lam + (size_t)inst * mtot;
-    const double* yg = a.state.y + (size_t)inst * mtot;
-    for (int e = tid; e < mtot; e += nthr) {
-      z[e] = zg[e];
-      lam[e] = lg[e];
-      y[e] = yg[e];
-      w[e] = yg[e] - zg[e];
-    }
+    for (int e = tid; e < mtot; e += nthr) w[e] = y[e] - z[e];
     for (int i = tid; i < n; i += nthr) dx0s[i] = a.qp.dx0[(size_t)inst * n + i];
   }
   cl.sync();  // every replica exists before the first remote store
@@ -1358,6 +1351,13 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
         const double* x2 = reinterpret_cast<const double*>(smb + (d.x2 < 0 ? d.x1 : d.x2));
         double pre_v = 0.0;  // global addend of this thread's first row, loaded before the wait
         if (gtid < rows && d.pre) pre_v = d.pre[gtid] + (d.pre2 ? v0[gtid] : 0.0);
+        double zo_v = 0.0, y_v = 0.0, l_v = 0.0;  // G rows: the ADMM state, loaded before the wait
+        if (kind == IT_G && gtid < rows) {
+          const int e = d.e0 + gtid;
+          zo_v = z[e];
+          y_v = y[e];
+          l_v = lam[e];
+        }
         const int slot = grp + G * gi;
         mbar_wait(full + slot, (unsigned)gpar);
         const float* M = reinterpret_cast<const float*>(ring + (size_t)slot * SL.slot);
@@ -1424,9 +1424,10 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
             case IT_FF2: cl.put_mask(dst + i, pv_ + sum, d.mask); break;
             default: {  // z = min(G + y, f); lam += rho (G - z); y = lam / rho (admm.py:130-135)
               const int e = d.e0 + i;
-              const double zo = z[e];
-              const double zn = fmin(sum + y[e], pv_);
-              const double ln = lam[e] + rho * (sum - zn);
+              const bool own = i == gtid;
+              const double zo = own ? zo_v : z[e];
+              const double zn = fmin(sum + (own ? y_v : y[e]), pv_);
+              const double ln = (own ? l_v : lam[e]) + rho * (sum - zn);
               const double yn = ln / rho;
               lam[e] = ln;
               y[e] = yn;
@@ -1544,15 +1545,9 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_admm_staged(ReplayArgs a,
     __syncthreads();
     const double rho_new = s_rho;
     auto owns_row = [&](int e) { return srank(e < N * c ? e / c : N) == rank; };
-    double* zg = a.state.z + (size_t)inst * mtot;
-    double* lg = a.state.lam + (size_t)inst * mtot;
-    double* yg = a.state.y + (size_t)inst * mtot;
-    for (int e = tid; e < mtot; e += nthr)
-      if (owns_row(e)) {
-        zg[e] = z[e];
-        lg[e] = lam[e];
-        yg[e] = (rho_new != rho) ? lam[e] / rho_new : y[e];  // a committed change rescales y (admm.py:149)
-      }
+    if (rho_new != rho)  // a committed change rescales y (admm.py:149); z, lam are already in place
+      for (int e = tid; e < mtot; e += nthr)
+        if (owns_row(e)) y[e] = lam[e] / rho_new;
     if (flag == 1) {
       double* gdx = a.dx + (size_t)inst * (N + 1) * n;
       double* gdu = a.du + (size_t)inst * N * m;
