@@ -57,11 +57,11 @@ template <class Epi>
 __device__ inline void gemm_tn_mn(int M, int Nc, int K, const float* At, int lda, const float* B, int ldb,
                                   Epi epi) {
   const int TM = (M + 3) >> 2, TN = (Nc + 3) >> 2, tiles = TM * TN;
-  const int ks = gemm_ks(tiles, K);
+  const int ks = gemm_ks(tiles, K), kslog = __ffs(ks) - 1;  // ks: a power of two
   const int work = tiles * ks;
   for (int base = 0; base < work; base += blockDim.x) {
     const int t = base + threadIdx.x;
-    const int tile = t / ks, part = t - tile * ks;
+    const int tile = t >> kslog, part = t & (ks - 1);
     const bool valid = t < work;
     const int ti = valid ? tile / TN : 0, tj = valid ? tile - ti * TN : 0;
     float acc[4][4];
@@ -96,11 +96,11 @@ template <class Epi>
 __device__ inline void gemm_nn_mn(int M, int Nc, int K, const float* A, int lda, const float* B, int ldb,
                                   Epi epi) {
   const int TM = (M + 3) >> 2, TN = (Nc + 3) >> 2, tiles = TM * TN;
-  const int ks = gemm_ks(tiles, K);
+  const int ks = gemm_ks(tiles, K), kslog = __ffs(ks) - 1;  // ks: a power of two
   const int work = tiles * ks;
   for (int base = 0; base < work; base += blockDim.x) {
     const int t = base + threadIdx.x;
-    const int tile = t / ks, part = t - tile * ks;
+    const int tile = t >> kslog, part = t & (ks - 1);
     const bool valid = t < work;
     const int ti = valid ? tile / TN : 0, tj = valid ? tile - ti * TN : 0;
     float acc[4][4];

@@ -46,12 +46,28 @@ __device__ inline void cta_transpose(float* dst, const float* src, int lds, int 
 }
 
 // smem (lds) -> global (ldg) copy of an n x ldg(n) block, float4 rows.
+// Walks the (row, float4 column) chunks e = threadIdx.x, + blockDim.x, ... of an n x 4q
+// block with two integer divisions in total (the combine kernels' index math was a
+// visible share of their issue slots): f(i, j) with j the first float of the chunk.
+template <class F>
+__device__ __forceinline__ void cta_chunks(int n, int q, F f) {
+  const int nt = blockDim.x;
+  int i = threadIdx.x / q, j4 = threadIdx.x - i * q;
+  const int di = nt / q, dj = nt - di * q;
+  while (i < n) {
+    f(i, j4 << 2);
+    i += di;
+    j4 += dj;
+    if (j4 >= q) { j4 -= q; ++i; }
+  }
+}
+
 __device__ inline void cta_store(float* __restrict__ dst, const float* src, int lds, int n) {
   const int q = ldg_of(n) / 4;
-  for (int e = threadIdx.x; e < n * q; e += blockDim.x) {
-    const int i = e / q, j = (e - i * q) * 4;
-    *reinterpret_cast<float4*>(dst + (size_t)i * ldg_of(n) + j) = *reinterpret_cast<const float4*>(src + i * lds + j);
-  }
+  const int ld = q << 2;
+  cta_chunks(n, q, [&](int i, int j) {
+    *reinterpret_cast<float4*>(dst + (size_t)i * ld + j) = *reinterpret_cast<const float4*>(src + i * lds + j);
+  });
 }
 
 // ---- async copies -------------------------------------------------------------
@@ -71,10 +87,7 @@ __device__ inline void cp_async_wait() {
 // (ld = lds); the caller commits / waits.  Padding columns arrive as stored (zero).
 __device__ inline void cta_load_async(float* dst, int lds, const float* __restrict__ src, int n) {
   const int q = ldg_of(n) >> 2;
-  for (int e = threadIdx.x; e < n * q; e += blockDim.x) {
-    const int i = e / q, j = (e - i * q) << 2;
-    cp_async16(dst + i * lds + j, src + (size_t)i * (q << 2) + j);
-  }
+  cta_chunks(n, q, [&](int i, int j) { cp_async16(dst + i * lds + j, src + (size_t)i * (q << 2) + j); });
 }
 
 // ---- GEMM ---------------------------------------------------------------------
