@@ -27,6 +27,27 @@ __host__ __device__ inline int lds_of(int n) {
 }
 __host__ __device__ inline size_t mat_elems(int n) { return (size_t)n * ldg_of(n); }
 
+// Division by a runtime constant d >= 1 for 0 <= x < 2^31: q = umulhi(x, mul) >> sh with the
+// round-up multiplier mul = ceil(2^(31 + ceil(log2 d)) / d) (Granlund-Montgomery).  The small
+// per-cell kernels index their (row, column) loops with it instead of a ~20-instruction
+// integer division per iteration.
+struct FastDiv {
+  int d;
+  unsigned mul, sh;
+  __host__ __device__ void init(int dv) {
+    d = dv;
+    if (dv <= 1) { mul = 0; sh = 0; return; }
+    unsigned l = 0;
+    while ((1u << l) < (unsigned)dv) ++l;
+    const unsigned p = 31 + l;
+    mul = (unsigned)(((1ull << p) + (unsigned)dv - 1) / (unsigned)dv);
+    sh = p - 32;
+  }
+#ifdef __CUDACC__
+  __device__ __forceinline__ int div(int x) const { return d <= 1 ? x : (int)(__umulhi((unsigned)x, mul) >> sh); }
+#endif
+};
+
 // Per-instance error record.  Kernels run stages / cells / ops in parallel, but
 // the reference raises the FIRST failure of its sequential loops: spd_inverse
 // names the lowest stage (lqr.py:204-215), _locate_singular the first valid

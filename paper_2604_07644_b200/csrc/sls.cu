@@ -71,6 +71,7 @@ static ScanPlan merge_columns(int N, bool cvf, int j0 = 0, int j1 = -1) {
 
 struct DevSls {
   int n, m, c, nf, N, ldg, ncell, cmax;
+  FastDiv fd_ldg, fd_q4, fd_m, fd_n;  // ldg (= np), ldg / 4, m, n: the cell kernels' loop indices
   int j0, j1, cell0;  // column shard [j0, j1); ncell counts its cells, which start at global cell0
   const int2* cell_kj;
   const int* leaf_dead;  // per cell: bit 0 A, bit 1 A^T, bit 2 C of its CVF leaf never read
@@ -125,6 +126,10 @@ static int sls_init(Ctx* c) {
   DevSls& S = s->dev;
   const int N = d.N, n = d.nx, m = d.nu;
   S.n = n; S.m = m; S.c = d.nc; S.nf = d.nf; S.N = N; S.ldg = ldg_of(n);
+  S.fd_ldg.init(S.ldg);
+  S.fd_q4.init(S.ldg / 4);
+  S.fd_m.init(m);
+  S.fd_n.init(n);
   S.j0 = c->sls_j0;
   S.j1 = c->sls_j1 < 0 ? N : c->sls_j1;
   S.cell0 = cell_of(N, S.j0 + 1, S.j0);
@@ -215,14 +220,14 @@ __global__ void __launch_bounds__(256) k_sls_assemble(DevSls S, gsls_qp_t qp, co
   __syncthreads();
   const int na = s_nact;
   for (int e = threadIdx.x; e < na * n; e += blockDim.x) {
-    const int a = e / n, i = e - a * n, r = act[a];
+    const int a = S.fd_n.div(e), i = e - a * n, r = act[a];
     const double v = Cg[r * n + i];
     Cr[e] = v;
     Cw[e] = tg[r] * v;
   }
   if (!term)
     for (int e = threadIdx.x; e < na * m; e += blockDim.x) {
-      const int a = e / m, i = e - a * m, r = act[a];
+      const int a = S.fd_m.div(e), i = e - a * m, r = act[a];
       const double v = Dg[r * m + i];
       Dr[e] = v;
       Dw[e] = tg[r] * v;
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(256) k_sls_assemble(DevSls S, gsls_qp_t qp, co
   const float* Qb = term ? QbarN + (size_t)inst * wst * n * n : Qbar + (size_t)inst * wst * n * n;
   const int q4 = (n + 3) >> 2;
   for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
-    const int i = e / q4, j0 = (e - i * q4) << 2;
+    const int i = S.fd_q4.div(e), j0 = (e - i * q4) << 2;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int a = 0; a < na; ++a) {
       const double w = Cw[a * n + i];
@@ -248,14 +253,14 @@ __global__ void __launch_bounds__(256) k_sls_assemble(DevSls S, gsls_qp_t qp, co
   const float* Rb = Rbar + (size_t)inst * wst * m * m;
   double* Qu = S.Qu + cb * m * m;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    const int a = e / m, b2 = e - a * m;
+    const int a = S.fd_m.div(e), b2 = e - a * m;
     double s = 0.0;
     for (int r = 0; r < na; ++r) s = fma(Dw[r * m + a], Dr[r * m + b2], s);
     Qu[e] = s + (double)Rb[e];
   }
   double* Qux = S.Qux + cb * m * n;
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
-    const int a = e / n, i = e - a * n;
+    const int a = S.fd_n.div(e), i = e - a * n;
     double s = 0.0;
     for (int r = 0; r < na; ++r) s = fma(Dw[r * m + a], Cr[r * n + i], s);
     Qux[e] = s;
@@ -287,7 +292,7 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   const double* Qx = S.Qx + cb * n * n;
   if (k == N) {  // terminal element (Qx_term, 0, 0)
     for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
-      const int i = e / ldg, jj = e - i * ldg;
+      const int i = S.fd_ldg.div(e), jj = e - i * ldg;
       Pd[e] = (jj < n) ? (float)Qx[i * n + jj] : 0.f;
       Ad[e] = 0.f;
       ATd[e] = 0.f;
@@ -312,7 +317,7 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) Qu[e] = S.Qu[cb * m * m + e];
   const float* Bg = qp.B + st * n * m;
   for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
-    const int l = e / np, i = e - l * np;
+    const int l = S.fd_ldg.div(e), i = e - l * np;
     Qux[e] = (i < n) ? S.Qux[cb * m * n + l * n + i] : 0.0;
     BT[e] = (i < n) ? (double)Bg[i * m + l] : 0.0;
   }
@@ -329,7 +334,7 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   const bool cfac = (dead & 8) != 0;
   const double* Linv = wk + kMaxM * (kMaxM + 1);
   for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
-    const int a = e / np, i = e - a * np;
+    const int a = S.fd_ldg.div(e), i = e - a * np;
     double s1 = 0.0, s2 = 0.0;
     for (int b2 = 0; b2 < m; ++b2) {
       const double qi = Qi[b2 * m + a];  // Qi symmetric in exact arithmetic; use Qi^T consistently
@@ -345,7 +350,7 @@ __global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   const float* Ak = qp.A + st * n * n;
   const int q4 = np >> 2;
   for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
-    const int i = e / q4, j0 = (e - i * q4) << 2;
+    const int i = S.fd_q4.div(e), j0 = (e - i * q4) << 2;
     double p4[4] = {0.0, 0.0, 0.0, 0.0}, a4[4] = {0.0, 0.0, 0.0, 0.0}, c4[4] = {0.0, 0.0, 0.0, 0.0};
     for (int l = 0; l < m; ++l) {
       const double qx = Qux[l * np + i], bt = BT[l * np + i], bq = BQT[l * np + i];
@@ -394,7 +399,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
     float* MTl = MTbase + (size_t)(cell_of(N, j + 1, j) - S.cell0) * MS;
     const float* Ej = E + ((size_t)inst * N + j) * n * n;
     for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
-      const int i = e / ldg, jj = e - i * ldg;
+      const int i = S.fd_ldg.div(e), jj = e - i * ldg;
       Ml[e] = (jj < n) ? Ej[i * n + jj] : 0.f;
       MTl[e] = (jj < n) ? Ej[jj * n + i] : 0.f;
     }
@@ -422,7 +427,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   const float* Bg = qp.B + st * n * m;
   const float* Ag = qp.A + st * n * n;
   for (int e = threadIdx.x; e < n * np; e += blockDim.x) {  // A_k: 4-byte async copies (rows of n floats)
-    const int i = e / np, jj = e - i * np;
+    const int i = S.fd_ldg.div(e), jj = e - i * np;
     if (jj < n) {
       const unsigned d = (unsigned)__cvta_generic_to_shared(Ak + i * lds + jj);
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(Ag + i * n + jj) : "memory");
@@ -432,14 +437,14 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   }
   cp_async_commit();
   for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
-    const int l = e / np, i = e - l * np;
+    const int l = S.fd_ldg.div(e), i = e - l * np;
     BT[e] = (i < n) ? (double)Bg[i * m + l] : 0.0;
   }
   cp_async_wait<0>();
   __syncthreads();
   const int q4 = np >> 2;
   for (int e = threadIdx.x; e < m * q4; e += blockDim.x) {  // B' P+ (1x4 tiles)
-    const int l = e / q4, j0 = (e - l * q4) << 2;
+    const int l = S.fd_q4.div(e), j0 = (e - l * q4) << 2;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int i = 0; i < n; ++i) {
       const double b = BT[l * np + i];
@@ -457,7 +462,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   const double* Qu = S.Qu + cb * m * m;
   const double* Qux = S.Qux + cb * m * n;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    const int l = e / m, t = e - l * m;
+    const int l = S.fd_m.div(e), t = e - l * m;
     double s = 0.0;
     for (int i = 0; i < n; ++i) s = fma(BtP[l * np + i], BT[t * np + i], s);
     H[e] = Qu[e] + s;
@@ -469,7 +474,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
       raise_err(S.err + inst, GSLS_ERR_SINGULAR_STAGE, k, j, GSLS_LABEL_QU_BPB);
   }
   for (int e = (int)threadIdx.x - 32; e >= 0 && e < m * q4; e += (int)blockDim.x - 32) {  // 1x4 tiles
-    const int l = e / q4, j0 = (e - l * q4) << 2;
+    const int l = S.fd_q4.div(e), j0 = (e - l * q4) << 2;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int i = 0; i < n; ++i) {
       const double b = BtP[l * np + i];
@@ -488,7 +493,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   __syncthreads();
   float* Kg = S.Kc + cb * m * n;
   for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
-    const int l = e / np, jj = e - l * np;
+    const int l = S.fd_ldg.div(e), jj = e - l * np;
     double s = 0.0;
     for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Gm[t * np + jj], s);
     Ks[e] = -s;
@@ -498,7 +503,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   float* Ml = Mbase + (size_t)(cell_of(N, k + 1, j) - S.cell0) * MS;  // product leaf of position k
   float* MTl = MTbase + (size_t)(cell_of(N, k + 1, j) - S.cell0) * MS;
   for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {  // A + B K (1x4 tiles)
-    const int i = e / q4, j0 = (e - i * q4) << 2;
+    const int i = S.fd_q4.div(e), j0 = (e - i * q4) << 2;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int l = 0; l < m; ++l) {
       const double b = BT[l * np + i];
@@ -523,7 +528,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   __syncthreads();
   // M^T rows: coalesced 16-byte stores instead of one scattered store per element
   for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
-    const int jj = e / q4, i0 = (e - jj * q4) << 2;
+    const int jj = S.fd_q4.div(e), i0 = (e - jj * q4) << 2;
     float v[4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) v[t] = (i0 + t < n) ? Pn[jj * lds + i0 + t] : 0.f;
