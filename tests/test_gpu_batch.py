@@ -88,6 +88,25 @@ def test_batched_robust_step_matches_reference_per_instance(tag, count):
         assert rel(_host(eng.tau_term[i]), g[f"{tag}_tau_term"][i]) <= TOL, i
 
 
+def test_large_batch_one_cta_per_instance_matches_reference():
+    """At 256 instances the ADMM runs one CTA per instance (k_admm_staged<4>: 4 item groups,
+    z / lam / y in global memory; the benched configuration) instead of the small-batch
+    clusters: its first 64 instances are the fixture's scenarios and must reproduce the
+    reference exactly (iterations, rho changes, active set) and within 1e-4."""
+    tag, count = "q61", 256
+    g = load_golden("batch")
+    eng, wl, xs = _engine_step(tag, count)
+    assert np.abs(xs[:64] - g[f"{tag}_x"]).max() == 0.0
+    its, rc = _host(eng.stats.iterations), _host(eng.stats.rho_changes)
+    act = _active(eng)
+    bad = [i for i in range(64) if not (its[i] == g[f"{tag}_iters"][i] and rc[i] == g[f"{tag}_rho_changes"][i]
+                                         and (act[i] == g[f"{tag}_active"][i]).all())]
+    assert not bad, bad
+    for i in range(64):
+        assert rel(_host(eng.u0[i]), g[f"{tag}_u0"][i]) <= TOL, i
+        assert rel(_host(eng.state.lam[i]), g[f"{tag}_lam"][i].astype(float)) <= TOL, i
+
+
 def test_batch_fixture_spreads_iterations():
     """The benched scenarios are not near-identical: the reference's iteration counts vary
     (q61: 21..65 for most instances, a heavy tail up to the max_iter = 500 cap)."""
