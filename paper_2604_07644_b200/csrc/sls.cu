@@ -277,7 +277,9 @@ __device__ inline void prefetch_l2(const void* p, size_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
 }
 
-__global__ void __launch_bounds__(256) k_sls_leaf(DevSls S, gsls_qp_t qp) {
+// 4 CTAs per SM (<= 64 registers): 40 % of the warps' time is the wait for the one-warp
+// inverse, so the extra resident CTA pays (21.3 vs 23.2 ms at B = 1024; 5 CTAs spill)
+__global__ void __launch_bounds__(256, 4) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   const int cell = blockIdx.x, inst = blockIdx.y;
   const int2 kj = S.cell_kj[cell];
   const int k = kj.x, j = kj.y;
@@ -407,14 +409,16 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   }
   extern __shared__ double smd[];
   const int np = ldg, lds = lds_of(n);
+  // shared memory for 4 CTAs per SM (56.5 KB at 61/12): K overwrites B'P+ (dead once G is
+  // formed) and the inverse's workspace is sized for m
   double* BT = smd;              // m x np   B_k^T
-  double* BtP = BT + m * np;     // m x np   B' P+
+  double* BtP = BT + m * np;     // m x np   B' P+, then K
   double* Gm = BtP + m * np;     // m x np
-  double* Ks = Gm + m * np;      // m x np
-  double* H = Ks + m * np;       // m x m
+  double* Ks = BtP;
+  double* H = Gm + m * np;       // m x m
   double* Ga = H + m * m;        // m x m
-  double* wk = Ga + m * m;
-  float* Pn = reinterpret_cast<float*>(wk + 2 * kMaxM * (kMaxM + 1) + 8);  // n x lds
+  double* wk = Ga + m * m;       // 2 m (m + 1) (+ 8): the inverse's L and X
+  float* Pn = reinterpret_cast<float*>(wk + 2 * m * (m + 1) + 8);  // n x lds
   float* Ak = Pn + n * lds;                                                // n x lds
   const float* Pg = S.Ps + ((size_t)inst * S.cvf_nslots + S.cvf_out[cell_of(N, k + 1, j) - S.cell0]) * MS;
   if (threadIdx.x == 0) {  // Qu, Qux: read after the B' P+ product
@@ -470,7 +474,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   __syncthreads();
   // warp 0 inverts H while warps 1.. form G = Qux + B' P+ A (independent of the inverse)
   if (threadIdx.x < 32) {
-    if (warp_spd_inverse(H, m, Ga, m, wk) && threadIdx.x == 0)
+    if (warp_spd_inverse(H, m, Ga, m, wk, m + 1, m * (m + 1)) && threadIdx.x == 0)
       raise_err(S.err + inst, GSLS_ERR_SINGULAR_STAGE, k, j, GSLS_LABEL_QU_BPB);
   }
   for (int e = (int)threadIdx.x - 32; e >= 0 && e < m * q4; e += (int)blockDim.x - 32) {  // 1x4 tiles
@@ -831,7 +835,8 @@ static int sls_synthesize_once(Ctx* c, const gsls_qp_t* qp, const float* E, cuda
     if ((rc = launch_combine(a, o1 - o0, B, st))) return rc;
   }
   {
-    const size_t sb = (4 * (size_t)m * ldg + 2 * m * m + wk) * sizeof(double) + 2 * (size_t)n * lds_of(n) * sizeof(float);
+    const size_t sb = (3 * (size_t)m * ldg + 2 * m * m + 2 * m * (m + 1) + 8) * sizeof(double) +
+                      2 * (size_t)n * lds_of(n) * sizeof(float);
     if ((rc = smem_attr((const void*)k_sls_gains, sb))) return rc;
     ProfScope ps(P_SLS_GAINS, st, (double)S.ncell * B);
     k_sls_gains<<<dim3(S.ncell, B), 256, sb, st>>>(S, *qp, E);

@@ -276,11 +276,13 @@ __device__ inline bool gj_inverse(float* a, float* out, int lds, int n, float* b
 // Cholesky; min pivot^2 < 1e-10 or failure -> retry with ridge 1e-9 (no pivot
 // test) -> failure is SingularStageError.
 template <class T>
-__device__ inline int warp_spd_inverse(const T* M, int ldm, T* inv, int m, T* work) {
+__device__ inline int warp_spd_inverse(const T* M, int ldm, T* inv, int m, T* work, int ld = kMaxM + 1,
+                                       int xoff = kMaxM * (kMaxM + 1)) {
+  // work: L (m x ld) at 0 and X = L^-1 (m x ld) at xoff; the defaults fit any m <= kMaxM
+  // (callers that read L^-1 afterwards index it with them)
   const int lane = threadIdx.x & 31;
-  const int ld = kMaxM + 1;
   T* L = work;
-  T* X = work + kMaxM * ld;
+  T* X = work + xoff;
   for (int attempt = 0; attempt < 2; ++attempt) {
     const T ridge = attempt ? T(1e-9) : T(0);
     for (int e = lane; e < m * m; e += 32) {
