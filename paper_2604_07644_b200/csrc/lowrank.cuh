@@ -304,13 +304,19 @@ __device__ inline bool chol_stack(float* Sb, float* Fb, float* Wb, int lds, int 
     // conflict-free (ld = 4 mod 8 words) and the group's L rows are broadcasts
     const int g0 = (jb >> 2) + 1, ng = (R >> 2) - g0;
     if (ng > 0) {
-      const int rows_below = nrow - (jb + 4);
-      for (int e = threadIdx.x; e < rows_below * ng; e += blockDim.x) {
-        const int gg = e / rows_below, ii = e - gg * rows_below;
-        const int g = g0 + gg, i = jb + 4 + ii;
-        if (i < R && 4 * g > i) continue;  // S: lower triangle (and diagonal blocks) only
+      // thread -> (row, pass): the row's panel entries z are loaded once and the column
+      // groups g0 + pass, g0 + pass + npass, ... updated in turn (one division per panel)
+      const int rows_below = nrow - (jb + 4), nt = blockDim.x;
+      const int npass = max(1, nt / rows_below);           // threads per row
+      const int pass = threadIdx.x / rows_below, ii0 = threadIdx.x - pass * rows_below;
+      const int stride = rows_below > nt ? nt : rows_below;  // more rows than threads: loop
+      for (int ii = (pass < npass ? ii0 : rows_below); ii < rows_below; ii += stride) {
+        const int i = jb + 4 + ii;
         float* p = row(i);
         const float4 z = *reinterpret_cast<const float4*>(p + jb);
+        for (int gg = pass; gg < ng; gg += npass) {
+        const int g = g0 + gg;
+        if (i < R && 4 * g > i) break;  // S: lower triangle (and diagonal blocks) only
         float4 acc = *reinterpret_cast<const float4*>(p + 4 * g);
         float* accv = &acc.x;
 #pragma unroll
@@ -324,6 +330,7 @@ __device__ inline bool chol_stack(float* Sb, float* Fb, float* Wb, int lds, int 
           accv[t] = s;
         }
         *reinterpret_cast<float4*>(p + 4 * g) = acc;
+        }
       }
     }
     __syncthreads();
