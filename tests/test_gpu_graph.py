@@ -1,7 +1,10 @@
 """One MPC step as a single CUDA graph (RtiEngine.capture, csrc/admm.cu admm_solve_captured):
 the captured step — with the ADMM's rebuild loop as a conditional WHILE node — must give
-bitwise the same results as the eager step it records, at batch 1 (cluster replay) and at a
-small batch, and keep doing so over a receding-horizon sequence of replays."""
+bitwise the same results as the eager step it records, at batch 1 (cluster replay), at a
+small batch, and keep doing so over a receding-horizon sequence of replays.  At a batch
+large enough for one CTA per instance (the eager driver then pauses instances in
+sigma-aligned waves and the captured loop does not) the iterations, rho changes and builds
+are still identical and the values agree to 1e-6."""
 
 import numpy as np
 import pytest
@@ -37,7 +40,8 @@ def _settings(m, rho0):
     return rs
 
 
-@pytest.mark.parametrize("tag,B,rho0", [("q61", 1, None), ("q61", 1, 1e-3), ("q61", 4, 1e-3), ("h75", 1, 1e-3)])
+@pytest.mark.parametrize("tag,B,rho0", [("q61", 1, None), ("q61", 1, 1e-3), ("q61", 4, 1e-3), ("h75", 1, 1e-3),
+                                        ("q61", 200, None)])  # 200: one CTA per instance (4 item groups)
 def test_captured_step_equals_eager(tag, B, rho0):
     import torch
     from paper_2604_07644_b200.engine import RtiEngine
@@ -53,12 +57,20 @@ def test_captured_step_equals_eager(tag, B, rho0):
     g = RtiEngine(m, wl.N, B, _settings(m, rho0))
     g.step(xb, px, pu, tau=tc, tau_term=tt)
     step = g.capture(xb, px, pu)  # its warm-up is the second eager step
+    exact_keys = ("its", "rho_changes", "builds")
     for k in range(1, 4):
         step()
         step.check()
         got = _snap(g)
         for key, v in ref[k].items():
-            assert np.array_equal(got[key], v), (k, key)
+            if B <= 148 or key in exact_keys:
+                assert np.array_equal(got[key], v), (k, key)
+            else:
+                # Above one wave of SMs the eager driver pauses instances at sigma multiples and
+                # finishes the long ones on clusters, whose matvecs split k differently from the
+                # captured loop's one-CTA launches: the same iterations and decisions, values
+                # equal up to the summation order.
+                assert np.abs(got[key] - v).max() <= 1e-6 * max(1.0, np.abs(v).max()), (k, key)
     if rho0 is not None:
         assert (ref[-1]["rho_changes"] > 0).all(), "the ADMM rebuild loop was not exercised"
 
