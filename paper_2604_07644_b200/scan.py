@@ -31,10 +31,21 @@ def scan_depth(length: int) -> int:
 
 @dataclass
 class LayerCounter:
-    """scan.py:46-51."""
+    """scan.py:46-51: layers and combines a scan executes.  The reference counts every
+    combine of its power-of-two padded tree (scan.py:190, :208, :229); the device plan
+    elides the identity combines, so ``count`` restates the reference's numbers."""
 
     layers: int = 0
     combines: int = 0
+
+    def count(self, length: int) -> "LayerCounter":
+        """Add one scan of ``length`` elements: 2 log2(p) layers and 2 (p - 1) - log2(p)
+        combines for p = next_pow2(length) (upsweep p - 1, downsweep sum of width - 1)."""
+        p = next_pow2(length)
+        lg = p.bit_length() - 1
+        self.layers += 2 * lg
+        self.combines += 2 * (p - 1) - lg
+        return self
 
 
 @dataclass
@@ -64,6 +75,16 @@ def tree_plan(length: int, reverse: bool = False) -> TreePlan:
                                  loff.ctypes.data_as(i32), out.ctypes.data_as(i32), ctypes.byref(n_ops),
                                  ctypes.byref(n_layers)), "gsls_scan_plan")
     return TreePlan(ops[: n_ops.value], loff, out)
+
+
+def tree_scan(values: list, combine, identity, reverse: bool = False, counter: LayerCounter | None = None):
+    """scan.tree_scan (scan.py:141-234) on host objects through the device schedule: the
+    inclusive scan in time order (reverse: suffix scan), combine(earlier, later); ``counter``
+    is incremented as the reference increments it."""
+    out = run_plan(tree_plan(len(values), reverse), values, combine, identity)
+    if counter is not None:
+        counter.count(len(values))
+    return out
 
 
 def run_plan(plan: TreePlan, values: list, combine, identity):

@@ -85,6 +85,20 @@ def test_plan_matches_reference_tree(length, reverse):
     assert ours == ref
 
 
+@pytest.mark.parametrize("length", [1, 2, 3, 8, 17, 26, 51, 100])
+@pytest.mark.parametrize("reverse", [False, True])
+def test_layer_counter_matches_reference(length, reverse):
+    """scan.tree_scan's LayerCounter counts layers and combines as the reference's tree_scan
+    (scan.py:46-51, :190-229) does, padding combines included (the oracle's tally)."""
+    mats = [np.array([[1, i], [0, 1]]) for i in range(length)]
+    c = scan.LayerCounter()
+    ours = scan.tree_scan(mats, lambda a, b: a @ b, np.eye(2, dtype=np.int64), reverse=reverse, counter=c)
+    t = tree.Tally()
+    ref = tree.scan_list(mats, lambda a, b: a @ b, np.eye(2, dtype=np.int64), reverse=reverse, tally=t)
+    assert all((a == b).all() for a, b in zip(ours, ref))
+    assert (c.layers, c.combines) == (t.layers, t.combines)
+
+
 def test_plan_golden_integers():
     g = load_golden("scan")
     ints = g["ints"].tolist()
