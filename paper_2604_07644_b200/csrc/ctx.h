@@ -51,6 +51,7 @@ struct DevLqr {
   //   cb_k       = B_k kf_k + b_k                   Bcm: n x m, ld ldn
   //   G_k        = [Z D]_k [dx; kf]_k               ZD: c x (n + m), ld ldc  (Z = C + D K)
   int ldm, ldn, ldc, ld2n;
+  FastDiv fd_ldg, fd_m, fd_n, fd_c, fd_ldm, fd_ldn, fd_ldc, fd_ld2n;  // the per-stage kernels' loop indices
   float *X23, *XK, *Bcm, *ZD;
   // physical storage of the replay vectors per scan slot (plan.h compress_slots)
   const int* cvf_phys;

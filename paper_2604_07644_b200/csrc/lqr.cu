@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
     const float* QN = qp.QN + (size_t)inst * n * n;
     const float* CN = qp.CN + (size_t)inst * nf * n;
     for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
-      const int i = e / ldg, j = e - i * ldg;
+      const int i = L.fd_ldg.div(e), j = e - i * ldg;
       double v = 0.0;
       if (j < n) {
         double s = 0.0;
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   const float* Rg = qp.R + st * m * m;
   const float* Sg = qp.S ? qp.S + st * m * n : nullptr;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    const int i = e / m, j = e - i * m;
+    const int i = L.fd_m.div(e), j = e - i * m;
     double s = 0.0;
     for (int r = 0; r < c; ++r) s = fma(Dst[r * m + i], Dst[r * m + j], s);
     Rh[e] = (double)Rg[e] + rho * s;
@@ -195,20 +195,20 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
       raise_err(L.err + inst, GSLS_ERR_SINGULAR_STAGE, k, -1, GSLS_LABEL_R);
   }
   for (int e = (int)threadIdx.x - 32; e >= 0 && e < m * n; e += (int)blockDim.x - 32) {
-    const int i = e / n, j = e - i * n;
+    const int i = L.fd_n.div(e), j = e - i * n;
     double s = 0.0;
     for (int r = 0; r < c; ++r) s = fma(Dst[r * m + i], Cst[r * n + j], s);
     Sh[e] = (Sg ? (double)Sg[e] : 0.0) + rho * s;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
-    const int l = e / n, j = e - l * n;
+    const int l = L.fd_n.div(e), j = e - l * n;
     double s = 0.0;
     for (int t = 0; t < m; ++t) s = fma(Ri[l * m + t], Sh[t * n + j], s);
     RS[e] = s;
   }
   for (int e = threadIdx.x; e < n * m; e += blockDim.x) {
-    const int i = e / m, l = e - i * m;
+    const int i = L.fd_m.div(e), l = e - i * m;
     double s = 0.0;
     for (int t = 0; t < m; ++t) s = fma(Bst[i * m + t], Ri[t * m + l], s);
     BR[e] = s;
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   const bool cfac = L.cvf_leaf && (L.cvf_leaf[k] & 8);
   const double* Linv = wk + kMaxM * (kMaxM + 1);
   for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
-    const int i = e / ldg, j = e - i * ldg;
+    const int i = L.fd_ldg.div(e), j = e - i * ldg;
     double p = 0.0, a = 0.0, cc = 0.0;
     if (cfac && j < m) {
       double f = 0.0;
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   const double* rg = qp.r + st * m;
   for (int e = threadIdx.x; e < m * c + m; e += blockDim.x) {
     if (e < m * c) {
-      const int l = e / c, r = e - l * c;
+      const int l = L.fd_c.div(e), r = e - l * c;
       double s = 0.0;
       for (int t = 0; t < m; ++t) s = fma(Ri[l * m + t], Dst[r * m + t], s);
       X1[e] = rho * s;
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   const int ld2n = L.ld2n, ldn = L.ldn, ldc = L.ldc;
   float* X23 = L.X23 + st * (size_t)c * ld2n;
   for (int e = threadIdx.x; e < c * ld2n; e += blockDim.x) {
-    const int r = e / ld2n, i = e - r * ld2n;
+    const int r = L.fd_ld2n.div(e), i = e - r * ld2n;
     double v = 0.0;
     if (i < n) {
       double s = 0.0;
@@ -306,12 +306,12 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   }
   float* Bcm = L.Bcm + st * (size_t)m * ldn;
   for (int e = threadIdx.x; e < m * ldn; e += blockDim.x) {
-    const int j = e / ldn, i = e - j * ldn;
+    const int j = L.fd_ldn.div(e), i = e - j * ldn;
     Bcm[e] = (i < n) ? (float)Bst[i * m + j] : 0.f;
   }
   float* Dcm = L.ZD + st * (size_t)(n + m) * ldc + (size_t)n * ldc;  // D columns of [Z D]
   for (int e = threadIdx.x; e < m * ldc; e += blockDim.x) {
-    const int j = e / ldc, i = e - j * ldc;
+    const int j = L.fd_ldc.div(e), i = e - j * ldc;
     Dcm[e] = (i < c) ? (float)Dst[i * m + j] : 0.f;
   }
 }
@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
   for (int e = threadIdx.x; e < n * m; e += blockDim.x) Bst[e] = Bg[e];
   __syncthreads();
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
-    const int l = e / n, j = e - l * n;
+    const int l = L.fd_n.div(e), j = e - l * n;
     double s = 0.0;
     for (int i = 0; i < n; ++i) s = fma(Bst[i * m + l], (double)Pn[i * ldg + j], s);
     BtP[e] = s;
@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
   const double* Rhat = L.Rhat + st * m * m;
   const double* Shat = L.Shat64 + st * m * n;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    const int l = e / m, t = e - l * m;
+    const int l = L.fd_m.div(e), t = e - l * m;
     double s = 0.0;
     for (int j = 0; j < n; ++j) s = fma(BtP[l * n + j], Bst[j * m + t], s);
     H[e] = Rhat[e] + s;
@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
   __syncthreads();
   // warps 1.. form G = Shat + B' P+ A while warp 0 inverts H (independent)
   for (int e = (int)threadIdx.x - 32; e >= 0 && e < m * n; e += (int)blockDim.x - 32) {
-    const int l = e / n, j = e - l * n;
+    const int l = L.fd_n.div(e), j = e - l * n;
     double s = 0.0;
     for (int i = 0; i < n; ++i) s = fma(BtP[l * n + i], (double)Ag[i * n + j], s);
     Gm[e] = Shat[e] + s;
@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
   __syncthreads();
   float* Kg = L.K + st * m * n;
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
-    const int l = e / n, j = e - l * n;
+    const int l = L.fd_n.div(e), j = e - l * n;
     double s = 0.0;
     for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Gm[t * n + j], s);
     Ks[e] = -s;
@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
   float* Ad = L.cotA + ((size_t)inst * L.cot_nslots + k) * MS;
   float* ATd = L.cotAT + ((size_t)inst * L.cot_nslots + k) * MS;
   for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
-    const int i = e / ldg, j = e - i * ldg;
+    const int i = L.fd_ldg.div(e), j = e - i * ldg;
     double v = 0.0;
     if (j < n) {
       double s = 0.0;
@@ -662,7 +662,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
     const int ldm = L.ldm, ldc = L.ldc;
     float* X5 = L.XK + st * (size_t)(n + c) * ldm;  // [X5 X4]
     for (int e = threadIdx.x; e < n * ldm; e += blockDim.x) {
-      const int i = e / ldm, l = e - i * ldm;
+      const int i = L.fd_ldm.div(e), l = e - i * ldm;
       double s = 0.0;
       if (l < m)
         for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Bst[i * m + t], s);
@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
     }
     float* X4 = X5 + (size_t)n * ldm;
     for (int e = threadIdx.x; e < c * ldm; e += blockDim.x) {
-      const int r = e / ldm, l = e - r * ldm;
+      const int r = L.fd_ldm.div(e), l = e - r * ldm;
       double s = 0.0;
       if (l < m)
         for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Dst[r * m + t], s);
@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
     const float* Cg = qp.C + st * c * n;
     float* Zcm = L.ZD + st * (size_t)(n + m) * ldc;
     for (int e = threadIdx.x; e < n * ldc; e += blockDim.x) {
-      const int i = e / ldc, r = e - i * ldc;
+      const int i = L.fd_ldc.div(e), r = e - i * ldc;
       double v = 0.0;
       if (r < c) {
         double s = (double)Cg[r * n + i];
@@ -1059,6 +1059,8 @@ int ctx_create(const gsls_dims_t* dims, Ctx** out) {
   L.err = (ErrSlot*)dev_alloc(c, B * sizeof(ErrSlot));
   const size_t cc = d.nc;
   L.ldm = ldg_of(d.nu); L.ldn = ldg_of(d.nx); L.ldc = ldg_of(std::max(1, d.nc)); L.ld2n = ldg_of(2 * d.nx);
+  L.fd_ldg.init(ldg_of(d.nx)); L.fd_m.init(d.nu); L.fd_n.init(d.nx); L.fd_c.init(std::max(1, d.nc));
+  L.fd_ldm.init(L.ldm); L.fd_ldn.init(L.ldn); L.fd_ldc.init(L.ldc); L.fd_ld2n.init(L.ld2n);
   L.X23 = (float*)dev_alloc(c, std::max<size_t>(1, B * N * cc * L.ld2n) * 4);
   L.pb0 = (double*)dev_alloc(c, std::max<size_t>(1, B * N * 2 * n) * 8);
   L.XK = (float*)dev_alloc(c, std::max<size_t>(1, B * N * (n + cc) * L.ldm) * 4);
