@@ -85,6 +85,7 @@ struct DevSls {
   int mp_nslots, mp_nops, mp_layers;
   float *Ps, *As, *Cs, *ATs, *Ms, *MsT;
   double *Qx, *Qu, *Qux;  // cost blocks (float64: the leaf Schur complement cancels O(tau) terms)
+  double *Qi, *QL;        // per cell: Qu^-1 and L^-1 (Qu = L L') from k_sls_qu_inverse (m x m each)
   float *Kc, *Phiu;
   double* rn;
   ErrSlot* err;
@@ -169,11 +170,13 @@ static int sls_init(Ctx* c) {
   S.Qx = (double*)dev_alloc(c, B * S.ncell * n * n * 8);
   S.Qu = (double*)dev_alloc(c, B * S.ncell * m * m * 8);
   S.Qux = (double*)dev_alloc(c, B * S.ncell * m * n * 8);
+  S.Qi = (double*)dev_alloc(c, B * S.ncell * m * m * 8);
+  S.QL = (double*)dev_alloc(c, B * S.ncell * m * m * 8);
   S.Kc = (float*)dev_alloc(c, B * S.ncell * m * n * 4);
   S.Phiu = (float*)dev_alloc(c, B * S.ncell * m * n * 4);
   S.rn = (double*)dev_alloc(c, B * S.ncell * S.cmax * 8);
   S.err = c->dev.err;
-  if (!S.Ps || !S.As || !S.Cs || !S.ATs || !S.Ms || !S.MsT || !S.Qx || !S.Qu || !S.Qux || !S.Kc || !S.Phiu || !S.rn) {
+  if (!S.Ps || !S.As || !S.Cs || !S.ATs || !S.Ms || !S.MsT || !S.Qx || !S.Qu || !S.Qux || !S.Qi || !S.QL || !S.Kc || !S.Phiu || !S.rn) {
     set_error(GSLS_ERR_CUDA, -1, 0, 0, 0, "SLS workspace allocation failed");
     return GSLS_ERR_CUDA;
   }
@@ -277,6 +280,36 @@ __device__ inline void prefetch_l2(const void* p, size_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
 }
 
+// The leaves' m x m SPD inverses (sls.py:258-261 via lqr.spd_inverse, lqr.py:185-220), one
+// warp per cell and eight cells per CTA, ahead of k_sls_leaf: inside the leaf kernel the
+// one-warp inverse held the other seven warps at a barrier (40 % of its stall samples).
+// Writes Qu^-1 and L^-1 (Qu = L L', the factor the factored tree uses) per cell.
+__global__ void __launch_bounds__(256) k_sls_qu_inverse(DevSls S) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cell = blockIdx.x * 8 + warp, inst = blockIdx.y;
+  const int m = S.m;
+  const int ld = m + 1, xoff = m * ld;  // the inverse's workspace: L, X = L^-1 (ld m + 1)
+  extern __shared__ double smq[];
+  double* Qu = smq + warp * (m * m + 2 * xoff + 8);
+  double* wk = Qu + m * m;
+  const bool live = cell < S.ncell && S.cell_kj[cell].x < S.N;  // terminal cells have no inverse
+  if (!live) return;  // warp-uniform
+  const size_t cb = (size_t)inst * S.ncell + cell;
+  for (int e = lane; e < m * m; e += 32) Qu[e] = S.Qu[cb * m * m + e];
+  __syncwarp();
+  double* Qi = S.Qi + cb * m * m;
+  if (warp_spd_inverse(Qu, m, Qi, m, wk, ld, xoff) && lane == 0) {
+    const int2 kj = S.cell_kj[cell];
+    raise_err(S.err + inst, GSLS_ERR_SINGULAR_STAGE, kj.x, kj.y, GSLS_LABEL_QU);
+  }
+  __syncwarp();
+  double* QL = S.QL + cb * m * m;
+  for (int e = lane; e < m * m; e += 32) {
+    const int a = e / m, b = e - a * m;
+    QL[e] = (b <= a) ? wk[xoff + a * ld + b] : 0.0;
+  }
+}
+
 // 4 CTAs per SM (<= 64 registers): 40 % of the warps' time is the wait for the one-warp
 // inverse, so the extra resident CTA pays (21.3 vs 23.2 ms at B = 1024; 5 CTAs spill)
 __global__ void __launch_bounds__(256, 4) k_sls_leaf(DevSls S, gsls_qp_t qp) {
@@ -315,8 +348,10 @@ __global__ void __launch_bounds__(256, 4) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   double* QQ = Qux + m * np;         // m x np   Qu^-1 Qux
   double* BT = QQ + m * np;          // m x np   B_k^T
   double* BQT = BT + m * np;         // m x np   (B_k Qu^-1)^T
-  double* wk = BQT + m * np;
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) Qu[e] = S.Qu[cb * m * m + e];
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {  // Qu^-1 and L^-1 from k_sls_qu_inverse
+    Qi[e] = S.Qi[cb * m * m + e];
+    Qu[e] = S.QL[cb * m * m + e];  // (the Qu buffer holds L^-1 here)
+  }
   const float* Bg = qp.B + st * n * m;
   for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
     const int l = S.fd_ldg.div(e), i = e - l * np;
@@ -324,17 +359,12 @@ __global__ void __launch_bounds__(256, 4) k_sls_leaf(DevSls S, gsls_qp_t qp) {
     BT[e] = (i < n) ? (double)Bg[i * m + l] : 0.0;
   }
   __syncthreads();
-  if (threadIdx.x < 32) {
-    if (warp_spd_inverse(Qu, m, Qi, m, wk) && threadIdx.x == 0)
-      raise_err(S.err + inst, GSLS_ERR_SINGULAR_STAGE, k, j, GSLS_LABEL_QU);
-  }
-  __syncthreads();
   const int dead = S.leaf_dead[cell];  // parts of this leaf no combine reads (scan-plan analysis)
   // C = B Qu^-1 B' is stored as the factor F = B L^-T (Qu = L L', L^-1 left in the
   // inverse's work area) when the plan carries it factored (lowrank.cuh): BQT then
   // holds F' = L^-1 B' instead of (B Qu^-1)'
   const bool cfac = (dead & 8) != 0;
-  const double* Linv = wk + kMaxM * (kMaxM + 1);
+  const double* Linv = Qu;  // m x m, row-major (ld m)
   for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
     const int a = S.fd_ldg.div(e), i = e - a * np;
     double s1 = 0.0, s2 = 0.0;
@@ -344,7 +374,7 @@ __global__ void __launch_bounds__(256, 4) k_sls_leaf(DevSls S, gsls_qp_t qp) {
       if (!cfac) s2 = fma(qi, BT[b2 * np + i], s2);
     }
     if (cfac)
-      for (int b2 = 0; b2 <= a; ++b2) s2 = fma(Linv[a * (kMaxM + 1) + b2], BT[b2 * np + i], s2);
+      for (int b2 = 0; b2 <= a; ++b2) s2 = fma(Linv[a * m + b2], BT[b2 * np + i], s2);
     QQ[e] = s1;
     BQT[e] = s2;
   }
@@ -820,9 +850,12 @@ static int sls_synthesize_once(Ctx* c, const gsls_qp_t* qp, const float* E, cuda
   const size_t MS = mat_elems(n);
   const size_t wk = 2 * kMaxM * (kMaxM + 1) + 8;
   {
-    const size_t sb = (2 * m * m + 4 * (size_t)m * ldg + wk) * sizeof(double);
+    const size_t sbq = 8 * (size_t)(m * m + 2 * m * (m + 1) + 8) * sizeof(double);
+    const size_t sb = (2 * m * m + 4 * (size_t)m * ldg) * sizeof(double);
     if ((rc = smem_attr((const void*)k_sls_leaf, sb))) return rc;
+    if ((rc = smem_attr((const void*)k_sls_qu_inverse, sbq))) return rc;
     ProfScope ps(P_SLS_LEAF, st, (double)S.ncell * B);
+    k_sls_qu_inverse<<<dim3((S.ncell + 7) / 8, B), 256, sbq, st>>>(S);
     k_sls_leaf<<<dim3(S.ncell, B), 256, sb, st>>>(S, *qp);
     GSLS_CUDA_CHECK(cudaGetLastError());
   }
