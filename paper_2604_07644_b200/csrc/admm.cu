@@ -976,8 +976,7 @@ constexpr int kTraceIter = 5;  // GSLS_REPLAY_TRACE samples this ADMM iteration 
 
 struct StagedLayout {
   // byte offsets into dynamic shared memory
-  int ring, pv, bv, cb, t1, t2, z, lam, y, w, kf, dx0, part, red, redall, masks, ops, phys, items, gseq, phase, mbar,
-      total;
+  int ring, pv, bv, cb, t1, t2, w, kf, dx0, part, red, redall, masks, ops, phys, items, gseq, phase, mbar, total;
   int slot;  // bytes per ring slot
   int R;     // ring slots
   int max_items, nphase;
@@ -1027,7 +1026,7 @@ __host__ __device__ inline StagedLayout staged_layout(const DevLqr& L, int max_l
   S.cb = take(L.cot_nphys * n * 8, 16);
   S.t1 = take(0, 16);  // (unused since the one-round CVF replay)
   S.t2 = take(0, 16);
-  S.z = S.lam = S.y = -1;  // z, lam, y stay in global memory (only their owner rows' G epilogue touches them)
+  // z, lam, y stay in global memory (only their owner rows' G epilogue touches them)
   S.w = take(L.mtot * 8, 16);
   S.kf = take(N * m * 8, 16);
   S.dx0 = take(n * 8, 16);
@@ -1784,8 +1783,6 @@ static int launch_admm_staged(Ctx* c, ReplayArgs& a, int count, cudaStream_t st)
       fprintf(stderr, " %llu|%llu", h[2 * p + 1] - prev, h[2 * p + 2] - h[2 * p + 1]);
       prev = h[2 * p + 2];
     }
-    fprintf(stderr, "\nitems (wait, matvec, sync, issue):");
-    for (int j = 0; j < 20; ++j) fprintf(stderr, " [%llu %llu %llu %llu]", h[100 + 5 * j], h[101 + 5 * j], h[102 + 5 * j], h[103 + 5 * j]);
     fprintf(stderr, "\n");
   }
   return GSLS_OK;
