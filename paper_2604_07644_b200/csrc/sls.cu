@@ -600,13 +600,19 @@ __global__ void __launch_bounds__(256) k_sls_phiu(DevSls S) {
   extern __shared__ float sm[];
   float* Px = sm;
   const float* Pg = S.Ms + ((size_t)inst * S.mp_nslots + S.mp_out[cell]) * MS;
-  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) Px[e] = Pg[e];
-  __syncthreads();
   const size_t cb = (size_t)inst * S.ncell + cell;
   const float* Kg = S.Kc + cb * m * n;
   float* Pug = S.Phiu + cb * m * n;
   float* Ks = Px + n * ldg;  // K staged in smem (m x n)
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) Ks[e] = Kg[e];
+  // 16-byte async copies of the contiguous blocks (K's per-cell blocks are 16-byte aligned
+  // when m n is a multiple of 4; otherwise plain loads)
+  for (int e = threadIdx.x; e < (n * ldg) >> 2; e += blockDim.x) cp_async16(Px + 4 * e, Pg + 4 * e);
+  if (((m * n) & 3) == 0)
+    for (int e = threadIdx.x; e < (m * n) >> 2; e += blockDim.x) cp_async16(Ks + 4 * e, Kg + 4 * e);
+  else
+    for (int e = threadIdx.x; e < m * n; e += blockDim.x) Ks[e] = Kg[e];
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   // Phi^u = K Phi^x: thread task = (row a, 4 columns), one broadcast K value and one
   // 16-byte Phi^x row load per l
@@ -637,9 +643,11 @@ __global__ void __launch_bounds__(256) k_sls_rownorm(DevSls S, gsls_qp_t qp) {
   float* Pu = Px + n * ldg;  // m x n
   const float* Pg = S.Ms + ((size_t)inst * S.mp_nslots + S.mp_out[cell]) * MS;
   const size_t cb = (size_t)inst * S.ncell + cell;
-  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) Px[e] = Pg[e];
+  for (int e = threadIdx.x; e < (n * ldg) >> 2; e += blockDim.x) cp_async16(Px + 4 * e, Pg + 4 * e);
+  cp_async_commit();
   if (k < N)
     for (int e = threadIdx.x; e < m * n; e += blockDim.x) Pu[e] = S.Phiu[cb * m * n + e];
+  cp_async_wait<0>();
   __syncthreads();
   double* rn = S.rn + cb * S.cmax;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
