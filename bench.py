@@ -714,7 +714,9 @@ def run_ours(args):
     total_iters = float(its_all.sum())
     iters_per_step = total_iters / args.steps
     fam = dict(zip(nat.PROF_FAMILIES, zip(pm, pu_, pl)))  # timed loop: (ms, units, launches)
-    fam_s, ms_serial, builds_per_step = serialized_phases(eng, lambda: step(dev), nat, lib)
+    fam_s, ms_serial, builds_per_step = serialized_phases(  # rank 0 alone from here: the step without its all-gather
+        eng, lambda: eng.step(dev["xbar0"], dev["prev_x"], dev["prev_u"], tau=dev["tau"],
+                              tau_term=dev["tau_term"]), nat, lib)
     dims = (n, mu, c, nf, N)
     rl_phase = phase_rooflines(fam_s, B, dims, iters_per_step, builds_per_step, fp32_peak, hbm_peak)
     tr = ncu_traffic()
