@@ -347,7 +347,8 @@ __global__ void __launch_bounds__(256, 4) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   double* Qux = Qi + m * m;          // m x np
   double* QQ = Qux + m * np;         // m x np   Qu^-1 Qux
   double* BT = QQ + m * np;          // m x np   B_k^T
-  double* BQT = BT + m * np;         // m x np   (B_k Qu^-1)^T
+  double* BQT = BT + m * np;         // m x ldq  (B_k Qu^-1)^T
+  const int ldq = np + 1;            // odd: the factored epilogue reads BQT by column (16 rows a warp)
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {  // Qu^-1 and L^-1 from k_sls_qu_inverse
     Qi[e] = S.Qi[cb * m * m + e];
     Qu[e] = S.QL[cb * m * m + e];  // (the Qu buffer holds L^-1 here)
@@ -376,49 +377,49 @@ __global__ void __launch_bounds__(256, 4) k_sls_leaf(DevSls S, gsls_qp_t qp) {
     if (cfac)
       for (int b2 = 0; b2 <= a; ++b2) s2 = fma(Linv[a * m + b2], BT[b2 * np + i], s2);
     QQ[e] = s1;
-    BQT[e] = s2;
+    BQT[a * ldq + i] = s2;
   }
   __syncthreads();
   const float* Ak = qp.A + st * n * n;
+  // 1x4 tiles over columns c, c + q4, c + 2 q4, c + 3 q4: a warp's lanes read consecutive
+  // doubles of a row (the 4-wide column tiles put lanes 32 bytes apart: 2x the shared
+  // wavefronts, the kernel being shared-memory bound)
   const int q4 = np >> 2;
   for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
-    const int i = S.fd_q4.div(e), j0 = (e - i * q4) << 2;
+    const int i = S.fd_q4.div(e), c0 = e - i * q4;
     double p4[4] = {0.0, 0.0, 0.0, 0.0}, a4[4] = {0.0, 0.0, 0.0, 0.0}, c4[4] = {0.0, 0.0, 0.0, 0.0};
     for (int l = 0; l < m; ++l) {
-      const double qx = Qux[l * np + i], bt = BT[l * np + i], bq = BQT[l * np + i];
-      const double2 q01 = *reinterpret_cast<const double2*>(QQ + l * np + j0);
-      const double2 q23 = *reinterpret_cast<const double2*>(QQ + l * np + j0 + 2);
-      const double2 b01 = *reinterpret_cast<const double2*>(BT + l * np + j0);
-      const double2 b23 = *reinterpret_cast<const double2*>(BT + l * np + j0 + 2);
-      const double qq[4] = {q01.x, q01.y, q23.x, q23.y}, bb[4] = {b01.x, b01.y, b23.x, b23.y};
+      const double qx = Qux[l * np + i], bt = BT[l * np + i], bq = BQT[l * ldq + i];
+      const double* qr = QQ + l * np + c0;
+      const double* br = BT + l * np + c0;
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        p4[t] = fma(qx, qq[t], p4[t]);
-        a4[t] = fma(bt, qq[t], a4[t]);
-        if (!cfac) c4[t] = fma(bq, bb[t], c4[t]);
+        const double qq = qr[t * q4];
+        p4[t] = fma(qx, qq, p4[t]);
+        a4[t] = fma(bt, qq, a4[t]);
+        if (!cfac) c4[t] = fma(bq, br[t * q4], c4[t]);
       }
     }
-    float po[4], ao[4], co[4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      const int jj = j0 + t;
+      const int jj = c0 + t * q4;
       const bool in = jj < n;
-      po[t] = in ? (float)(Qx[i * n + jj] - p4[t]) : 0.f;
-      ao[t] = in ? (float)((double)Ak[i * n + jj] - a4[t]) : 0.f;
-      co[t] = in ? (float)c4[t] : 0.f;
-      if (cfac) co[t] = jj < m ? (float)BQT[jj * np + i] : 0.f;
-      if (in && !(dead & 2)) ATd[(size_t)jj * ldg + i] = ao[t];
+      const float po = in ? (float)(Qx[i * n + jj] - p4[t]) : 0.f;
+      const float ao = in ? (float)((double)Ak[i * n + jj] - a4[t]) : 0.f;
+      float co = in ? (float)c4[t] : 0.f;
+      if (cfac) co = jj < m ? (float)BQT[jj * ldq + i] : 0.f;
+      if (in && !(dead & 2)) ATd[(size_t)jj * ldg + i] = ao;
+      Pd[(size_t)i * ldg + jj] = po;
+      if (!(dead & 1)) Ad[(size_t)i * ldg + jj] = ao;
+      if (!(dead & 4)) Cd[(size_t)i * ldg + jj] = co;
     }
-    *reinterpret_cast<float4*>(Pd + (size_t)i * ldg + j0) = make_float4(po[0], po[1], po[2], po[3]);
-    if (!(dead & 1)) *reinterpret_cast<float4*>(Ad + (size_t)i * ldg + j0) = make_float4(ao[0], ao[1], ao[2], ao[3]);
-    if (!(dead & 4)) *reinterpret_cast<float4*>(Cd + (size_t)i * ldg + j0) = make_float4(co[0], co[1], co[2], co[3]);
   }
 }
 
 // Gains on cell (k, j), k <= N-1, from P+ = P(k+1, j); closed loop -> product
 // leaf of position k (float64 algebra, 1x4 tiles).  Cell (N, j) writes E_j into
 // the leaf of position j.
-__global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const float* E) {
+__global__ void __launch_bounds__(256, 4) k_sls_gains(DevSls S, gsls_qp_t qp, const float* E) {
   const int cell = blockIdx.x, inst = blockIdx.y;
   const int2 kj = S.cell_kj[cell];
   const int k = kj.x, j = kj.y;
@@ -438,12 +439,14 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
     return;
   }
   extern __shared__ double smd[];
-  const int np = ldg, lds = lds_of(n);
-  // shared memory for 4 CTAs per SM (56.5 KB at 61/12): K overwrites B'P+ (dead once G is
+  // B' and B'P+ rows at an odd stride: H = (B'P+) B reads 12 rows of B' and 3 of B'P+
+  // per warp, all in one bank at an even stride
+  const int np = ldg, lds = lds_of(n), ldb = np + 1;
+  // shared memory for 4 CTAs per SM (56.7 KB at 61/12): K overwrites B'P+ (dead once G is
   // formed) and the inverse's workspace is sized for m
-  double* BT = smd;              // m x np   B_k^T
-  double* BtP = BT + m * np;     // m x np   B' P+, then K
-  double* Gm = BtP + m * np;     // m x np
+  double* BT = smd;              // m x ldb  B_k^T
+  double* BtP = BT + m * ldb;    // m x ldb  B' P+, then K
+  double* Gm = BtP + m * ldb;    // m x np
   double* Ks = BtP;
   double* H = Gm + m * np;       // m x m
   double* Ga = H + m * m;        // m x m
@@ -472,7 +475,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   cp_async_commit();
   for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
     const int l = S.fd_ldg.div(e), i = e - l * np;
-    BT[e] = (i < n) ? (double)Bg[i * m + l] : 0.0;
+    BT[l * ldb + i] = (i < n) ? (double)Bg[i * m + l] : 0.0;
   }
   cp_async_wait<0>();
   __syncthreads();
@@ -481,7 +484,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
     const int l = S.fd_q4.div(e), j0 = (e - l * q4) << 2;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int i = 0; i < n; ++i) {
-      const double b = BT[l * np + i];
+      const double b = BT[l * ldb + i];
       const float4 pv = *reinterpret_cast<const float4*>(Pn + i * lds + j0);
       acc[0] = fma(b, (double)pv.x, acc[0]);
       acc[1] = fma(b, (double)pv.y, acc[1]);
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
       acc[3] = fma(b, (double)pv.w, acc[3]);
     }
 #pragma unroll
-    for (int t = 0; t < 4; ++t) BtP[l * np + j0 + t] = acc[t];
+    for (int t = 0; t < 4; ++t) BtP[l * ldb + j0 + t] = acc[t];
   }
   __syncthreads();
   const size_t cb = (size_t)inst * S.ncell + cell;
@@ -498,7 +501,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
     const int l = S.fd_m.div(e), t = e - l * m;
     double s = 0.0;
-    for (int i = 0; i < n; ++i) s = fma(BtP[l * np + i], BT[t * np + i], s);
+    for (int i = 0; i < n; ++i) s = fma(BtP[l * ldb + i], BT[t * ldb + i], s);
     H[e] = Qu[e] + s;
   }
   __syncthreads();
@@ -511,7 +514,7 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
     const int l = S.fd_q4.div(e), j0 = (e - l * q4) << 2;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int i = 0; i < n; ++i) {
-      const double b = BtP[l * np + i];
+      const double b = BtP[l * ldb + i];
       const float4 av = *reinterpret_cast<const float4*>(Ak + i * lds + j0);
       acc[0] = fma(b, (double)av.x, acc[0]);
       acc[1] = fma(b, (double)av.y, acc[1]);
@@ -530,43 +533,38 @@ __global__ void __launch_bounds__(256) k_sls_gains(DevSls S, gsls_qp_t qp, const
     const int l = S.fd_ldg.div(e), jj = e - l * np;
     double s = 0.0;
     for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Gm[t * np + jj], s);
-    Ks[e] = -s;
+    Ks[l * ldb + jj] = -s;
     if (jj < n) Kg[l * n + jj] = (float)(-s);
   }
   __syncthreads();
   float* Ml = Mbase + (size_t)(cell_of(N, k + 1, j) - S.cell0) * MS;  // product leaf of position k
   float* MTl = MTbase + (size_t)(cell_of(N, k + 1, j) - S.cell0) * MS;
-  for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {  // A + B K (1x4 tiles)
-    const int i = S.fd_q4.div(e), j0 = (e - i * q4) << 2;
+  // A + B K, 1x4 tiles over columns c, c + q4, c + 2 q4, c + 3 q4 (lanes on consecutive
+  // doubles of a K row; 4-wide column tiles put them 32 bytes apart)
+  for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
+    const int i = S.fd_q4.div(e), c0 = e - i * q4;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int l = 0; l < m; ++l) {
-      const double b = BT[l * np + i];
-      const double2 k01 = *reinterpret_cast<const double2*>(Ks + l * np + j0);
-      const double2 k23 = *reinterpret_cast<const double2*>(Ks + l * np + j0 + 2);
-      acc[0] = fma(b, k01.x, acc[0]);
-      acc[1] = fma(b, k01.y, acc[1]);
-      acc[2] = fma(b, k23.x, acc[2]);
-      acc[3] = fma(b, k23.y, acc[3]);
+      const double b = BT[l * ldb + i];
+      const double* kr = Ks + l * ldb + c0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc[t] = fma(b, kr[t * q4], acc[t]);
     }
-    const float4 av = *reinterpret_cast<const float4*>(Ak + i * lds + j0);
-    const float a4[4] = {av.x, av.y, av.z, av.w};
-    float o[4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      const int jj = j0 + t;
-      o[t] = (jj < n) ? (float)((double)a4[t] + acc[t]) : 0.f;
-      if (jj < n) Pn[jj * lds + i] = o[t];  // transpose staged in smem (P+ is dead here)
+      const int jj = c0 + t * q4;
+      const float o = (jj < n) ? (float)((double)Ak[i * lds + jj] + acc[t]) : 0.f;
+      if (jj < n) Pn[jj * lds + i] = o;  // transpose staged in smem (P+ is dead here)
+      Ml[(size_t)i * ldg + jj] = o;
     }
-    *reinterpret_cast<float4*>(Ml + (size_t)i * ldg + j0) = make_float4(o[0], o[1], o[2], o[3]);
   }
   __syncthreads();
   // M^T rows: coalesced 16-byte stores instead of one scattered store per element
   for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
     const int jj = S.fd_q4.div(e), i0 = (e - jj * q4) << 2;
-    float v[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) v[t] = (i0 + t < n) ? Pn[jj * lds + i0 + t] : 0.f;
-    *reinterpret_cast<float4*>(MTl + (size_t)jj * ldg + i0) = make_float4(v[0], v[1], v[2], v[3]);
+    const float4 p = *reinterpret_cast<const float4*>(Pn + jj * lds + i0);
+    const float v[4] = {p.x, i0 + 1 < n ? p.y : 0.f, i0 + 2 < n ? p.z : 0.f, i0 + 3 < n ? p.w : 0.f};
+    *reinterpret_cast<float4*>(MTl + (size_t)jj * ldg + i0) = make_float4(i0 < n ? v[0] : 0.f, v[1], v[2], v[3]);
   }
 }
 
@@ -859,7 +857,7 @@ static int sls_synthesize_once(Ctx* c, const gsls_qp_t* qp, const float* E, cuda
   const size_t wk = 2 * kMaxM * (kMaxM + 1) + 8;
   {
     const size_t sbq = 8 * (size_t)(m * m + 2 * m * (m + 1) + 8) * sizeof(double);
-    const size_t sb = (2 * m * m + 4 * (size_t)m * ldg) * sizeof(double);
+    const size_t sb = (2 * m * m + 4 * (size_t)m * ldg + m) * sizeof(double);  // + BQT's odd stride
     if ((rc = smem_attr((const void*)k_sls_leaf, sb))) return rc;
     if ((rc = smem_attr((const void*)k_sls_qu_inverse, sbq))) return rc;
     ProfScope ps(P_SLS_LEAF, st, (double)S.ncell * B);
@@ -876,7 +874,7 @@ static int sls_synthesize_once(Ctx* c, const gsls_qp_t* qp, const float* E, cuda
     if ((rc = launch_combine(a, o1 - o0, B, st))) return rc;
   }
   {
-    const size_t sb = (3 * (size_t)m * ldg + 2 * m * m + 2 * m * (m + 1) + 8) * sizeof(double) +
+    const size_t sb = (3 * (size_t)m * ldg + 2 * m + 2 * m * m + 2 * m * (m + 1) + 8) * sizeof(double) +
                       2 * (size_t)n * lds_of(n) * sizeof(float);
     if ((rc = smem_attr((const void*)k_sls_gains, sb))) return rc;
     ProfScope ps(P_SLS_GAINS, st, (double)S.ncell * B);
