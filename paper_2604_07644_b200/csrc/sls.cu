@@ -385,6 +385,45 @@ __global__ void __launch_bounds__(256, 4) k_sls_leaf(DevSls S, gsls_qp_t qp) {
   // doubles of a row (the 4-wide column tiles put lanes 32 bytes apart: 2x the shared
   // wavefronts, the kernel being shared-memory bound)
   const int q4 = np >> 2;
+  auto epilogue = [&](int i, int jj, double p, double a, double cc) {
+    const bool in = jj < n;
+    const float po = in ? (float)(Qx[i * n + jj] - p) : 0.f;
+    const float ao = in ? (float)((double)Ak[i * n + jj] - a) : 0.f;
+    const float co = cfac ? (jj < m ? (float)BQT[jj * ldq + i] : 0.f) : (in ? (float)cc : 0.f);
+    if (in && !(dead & 2)) ATd[(size_t)jj * ldg + i] = ao;
+    Pd[(size_t)i * ldg + jj] = po;
+    if (!(dead & 1)) Ad[(size_t)i * ldg + jj] = ao;
+    if (!(dead & 4)) Cd[(size_t)i * ldg + jj] = co;
+  };
+  if (cfac) {  // C comes from BQT directly: 2x4 tiles (rows i, i + nh), one QQ row load feeds both
+    const int nh = (n + 1) >> 1;
+    for (int e = threadIdx.x; e < nh * q4; e += blockDim.x) {
+      const int i = S.fd_q4.div(e), c0 = e - i * q4;
+      const bool two = i + nh < n;
+      const int i1 = two ? i + nh : i;
+      double p0[4] = {0.0, 0.0, 0.0, 0.0}, a0[4] = {0.0, 0.0, 0.0, 0.0};
+      double p1[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int l = 0; l < m; ++l) {
+        const double qx0 = Qux[l * np + i], bt0 = BT[l * np + i];
+        const double qx1 = Qux[l * np + i1], bt1 = BT[l * np + i1];
+        const double* qr = QQ + l * np + c0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const double qq = qr[t * q4];
+          p0[t] = fma(qx0, qq, p0[t]);
+          a0[t] = fma(bt0, qq, a0[t]);
+          p1[t] = fma(qx1, qq, p1[t]);
+          a1[t] = fma(bt1, qq, a1[t]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        epilogue(i, c0 + t * q4, p0[t], a0[t], 0.0);
+        if (two) epilogue(i1, c0 + t * q4, p1[t], a1[t], 0.0);
+      }
+    }
+    return;
+  }
   for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
     const int i = S.fd_q4.div(e), c0 = e - i * q4;
     double p4[4] = {0.0, 0.0, 0.0, 0.0}, a4[4] = {0.0, 0.0, 0.0, 0.0}, c4[4] = {0.0, 0.0, 0.0, 0.0};
@@ -397,22 +436,11 @@ __global__ void __launch_bounds__(256, 4) k_sls_leaf(DevSls S, gsls_qp_t qp) {
         const double qq = qr[t * q4];
         p4[t] = fma(qx, qq, p4[t]);
         a4[t] = fma(bt, qq, a4[t]);
-        if (!cfac) c4[t] = fma(bq, br[t * q4], c4[t]);
+        c4[t] = fma(bq, br[t * q4], c4[t]);
       }
     }
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int jj = c0 + t * q4;
-      const bool in = jj < n;
-      const float po = in ? (float)(Qx[i * n + jj] - p4[t]) : 0.f;
-      const float ao = in ? (float)((double)Ak[i * n + jj] - a4[t]) : 0.f;
-      float co = in ? (float)c4[t] : 0.f;
-      if (cfac) co = jj < m ? (float)BQT[jj * ldq + i] : 0.f;
-      if (in && !(dead & 2)) ATd[(size_t)jj * ldg + i] = ao;
-      Pd[(size_t)i * ldg + jj] = po;
-      if (!(dead & 1)) Ad[(size_t)i * ldg + jj] = ao;
-      if (!(dead & 4)) Cd[(size_t)i * ldg + jj] = co;
-    }
+    for (int t = 0; t < 4; ++t) epilogue(i, c0 + t * q4, p4[t], a4[t], c4[t]);
   }
 }
 
@@ -479,20 +507,29 @@ __global__ void __launch_bounds__(256, 4) k_sls_gains(DevSls S, gsls_qp_t qp, co
   }
   cp_async_wait<0>();
   __syncthreads();
-  const int q4 = np >> 2;
-  for (int e = threadIdx.x; e < m * q4; e += blockDim.x) {  // B' P+ (1x4 tiles)
+  // The products below are register-blocked two or four rows deep: the kernel is bound by
+  // shared-memory wavefronts, and a row of the right operand loaded once feeds every row of
+  // the tile.  Each element keeps its own ascending fma chain.
+  const int q4 = np >> 2, mh = (m + 1) >> 1;
+  for (int e = threadIdx.x; e < mh * q4; e += blockDim.x) {  // B' P+ (2x4 tiles: rows l, l + mh)
     const int l = S.fd_q4.div(e), j0 = (e - l * q4) << 2;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const int l1 = l + mh < m ? l + mh : l;
+    double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
     for (int i = 0; i < n; ++i) {
-      const double b = BT[l * ldb + i];
+      const double b0 = BT[l * ldb + i], b1 = BT[l1 * ldb + i];
       const float4 pv = *reinterpret_cast<const float4*>(Pn + i * lds + j0);
-      acc[0] = fma(b, (double)pv.x, acc[0]);
-      acc[1] = fma(b, (double)pv.y, acc[1]);
-      acc[2] = fma(b, (double)pv.z, acc[2]);
-      acc[3] = fma(b, (double)pv.w, acc[3]);
+      const double p4[4] = {(double)pv.x, (double)pv.y, (double)pv.z, (double)pv.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        a0[t] = fma(b0, p4[t], a0[t]);
+        a1[t] = fma(b1, p4[t], a1[t]);
+      }
     }
 #pragma unroll
-    for (int t = 0; t < 4; ++t) BtP[l * ldb + j0 + t] = acc[t];
+    for (int t = 0; t < 4; ++t) {
+      BtP[l * ldb + j0 + t] = a0[t];
+      BtP[l1 * ldb + j0 + t] = (l1 != l) ? a1[t] : a0[t];
+    }
   }
   __syncthreads();
   const size_t cb = (size_t)inst * S.ncell + cell;
@@ -510,52 +547,81 @@ __global__ void __launch_bounds__(256, 4) k_sls_gains(DevSls S, gsls_qp_t qp, co
     if (warp_spd_inverse(H, m, Ga, m, wk, m + 1, m * (m + 1)) && threadIdx.x == 0)
       raise_err(S.err + inst, GSLS_ERR_SINGULAR_STAGE, k, j, GSLS_LABEL_QU_BPB);
   }
-  for (int e = (int)threadIdx.x - 32; e >= 0 && e < m * q4; e += (int)blockDim.x - 32) {  // 1x4 tiles
+  for (int e = (int)threadIdx.x - 32; e >= 0 && e < mh * q4; e += (int)blockDim.x - 32) {  // 2x4 tiles
     const int l = S.fd_q4.div(e), j0 = (e - l * q4) << 2;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const int l1 = l + mh < m ? l + mh : l;
+    double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
     for (int i = 0; i < n; ++i) {
-      const double b = BtP[l * ldb + i];
+      const double b0 = BtP[l * ldb + i], b1 = BtP[l1 * ldb + i];
       const float4 av = *reinterpret_cast<const float4*>(Ak + i * lds + j0);
-      acc[0] = fma(b, (double)av.x, acc[0]);
-      acc[1] = fma(b, (double)av.y, acc[1]);
-      acc[2] = fma(b, (double)av.z, acc[2]);
-      acc[3] = fma(b, (double)av.w, acc[3]);
+      const double v4[4] = {(double)av.x, (double)av.y, (double)av.z, (double)av.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        a0[t] = fma(b0, v4[t], a0[t]);
+        a1[t] = fma(b1, v4[t], a1[t]);
+      }
     }
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const int jj = j0 + t;
-      Gm[l * np + jj] = (jj < n) ? Qux[l * n + jj] + acc[t] : 0.0;
+      Gm[l * np + jj] = (jj < n) ? Qux[l * n + jj] + a0[t] : 0.0;
+      if (l1 != l) Gm[l1 * np + jj] = (jj < n) ? Qux[l1 * n + jj] + a1[t] : 0.0;
     }
   }
   __syncthreads();
   float* Kg = S.Kc + cb * m * n;
-  for (int e = threadIdx.x; e < m * np; e += blockDim.x) {
+  const int mq = (m + 3) >> 2;
+  for (int e = threadIdx.x; e < mq * np; e += blockDim.x) {  // K = -H^-1 G, rows l + r mq (r < 4)
     const int l = S.fd_ldg.div(e), jj = e - l * np;
-    double s = 0.0;
-    for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Gm[t * np + jj], s);
-    Ks[l * ldb + jj] = -s;
-    if (jj < n) Kg[l * n + jj] = (float)(-s);
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int t = 0; t < m; ++t) {
+      const double g = Gm[t * np + jj];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (l + r * mq < m) s[r] = fma(Ga[(l + r * mq) * m + t], g, s[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int lr = l + r * mq;
+      if (lr < m) {
+        Ks[lr * ldb + jj] = -s[r];
+        if (jj < n) Kg[lr * n + jj] = (float)(-s[r]);
+      }
+    }
   }
   __syncthreads();
   float* Ml = Mbase + (size_t)(cell_of(N, k + 1, j) - S.cell0) * MS;  // product leaf of position k
   float* MTl = MTbase + (size_t)(cell_of(N, k + 1, j) - S.cell0) * MS;
   // A + B K, 1x4 tiles over columns c, c + q4, c + 2 q4, c + 3 q4 (lanes on consecutive
   // doubles of a K row; 4-wide column tiles put them 32 bytes apart)
-  for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
+  // rows i and i + nh of each 2x4 tile
+  const int nh = (n + 1) >> 1;
+  for (int e = threadIdx.x; e < nh * q4; e += blockDim.x) {
     const int i = S.fd_q4.div(e), c0 = e - i * q4;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const bool two = i + nh < n;
+    const int i1 = two ? i + nh : i;
+    double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
     for (int l = 0; l < m; ++l) {
-      const double b = BT[l * ldb + i];
+      const double b0 = BT[l * ldb + i], b1 = BT[l * ldb + i1];
       const double* kr = Ks + l * ldb + c0;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) acc[t] = fma(b, kr[t * q4], acc[t]);
+      for (int t = 0; t < 4; ++t) {
+        const double kv = kr[t * q4];
+        a0[t] = fma(b0, kv, a0[t]);
+        a1[t] = fma(b1, kv, a1[t]);
+      }
     }
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const int jj = c0 + t * q4;
-      const float o = (jj < n) ? (float)((double)Ak[i * lds + jj] + acc[t]) : 0.f;
-      if (jj < n) Pn[jj * lds + i] = o;  // transpose staged in smem (P+ is dead here)
-      Ml[(size_t)i * ldg + jj] = o;
+      const float o0 = (jj < n) ? (float)((double)Ak[i * lds + jj] + a0[t]) : 0.f;
+      if (jj < n) Pn[jj * lds + i] = o0;  // transpose staged in smem (P+ is dead here)
+      Ml[(size_t)i * ldg + jj] = o0;
+      if (two) {
+        const float o1 = (jj < n) ? (float)((double)Ak[i1 * lds + jj] + a1[t]) : 0.f;
+        if (jj < n) Pn[jj * lds + i1] = o1;
+        Ml[(size_t)i1 * ldg + jj] = o1;
+      }
     }
   }
   __syncthreads();

@@ -305,9 +305,19 @@ __device__ inline int warp_spd_inverse(const T* M, int ldm, T* inv, int m, T* wo
       }
       if (lane > j && lane < m) L[lane * ld + j] *= r;
       __syncwarp();
-      if (lane > j && lane < m) {
+      if (lane > j && lane < m) {  // row lane: independent updates, loads batched 4 deep
         const T lij = L[lane * ld + j];
-        for (int l = j + 1; l <= lane; ++l) L[lane * ld + l] = fma(-lij, L[l * ld + j], L[lane * ld + l]);
+        T* row = L + lane * ld;
+        int l = j + 1;
+        for (; l + 3 <= lane; l += 4) {
+          const T c0 = L[l * ld + j], c1 = L[(l + 1) * ld + j], c2 = L[(l + 2) * ld + j], c3 = L[(l + 3) * ld + j];
+          const T v0 = row[l], v1 = row[l + 1], v2 = row[l + 2], v3 = row[l + 3];
+          row[l] = fma(-lij, c0, v0);
+          row[l + 1] = fma(-lij, c1, v1);
+          row[l + 2] = fma(-lij, c2, v2);
+          row[l + 3] = fma(-lij, c3, v3);
+        }
+        for (; l <= lane; ++l) row[l] = fma(-lij, L[l * ld + j], row[l]);
       }
       __syncwarp();
     }
@@ -315,14 +325,27 @@ __device__ inline int warp_spd_inverse(const T* M, int ldm, T* inv, int m, T* wo
       if (attempt == 1) return 1;
       continue;
     }
-    {  // X = L^{-1}: lane j solves L x = e_j
+    {  // X = L^{-1}: lane j solves L x = e_j, right-looking with X's column j as the
+       // accumulators (row i still receives -L[i][k] x_k for k = j .. i-1 in ascending order,
+       // the same fma chain as the row-by-row solve, but the rows below k update in parallel)
       const int j = lane;
-      for (int i = 0; i < m; ++i) {
-        const T ri = __shfl_sync(0xffffffffu, rd, i);
-        if (j < m) {
-          T s = (i == j) ? T(1) : T(0);
-          for (int k = j; k < i; ++k) s = fma(-L[i * ld + k], X[k * ld + j], s);
-          X[i * ld + j] = (i < j) ? T(0) : s * ri;
+      if (j < m)
+        for (int i = 0; i < m; ++i) X[i * ld + j] = (i == j) ? T(1) : T(0);
+      for (int k = 0; k < m; ++k) {
+        const T rk = __shfl_sync(0xffffffffu, rd, k);
+        if (j < m && k >= j) {
+          const T xk = X[k * ld + j] * rk;
+          X[k * ld + j] = xk;
+          int i = k + 1;
+          for (; i + 3 < m; i += 4) {
+            const T l0 = L[i * ld + k], l1 = L[(i + 1) * ld + k], l2 = L[(i + 2) * ld + k], l3 = L[(i + 3) * ld + k];
+            const T a0 = X[i * ld + j], a1 = X[(i + 1) * ld + j], a2 = X[(i + 2) * ld + j], a3 = X[(i + 3) * ld + j];
+            X[i * ld + j] = fma(-l0, xk, a0);
+            X[(i + 1) * ld + j] = fma(-l1, xk, a1);
+            X[(i + 2) * ld + j] = fma(-l2, xk, a2);
+            X[(i + 3) * ld + j] = fma(-l3, xk, a3);
+          }
+          for (; i < m; ++i) X[i * ld + j] = fma(-L[i * ld + k], xk, X[i * ld + j]);
         }
       }
     }
