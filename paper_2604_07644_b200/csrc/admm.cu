@@ -2042,7 +2042,13 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
         if (std::find(rebuild.begin(), rebuild.end(), i) == rebuild.end()) cont.push_back(i);
       if (nreb > 0) {
         if (!c->side) {
-          GSLS_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+          // highest priority: the rebuild chain's CTAs (and the rebuilt instances' replay)
+          // take SM slots as the main stream's replay CTAs retire, instead of queueing
+          // behind the whole wave (GSLS_SIDE_PRIORITY=0: default priority)
+          int lo = 0, hi = 0;
+          GSLS_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+          const char* pe = getenv("GSLS_SIDE_PRIORITY");
+          GSLS_CUDA_CHECK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, (pe && pe[0] == '0') ? lo : hi));
           GSLS_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
           GSLS_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         }
