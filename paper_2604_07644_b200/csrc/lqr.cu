@@ -165,8 +165,9 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   extern __shared__ double smd[];
   double* Cst = smd;                 // c x n
   double* Dst = Cst + c * n;         // c x m
-  double* Bst = Dst + c * m;         // n x m
-  double* Sh = Bst + n * m;          // m x n
+  const int ldb = m | 1;             // odd row stride: rows of B read across lanes hit distinct banks
+  double* Bst = Dst + c * m;         // n x ldb
+  double* Sh = Bst + n * ldb;        // m x n
   double* Rh = Sh + m * n;           // m x m
   double* Ri = Rh + m * m;           // m x m
   double* RS = Ri + m * m;           // m x n
@@ -178,7 +179,10 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   const float* Bg = qp.B + st * n * m;
   for (int e = threadIdx.x; e < c * n; e += blockDim.x) Cst[e] = Cg[e];
   for (int e = threadIdx.x; e < c * m; e += blockDim.x) Dst[e] = Dg[e];
-  for (int e = threadIdx.x; e < n * m; e += blockDim.x) Bst[e] = Bg[e];
+  for (int e = threadIdx.x; e < n * m; e += blockDim.x) {
+    const int i = L.fd_m.div(e);
+    Bst[i * ldb + (e - i * m)] = Bg[e];
+  }
   __syncthreads();
   const float* Rg = qp.R + st * m * m;
   const float* Sg = qp.S ? qp.S + st * m * n : nullptr;
@@ -210,7 +214,7 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   for (int e = threadIdx.x; e < n * m; e += blockDim.x) {
     const int i = L.fd_m.div(e), l = e - i * m;
     double s = 0.0;
-    for (int t = 0; t < m; ++t) s = fma(Bst[i * m + t], Ri[t * m + l], s);
+    for (int t = 0; t < m; ++t) s = fma(Bst[i * ldb + t], Ri[t * m + l], s);
     BR[e] = s;
   }
   __syncthreads();
@@ -225,22 +229,25 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
     double p = 0.0, a = 0.0, cc = 0.0;
     if (cfac && j < m) {
       double f = 0.0;
-      for (int b = 0; b <= j; ++b) f = fma(Bst[i * m + b], Linv[j * (kMaxM + 1) + b], f);
+      for (int b = 0; b <= j; ++b) f = fma(Bst[i * ldb + b], Linv[j * (kMaxM + 1) + b], f);
       cc = f;
     }
     if (j < n) {
       double s = 0.0;
       for (int r = 0; r < c; ++r) s = fma(Cst[r * n + i], Cst[r * n + j], s);
       const double qh = (double)Qg[i * n + j] + rho * s;
-      double sr = 0.0, br = 0.0, bb = 0.0;
+      double sr = 0.0, br = 0.0;
       for (int l = 0; l < m; ++l) {
         sr = fma(Sh[l * n + i], RS[l * n + j], sr);
-        br = fma(Bst[i * m + l], RS[l * n + j], br);
-        bb = fma(BR[i * m + l], Bst[j * m + l], bb);
+        br = fma(Bst[i * ldb + l], RS[l * n + j], br);
       }
       p = qh - sr;
       a = (double)Ag[i * n + j] - br;
-      if (!cfac) cc = bb;
+      if (!cfac) {  // dense C-hat = B R-hat^-1 B' (a factored leaf carries B L^-T instead)
+        double bb = 0.0;
+        for (int l = 0; l < m; ++l) bb = fma(BR[i * m + l], Bst[j * ldb + l], bb);
+        cc = bb;
+      }
     }
     Pd[e] = (float)p;
     Ad[e] = (float)a;
@@ -286,7 +293,7 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
     } else if (i < 2 * n) {
       const int ii = i - n;
       double s = 0.0;
-      for (int l = 0; l < m; ++l) s = fma(Bst[ii * m + l], X1[l * c + r], s);
+      for (int l = 0; l < m; ++l) s = fma(Bst[ii * ldb + l], X1[l * c + r], s);
       v = -s;
     }
     X23[e] = (float)v;
@@ -300,14 +307,14 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
       for (int l = 0; l < m; ++l) s = fma(Sh[l * n + i], om0[l], s);
       pb0[i] = qg[i] - s;
     } else {
-      for (int l = 0; l < m; ++l) s = fma(Bst[(i - n) * m + l], om0[l], s);
+      for (int l = 0; l < m; ++l) s = fma(Bst[(i - n) * ldb + l], om0[l], s);
       pb0[i] = bg[i - n] - s;
     }
   }
   float* Bcm = L.Bcm + st * (size_t)m * ldn;
   for (int e = threadIdx.x; e < m * ldn; e += blockDim.x) {
     const int j = L.fd_ldn.div(e), i = e - j * ldn;
-    Bcm[e] = (i < n) ? (float)Bst[i * m + j] : 0.f;
+    Bcm[e] = (i < n) ? (float)Bst[i * ldb + j] : 0.f;
   }
   float* Dcm = L.ZD + st * (size_t)(n + m) * ldc + (size_t)n * ldc;  // D columns of [Z D]
   for (int e = threadIdx.x; e < m * ldc; e += blockDim.x) {
@@ -575,7 +582,8 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
   double* Ga = Gm + m * n;       // m x m
   double* Ks = Ga + m * m;       // m x n
   double* wk = Ks + m * n;
-  float* Abar = reinterpret_cast<float*>(wk + 2 * kMaxM * (kMaxM + 1) + 8 + L.c * m + m);  // n x ldg (float)
+  const int ldd = m | 1;  // D's row stride (odd: the Z = C + D K loop reads D by column across lanes)
+  float* Abar = reinterpret_cast<float*>(wk + 2 * kMaxM * (kMaxM + 1) + 8 + L.c * ldd + m);  // n x ldg (float)
   const size_t st = (size_t)inst * N + k;
   const float* Pn = L.Ps + ((size_t)inst * L.cvf_nslots + L.cvf_out[k + 1]) * MS;
   const float* Bg = qp.B + st * n * m;
@@ -647,10 +655,13 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
   //   kf = kk0 + X5 p+ + X4 w with X5 = -Gamma B', X4 = -rho Gamma D', kk0 = -Gamma (B' cvec + r)
   //   G  = Z dx + D kf with Z = C + D K
   {
-    double* Dst = wk + 2 * kMaxM * (kMaxM + 1) + 8;  // c x m (Abar follows tk)
-    double* tk = Dst + c * m;                         // m
+    double* Dst = wk + 2 * kMaxM * (kMaxM + 1) + 8;  // c x ldd (Abar follows tk)
+    double* tk = Dst + c * ldd;                       // m
     const float* Dg = qp.D + st * c * m;
-    for (int e = threadIdx.x; e < c * m; e += blockDim.x) Dst[e] = Dg[e];
+    for (int e = threadIdx.x; e < c * m; e += blockDim.x) {
+      const int r = L.fd_m.div(e);
+      Dst[r * ldd + (e - r * m)] = Dg[e];
+    }
     __syncthreads();
     const double* rg = qp.r + st * m;
     for (int l = threadIdx.x; l < m; l += blockDim.x) {
@@ -673,7 +684,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
       const int r = L.fd_ldm.div(e), l = e - r * ldm;
       double s = 0.0;
       if (l < m)
-        for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Dst[r * m + t], s);
+        for (int t = 0; t < m; ++t) s = fma(Ga[l * m + t], Dst[r * ldd + t], s);
       X4[e] = (float)(-rho * s);
     }
     double* kk0 = L.kk0 + st * m;
@@ -689,7 +700,7 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
       double v = 0.0;
       if (r < c) {
         double s = (double)Cg[r * n + i];
-        for (int l = 0; l < m; ++l) s = fma(Dst[r * m + l], Ks[l * n + i], s);
+        for (int l = 0; l < m; ++l) s = fma(Dst[r * ldd + l], Ks[l * n + i], s);
         v = s;
       }
       Zcm[e] = (float)v;
@@ -731,12 +742,12 @@ __global__ void __launch_bounds__(512) k_cot_combine(DevLqr L, const int4* ops, 
 // ---------------------------------------------------------------------------
 // host driver
 
-static size_t leaf_smem_bytes(int n, int m, int c) {
-  return (size_t)(c * n + c * m + n * m + m * n + 2 * m * m + m * n + n * m + 2 * kMaxM * (kMaxM + 1) + 8 + m * c + m) *
+static size_t leaf_smem_bytes(int n, int m, int c) {  // B at row stride m | 1
+  return (size_t)(c * n + c * m + n * (m | 1) + m * n + 2 * m * m + m * n + n * m + 2 * kMaxM * (kMaxM + 1) + 8 + m * c + m) *
          sizeof(double);
 }
-static size_t gains_smem_bytes(int n, int m, int c) {
-  return (size_t)(n * m + m * n + m * m + m * n + m * m + m * n + 2 * kMaxM * (kMaxM + 1) + 8 + c * m + m) *
+static size_t gains_smem_bytes(int n, int m, int c) {  // D at row stride m | 1
+  return (size_t)(n * m + m * n + m * m + m * n + m * m + m * n + 2 * kMaxM * (kMaxM + 1) + 8 + c * (m | 1) + m) *
              sizeof(double) +
          (size_t)n * ldg_of(n) * sizeof(float);
 }

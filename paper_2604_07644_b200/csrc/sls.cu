@@ -697,20 +697,23 @@ __global__ void __launch_bounds__(256) k_sls_phiu(DevSls S) {
 }
 
 // Row norms of C_k Phi^x + D_k Phi^u (terminal cells: CN Phi^x), sls.py:146-147, :167, :336, :340.
-__global__ void __launch_bounds__(256) k_sls_rownorm(DevSls S, gsls_qp_t qp) {
+__global__ void __launch_bounds__(256, 5) k_sls_rownorm(DevSls S, gsls_qp_t qp) {
   const int cell = blockIdx.x, inst = blockIdx.y;
   const int k = S.cell_kj[cell].x;
   const int n = S.n, m = S.m, c = S.c, nf = S.nf, N = S.N, ldg = S.ldg;
   const size_t MS = (size_t)n * ldg;
   extern __shared__ float sm[];
   float* Px = sm;            // n x ldg
-  float* Pu = Px + n * ldg;  // m x n
+  float* Pu = Px + n * ldg;  // m x ldg (zero beyond n: 16-byte row loads)
   const float* Pg = S.Ms + ((size_t)inst * S.mp_nslots + S.mp_out[cell]) * MS;
   const size_t cb = (size_t)inst * S.ncell + cell;
   for (int e = threadIdx.x; e < (n * ldg) >> 2; e += blockDim.x) cp_async16(Px + 4 * e, Pg + 4 * e);
   cp_async_commit();
   if (k < N)
-    for (int e = threadIdx.x; e < m * n; e += blockDim.x) Pu[e] = S.Phiu[cb * m * n + e];
+    for (int e = threadIdx.x; e < m * ldg; e += blockDim.x) {
+      const int a = S.fd_ldg.div(e), i = e - a * ldg;
+      Pu[e] = i < n ? S.Phiu[cb * m * n + a * n + i] : 0.f;
+    }
   cp_async_wait<0>();
   __syncthreads();
   double* rn = S.rn + cb * S.cmax;
@@ -732,37 +735,53 @@ __global__ void __launch_bounds__(256) k_sls_rownorm(DevSls S, gsls_qp_t qp) {
   const size_t st = (size_t)inst * N + k;
   const float* Ck = qp.C + st * c * n;
   const float* Dk = qp.D + st * c * m;
-  // C_k, D_k staged in smem; thread task = (row r, 4 columns): 4 independent FMA chains
-  // per l from one broadcast C value and one 16-byte Phi^x row load
-  float* Cs = Pu + m * n;          // c x n
+  // C_k, D_k staged in smem; thread task = (rows r and r + ch, 4 columns): 8 independent
+  // FMA chains per l from two broadcast C values and one 16-byte Phi^x row load (the
+  // kernel is bound by shared-memory wavefronts)
+  float* Cs = Pu + m * ldg;        // c x n
   float* Ds = Cs + c * n;          // c x m
-  const int poff = (n * ldg + m * n + c * n + c * m + 1) & ~1;        // 8-byte aligned
+  const int poff = (n * ldg + m * ldg + c * n + c * m + 1) & ~1;      // 8-byte aligned
   double* part = reinterpret_cast<double*>(sm + poff);              // c x q4 partial sums of squares
   for (int e = threadIdx.x; e < c * n; e += blockDim.x) Cs[e] = Ck[e];
   for (int e = threadIdx.x; e < c * m; e += blockDim.x) Ds[e] = Dk[e];
   __syncthreads();
-  const int q4 = ldg >> 2;
-  for (int t = threadIdx.x; t < c * q4; t += blockDim.x) {
+  const int q4 = ldg >> 2, ch = (c + 1) >> 1;
+  for (int t = threadIdx.x; t < ch * q4; t += blockDim.x) {
     const int r = t / q4, i0 = (t - r * q4) << 2;
-    float s[4] = {0.f, 0.f, 0.f, 0.f}, u[4] = {0.f, 0.f, 0.f, 0.f};
+    const bool two = r + ch < c;
+    const int r1 = two ? r + ch : r;
+    float s0[4] = {0.f, 0.f, 0.f, 0.f}, u0[4] = {0.f, 0.f, 0.f, 0.f};
+    float s1[4] = {0.f, 0.f, 0.f, 0.f}, u1[4] = {0.f, 0.f, 0.f, 0.f};
     for (int l = 0; l < n; ++l) {
-      const float cv = Cs[r * n + l];
+      const float c0 = Cs[r * n + l], c1 = Cs[r1 * n + l];
       const float4 p = *reinterpret_cast<const float4*>(Px + l * ldg + i0);
-      s[0] = fmaf(cv, p.x, s[0]); s[1] = fmaf(cv, p.y, s[1]); s[2] = fmaf(cv, p.z, s[2]); s[3] = fmaf(cv, p.w, s[3]);
+      const float pv[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        s0[q] = fmaf(c0, pv[q], s0[q]);
+        s1[q] = fmaf(c1, pv[q], s1[q]);
+      }
     }
     for (int a = 0; a < m; ++a) {
-      const float dv = Ds[r * m + a];
+      const float d0 = Ds[r * m + a], d1 = Ds[r1 * m + a];
+      const float4 p = *reinterpret_cast<const float4*>(Pu + a * ldg + i0);
+      const float pv[4] = {p.x, p.y, p.z, p.w};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) u[q] = fmaf(dv, (i0 + q < n) ? Pu[a * n + i0 + q] : 0.f, u[q]);
+      for (int q = 0; q < 4; ++q) {
+        u0[q] = fmaf(d0, pv[q], u0[q]);
+        u1[q] = fmaf(d1, pv[q], u1[q]);
+      }
     }
-    double ss = 0.0;
+    double ss0 = 0.0, ss1 = 0.0;
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (i0 + q < n) {
-        const double v = (double)(s[q] + u[q]);
-        ss += v * v;
+        const double v0 = (double)(s0[q] + u0[q]), v1 = (double)(s1[q] + u1[q]);
+        ss0 += v0 * v0;
+        ss1 += v1 * v1;
       }
-    part[t] = ss;
+    part[r * q4 + (i0 >> 2)] = ss0;
+    if (two) part[r1 * q4 + (i0 >> 2)] = ss1;
   }
   __syncthreads();
   for (int r = warp; r < c; r += nw) {
@@ -972,7 +991,7 @@ static int sls_synthesize_once(Ctx* c, const gsls_qp_t* qp, const float* E, cuda
 
 static int sls_rownorms(Ctx* c, const gsls_qp_t* qp, cudaStream_t st) {
   DevSls& S = sls_of(c)->dev;
-  const size_t sb = (((size_t)S.n * S.ldg + S.m * S.n + (size_t)S.c * S.n + S.c * S.m + 1) & ~(size_t)1) * sizeof(float) +
+  const size_t sb = (((size_t)S.n * S.ldg + S.m * S.ldg + (size_t)S.c * S.n + S.c * S.m + 1) & ~(size_t)1) * sizeof(float) +
                     (size_t)S.c * (S.ldg / 4) * sizeof(double);
   int rc = smem_attr((const void*)k_sls_rownorm, sb);
   if (rc) return rc;
