@@ -237,20 +237,24 @@ __global__ void __launch_bounds__(256) k_sls_assemble(DevSls S, gsls_qp_t qp, co
     }
   __syncthreads();
   const float* Qb = term ? QbarN + (size_t)inst * wst * n * n : Qbar + (size_t)inst * wst * n * n;
+  // 1x4 tiles over columns c, c + q4, c + 2 q4, c + 3 q4: a warp stores whole runs of a Qx
+  // row (4 adjacent columns per lane wrote one 8-byte word per 32-byte sector per store)
   const int q4 = (n + 3) >> 2;
   for (int e = threadIdx.x; e < n * q4; e += blockDim.x) {
-    const int i = S.fd_q4.div(e), j0 = (e - i * q4) << 2;
+    const int i = S.fd_q4.div(e), c0 = e - i * q4;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int a = 0; a < na; ++a) {
       const double w = Cw[a * n + i];
-      const double* cr = Cr + a * n + j0;
+      const double* cr = Cr + a * n + c0;
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (j0 + t < n) acc[t] = fma(w, cr[t], acc[t]);
+        if (c0 + t * q4 < n) acc[t] = fma(w, cr[t * q4], acc[t]);
     }
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (j0 + t < n) Qx[i * n + j0 + t] = acc[t] + (double)Qb[i * n + j0 + t];
+    for (int t = 0; t < 4; ++t) {
+      const int jj = c0 + t * q4;
+      if (jj < n) Qx[i * n + jj] = acc[t] + (double)Qb[i * n + jj];
+    }
   }
   if (term) return;
   const float* Rb = Rbar + (size_t)inst * wst * m * m;
