@@ -682,21 +682,33 @@ __global__ void __launch_bounds__(256) k_sls_phiu(DevSls S) {
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
-  // Phi^u = K Phi^x: thread task = (row a, 4 columns), one broadcast K value and one
-  // 16-byte Phi^x row load per l
-  const int q4 = ldg >> 2;
-  for (int t = threadIdx.x; t < m * q4; t += blockDim.x) {
-    const int a = t / q4, i0 = (t - a * q4) << 2;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  // Phi^u = K Phi^x: thread task = (rows a and a + mh, columns c, c + q4, c + 2 q4, c + 3 q4):
+  // two broadcast K values and four consecutive-lane Phi^x loads per l, and whole warp runs
+  // of a Phi^u row per store (each element keeps its ascending fma chain)
+  const int q4 = ldg >> 2, mh = (m + 1) >> 1;
+  for (int t = threadIdx.x; t < mh * q4; t += blockDim.x) {
+    const int a = t / q4, c0 = t - a * q4;
+    const bool two = a + mh < m;
+    const int a1 = two ? a + mh : a;
+    float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
     for (int l = 0; l < n; ++l) {
-      const float kv = Ks[a * n + l];
-      const float4 p = *reinterpret_cast<const float4*>(Px + l * ldg + i0);
-      s0 = fmaf(kv, p.x, s0); s1 = fmaf(kv, p.y, s1); s2 = fmaf(kv, p.z, s2); s3 = fmaf(kv, p.w, s3);
-    }
-    const float sv[4] = {s0, s1, s2, s3};
+      const float k0 = Ks[a * n + l], k1 = Ks[a1 * n + l];
+      const float* pr = Px + l * ldg + c0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (i0 + q < n) Pug[a * n + i0 + q] = sv[q];
+      for (int q = 0; q < 4; ++q) {
+        const float p = pr[q * q4];
+        s0[q] = fmaf(k0, p, s0[q]);
+        s1[q] = fmaf(k1, p, s1[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = c0 + q * q4;
+      if (i < n) {
+        Pug[a * n + i] = s0[q];
+        if (two) Pug[a1 * n + i] = s1[q];
+      }
+    }
   }
 }
 
