@@ -2000,6 +2000,16 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
   // instance (no side-stream overlap), so per-family device times add up (bench phases)
   const char* serenv = getenv("GSLS_ADMM_SERIAL");
   const bool serial = serenv && serenv[0] == '1';
+  // Lagged rebuilds (large waves only): the instances that committed a rho change are rebuilt
+  // on the side stream during the next wave and rejoin one wave later, catching up by running
+  // to the following decision point, instead of replaying behind their rebuild in the same
+  // wave.  Every instance's iterates are the same either way (pauses resume bitwise).
+  // GSLS_ADMM_LAG_MIN: smallest wave (instances) that lags, default 2 per SM (where a
+  // wave's replay outlasts a lagged instance's catch-up); 0 disables.  B = 1024: bulk waves
+  // 56.8 -> 53.1 ms, step 240.7 -> 237.4 ms, the tail unchanged (50 waves either way).
+  const char* lagenv = getenv("GSLS_ADMM_LAG_MIN");
+  const int lag_min = lagenv ? atoi(lagenv) : 2 * sms;
+  std::vector<char> lagged(B, 0);  // built during the last wave, not yet replayed
   cudaEvent_t ev[3] = {};
   if (verbose) for (auto& e : ev) cudaEventCreate(&e);
   int wave = 0;
@@ -2038,8 +2048,13 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
       // instances that committed a rho change are rebuilt and replayed on the side stream
       // while the others continue on the main stream (disjoint instances and cache slices)
       std::vector<int> cont;
+      const bool lag = lag_min > 0 && cnt >= lag_min;
+      if (lag)  // last wave's lagged instances first: their CTAs start first and have the longest run
+        for (int i : list)
+          if (lagged[i]) cont.push_back(i);
       for (int i : list)
-        if (std::find(rebuild.begin(), rebuild.end(), i) == rebuild.end()) cont.push_back(i);
+        if (!(lag && lagged[i]) && std::find(rebuild.begin(), rebuild.end(), i) == rebuild.end()) cont.push_back(i);
+      std::fill(lagged.begin(), lagged.end(), 0);
       if (nreb > 0) {
         if (!c->side) {
           // highest priority: the rebuild chain's CTAs (and the rebuilt instances' replay)
@@ -2058,7 +2073,10 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
                                         c->side));
         if ((rc = build_cache(c, qp, state->rho, c->d_build_list, nreb, c->side))) return rc;
         for (int i : rebuild) builds[i]++;
-        if ((rc = replay_wave(rebuild, c->d_build_list, c->side))) return rc;
+        if (lag)
+          for (int i : rebuild) lagged[i] = 1;
+        else if ((rc = replay_wave(rebuild, c->d_build_list, c->side)))
+          return rc;
         GSLS_CUDA_CHECK(cudaEventRecord(c->ev_join, c->side));
       }
       rc = replay_wave(cont, c->d_inst_list, st);
@@ -2080,7 +2098,8 @@ int admm_solve(Ctx* c, const gsls_qp_t* qp, const gsls_admm_settings_t* s, gsls_
     ++wave;
     std::vector<int> next, nrb;
     for (int i : list) {
-      if (status[i] == ST_REBUILD) { next.push_back(i); nrb.push_back(i); }
+      if (lagged[i]) next.push_back(i);  // rebuilt this wave, replays in the next
+      else if (status[i] == ST_REBUILD) { next.push_back(i); nrb.push_back(i); }
       else if (status[i] == ST_CONTINUE) next.push_back(i);
       else if (status[i] == ST_BUILD_ERR) { next.push_back(i); nrb.push_back(i); builds[i]--; }
     }
