@@ -128,6 +128,13 @@ int check_errors(Ctx* c, cudaStream_t st, const char* what) {
 
 __device__ inline int inst_of(const int* list) { return list ? list[blockIdx.y] : (int)blockIdx.y; }
 
+// One bulk L2 prefetch of a contiguous operand read after the kernel's first phase.
+__device__ inline void lqr_prefetch_l2(const void* p, size_t bytes) {
+  const unsigned long long a = (unsigned long long)p & ~15ull;
+  const unsigned long long e = ((unsigned long long)p + bytes + 15ull) & ~15ull;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
+}
+
 // CVF leaves (Eq. 29) with penalty augmentation rho (0 for a plain LQR).
 // Computed in float64: the Schur complement Q^ - S^' R^-1 S^ cancels O(rho)
 // terms; only the result is rounded to the float32 scan storage.
@@ -174,6 +181,10 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   double* BR = RS + m * n;           // n x m
   double* wk = BR + n * m;           // spd work
   const size_t st = (size_t)inst * N + k;
+  if (threadIdx.x == 0) {  // Q_k and A_k: read once per element by the P / A loop after the inverse
+    lqr_prefetch_l2(qp.Q + st * n * n, (size_t)n * n * sizeof(float));
+    lqr_prefetch_l2(qp.A + st * n * n, (size_t)n * n * sizeof(float));
+  }
   const float* Cg = qp.C + st * c * n;
   const float* Dg = qp.D + st * c * m;
   const float* Bg = qp.B + st * n * m;
@@ -566,6 +577,7 @@ int matmul_threads(int n) {
   return t;
 }
 
+
 // Gains, closed loop and COT leaves per stage (lqr.py:398-404, :349-356), in float64.
 __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const double* rho_arr, const int* list) {
   if (L.build_count && (int)blockIdx.y >= *L.build_count) return;
@@ -583,16 +595,22 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
   double* Ks = Ga + m * m;       // m x n
   double* wk = Ks + m * n;
   const int ldd = m | 1;  // D's row stride (odd: the Z = C + D K loop reads D by column across lanes)
-  float* Abar = reinterpret_cast<float*>(wk + 2 * kMaxM * (kMaxM + 1) + 8 + L.c * ldd + m);  // n x ldg (float)
+  // n x ldg floats, 16-byte aligned; holds P+ (16-byte async copies) until Abar replaces it
+  float* Abar = reinterpret_cast<float*>(wk + ((2 * kMaxM * (kMaxM + 1) + 8 + L.c * ldd + m + 1) & ~1));
   const size_t st = (size_t)inst * N + k;
   const float* Pn = L.Ps + ((size_t)inst * L.cvf_nslots + L.cvf_out[k + 1]) * MS;
   const float* Bg = qp.B + st * n * m;
+  if (threadIdx.x == 0) lqr_prefetch_l2(qp.A + st * n * n, (size_t)n * n * sizeof(float));  // read by G and A + B K
+  float* Pns = Abar;
+  for (int e = threadIdx.x; e < (n * ldg) >> 2; e += blockDim.x) cp_async16(Pns + 4 * e, Pn + 4 * e);
+  cp_async_commit();
   for (int e = threadIdx.x; e < n * m; e += blockDim.x) Bst[e] = Bg[e];
+  cp_async_wait<0>();
   __syncthreads();
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     const int l = L.fd_n.div(e), j = e - l * n;
     double s = 0.0;
-    for (int i = 0; i < n; ++i) s = fma(Bst[i * m + l], (double)Pn[i * ldg + j], s);
+    for (int i = 0; i < n; ++i) s = fma(Bst[i * m + l], (double)Pns[i * ldg + j], s);
     BtP[e] = s;
   }
   __syncthreads();
@@ -747,7 +765,7 @@ static size_t leaf_smem_bytes(int n, int m, int c) {  // B at row stride m | 1
          sizeof(double);
 }
 static size_t gains_smem_bytes(int n, int m, int c) {  // D at row stride m | 1
-  return (size_t)(n * m + m * n + m * m + m * n + m * m + m * n + 2 * kMaxM * (kMaxM + 1) + 8 + c * (m | 1) + m) *
+  return (size_t)(n * m + m * n + m * m + m * n + m * m + m * n + 2 * kMaxM * (kMaxM + 1) + 8 + c * (m | 1) + m + 1) *
              sizeof(double) +
          (size_t)n * ldg_of(n) * sizeof(float);
 }
