@@ -638,6 +638,12 @@ __global__ void __launch_bounds__(256, 4) k_sls_gains(DevSls S, gsls_qp_t qp, co
   }
 }
 
+// k_matprod threads: one per 8 x 4 tile of the padded product (gemm_tn84), >= 2 warps.
+static int matprod_threads(int n) {
+  const int np = ldg_of(n), tiles = ((np + 7) / 8) * (np / 4);
+  return std::max(64, std::min(512, (tiles + 31) / 32 * 32));
+}
+
 // Matrix-product combine: M = M_later M_earlier (sls.py:217-218), both orientations.
 __global__ void __launch_bounds__(512) k_matprod(float* Ms, float* MsT, long long inst_stride, int n, const int4* ops) {
   const int inst = blockIdx.y;
@@ -655,7 +661,7 @@ __global__ void __launch_bounds__(512) k_matprod(float* Ms, float* MsT, long lon
   cp_async_wait<0>();
   __syncthreads();
   // plan .w = 1: no later product reads this slot, so its transposed copy is dead
-  gemm_tn(n, Lt, Er, lds, EpiGlobal{base + (size_t)op.x * MS, nullptr, ldg, n, (op.w & 1) ? nullptr : baseT + (size_t)op.x * MS});
+  gemm_tn84(n, Lt, Er, lds, EpiGlobal{base + (size_t)op.x * MS, nullptr, ldg, n, (op.w & 1) ? nullptr : baseT + (size_t)op.x * MS});
 }
 
 // Phi^u_{k,j} = K_{k,j} Phi^x_{k,j} (sls.py:310-318).
@@ -989,7 +995,7 @@ static int sls_synthesize_once(Ctx* c, const gsls_qp_t* qp, const float* E, cuda
       const int o0 = s->mp.layer_off[l], o1 = s->mp.layer_off[l + 1];
       if (o1 == o0) continue;
       ProfScope ps(P_SLS_MATPROD, st, (double)(o1 - o0) * B);
-      k_matprod<<<dim3(o1 - o0, B), matmul_threads(n), sb, st>>>(S.Ms, S.MsT, (long long)S.mp_nslots * (long long)MS, n,
+      k_matprod<<<dim3(o1 - o0, B), matprod_threads(n), sb, st>>>(S.Ms, S.MsT, (long long)S.mp_nslots * (long long)MS, n,
                                                                   S.mp_ops + o0);
       GSLS_CUDA_CHECK(cudaGetLastError());
     }

@@ -125,6 +125,41 @@ __device__ inline void gemm_tn(int n, const float* At, const float* B, int lds, 
   }
 }
 
+// The same product on 8 x 4 register tiles (two 4 x 4 epilogue calls, the lower one only
+// inside the padded np rows): one B row load feeds eight rows, halving gemm_tn's shared
+// wavefronts per FMA (k_matprod is bound by them).  Every element keeps its fma chain.
+template <class Epi>
+__device__ inline void gemm_tn84(int n, const float* At, const float* B, int lds, Epi epi) {
+  const int np = ldg_of(n), T = np >> 2, TR = (np + 7) >> 3;
+  const int tiles = TR * T;
+  for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+    const int ti = t / T, tj = t - ti * T;
+    float acc[8][4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+    const float* pa = At + 8 * ti;
+    const float* pb = B + 4 * tj;
+#pragma unroll 2
+    for (int k = 0; k < n; ++k) {
+      const float4 a0 = *reinterpret_cast<const float4*>(pa + k * lds);
+      const float4 a1 = *reinterpret_cast<const float4*>(pa + k * lds + 4);
+      const float4 b = *reinterpret_cast<const float4*>(pb + k * lds);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        acc[r][0] = fmaf(av[r], b.x, acc[r][0]);
+        acc[r][1] = fmaf(av[r], b.y, acc[r][1]);
+        acc[r][2] = fmaf(av[r], b.z, acc[r][2]);
+        acc[r][3] = fmaf(av[r], b.w, acc[r][3]);
+      }
+    }
+    epi(8 * ti, 4 * tj, *reinterpret_cast<float(*)[4][4]>(&acc[0][0]));
+    if (8 * ti + 4 < np) epi(8 * ti + 4, 4 * tj, *reinterpret_cast<float(*)[4][4]>(&acc[4][0]));
+  }
+}
+
 // epilogues
 struct EpiSmem {  // C (smem) = acc (+ I)
   float* C;
