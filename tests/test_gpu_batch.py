@@ -185,3 +185,22 @@ def test_lagged_rebuilds_keep_every_instance_path(monkeypatch):
         assert np.array_equal(a[k], b[k]), k
     assert np.abs(a[3] - b[3]).max() <= 1e-6
     assert np.abs(a[4] - b[4]).max() <= 1e-6 * max(1.0, np.abs(a[4]).max())
+
+
+def test_pack_engine_record_through_the_c_abi():
+    """dist.pack_engine (gsls_rti_pack_results): the per-instance record the ranks of a
+    multi-GPU bench all-gather after every step is [u0 | iterations, converged, rho
+    changes, cost], in instance order; gather_results at world size 1 copies it."""
+    import torch
+    from paper_2604_07644_b200 import dist as D
+    eng, wl, _ = _engine_step("q61", 8)
+    rec = _host(D.pack_engine(eng))
+    nu = eng.u0.shape[1]
+    assert rec.shape == (8, nu + len(D.RESULT_FIELDS))
+    assert np.array_equal(rec[:, :nu], _host(eng.u0))
+    assert np.array_equal(rec[:, nu], _host(eng.stats.iterations).astype(float))
+    assert np.array_equal(rec[:, nu + 1], _host(eng.stats.converged).astype(float))
+    assert np.array_equal(rec[:, nu + 2], _host(eng.stats.rho_changes).astype(float))
+    assert np.array_equal(rec[:, nu + 3], _host(eng.cost))
+    out = torch.empty(8, rec.shape[1], dtype=torch.float64, device="cuda")
+    assert np.array_equal(_host(D.gather_results(D.pack_engine(eng), 1, out=out)), rec)
