@@ -571,9 +571,17 @@ def run_ours(args):
     from paper_2604_07644_b200.sls import ragged_to_cells
 
     rank, local, world = dist_env()
+    # GSLS_BENCH_BACKEND=gloo (tests only): several ranks on one GPU, to check the multi-rank
+    # control flow (barriers, max-over-ranks timing, rank-0-only passes) on a one-GPU box
+    backend = os.environ.get("GSLS_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     lib = nat.load()
     peaks = measured_peaks()
 
