@@ -235,35 +235,64 @@ __global__ void __launch_bounds__(256) k_leaf_init(DevLqr L, gsls_qp_t qp, const
   // the inverse's work area) when the scan plan carries it factored (lowrank.cuh)
   const bool cfac = L.cvf_leaf && (L.cvf_leaf[k] & 8);
   const double* Linv = wk + kMaxM * (kMaxM + 1);
-  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
-    const int i = L.fd_ldg.div(e), j = e - i * ldg;
-    double p = 0.0, a = 0.0, cc = 0.0;
+  // rows i and i + nh per thread: the column-j operands (C, RS, B rows of j) are loaded once
+  // for both (the loop is bound by shared-memory wavefronts); every element keeps its chains
+  const int nh = (n + 1) >> 1;
+  for (int e = threadIdx.x; e < nh * ldg; e += blockDim.x) {
+    const int i0 = L.fd_ldg.div(e), j = e - i0 * ldg;
+    const bool two = i0 + nh < n;
+    const int i1 = two ? i0 + nh : i0;
+    double p0 = 0.0, a0 = 0.0, c0 = 0.0, p1 = 0.0, a1 = 0.0, c1 = 0.0;
     if (cfac && j < m) {
-      double f = 0.0;
-      for (int b = 0; b <= j; ++b) f = fma(Bst[i * ldb + b], Linv[j * (kMaxM + 1) + b], f);
-      cc = f;
+      double f0 = 0.0, f1 = 0.0;
+      for (int b = 0; b <= j; ++b) {
+        const double li = Linv[j * (kMaxM + 1) + b];
+        f0 = fma(Bst[i0 * ldb + b], li, f0);
+        f1 = fma(Bst[i1 * ldb + b], li, f1);
+      }
+      c0 = f0;
+      c1 = f1;
     }
     if (j < n) {
-      double s = 0.0;
-      for (int r = 0; r < c; ++r) s = fma(Cst[r * n + i], Cst[r * n + j], s);
-      const double qh = (double)Qg[i * n + j] + rho * s;
-      double sr = 0.0, br = 0.0;
-      for (int l = 0; l < m; ++l) {
-        sr = fma(Sh[l * n + i], RS[l * n + j], sr);
-        br = fma(Bst[i * ldb + l], RS[l * n + j], br);
+      double s0 = 0.0, s1 = 0.0;
+      for (int r = 0; r < c; ++r) {
+        const double cj = Cst[r * n + j];
+        s0 = fma(Cst[r * n + i0], cj, s0);
+        s1 = fma(Cst[r * n + i1], cj, s1);
       }
-      p = qh - sr;
-      a = (double)Ag[i * n + j] - br;
+      double sr0 = 0.0, br0 = 0.0, sr1 = 0.0, br1 = 0.0;
+      for (int l = 0; l < m; ++l) {
+        const double rs = RS[l * n + j];
+        sr0 = fma(Sh[l * n + i0], rs, sr0);
+        br0 = fma(Bst[i0 * ldb + l], rs, br0);
+        sr1 = fma(Sh[l * n + i1], rs, sr1);
+        br1 = fma(Bst[i1 * ldb + l], rs, br1);
+      }
+      p0 = ((double)Qg[i0 * n + j] + rho * s0) - sr0;
+      a0 = (double)Ag[i0 * n + j] - br0;
+      p1 = ((double)Qg[i1 * n + j] + rho * s1) - sr1;
+      a1 = (double)Ag[i1 * n + j] - br1;
       if (!cfac) {  // dense C-hat = B R-hat^-1 B' (a factored leaf carries B L^-T instead)
-        double bb = 0.0;
-        for (int l = 0; l < m; ++l) bb = fma(BR[i * m + l], Bst[j * ldb + l], bb);
-        cc = bb;
+        double bb0 = 0.0, bb1 = 0.0;
+        for (int l = 0; l < m; ++l) {
+          const double bj = Bst[j * ldb + l];
+          bb0 = fma(BR[i0 * m + l], bj, bb0);
+          bb1 = fma(BR[i1 * m + l], bj, bb1);
+        }
+        c0 = bb0;
+        c1 = bb1;
       }
     }
-    Pd[e] = (float)p;
-    Ad[e] = (float)a;
-    if (j < n) ATd[j * ldg + i] = (float)a;
-    Cd[e] = (float)cc;
+    Pd[i0 * ldg + j] = (float)p0;
+    Ad[i0 * ldg + j] = (float)a0;
+    if (j < n) ATd[j * ldg + i0] = (float)a0;
+    Cd[i0 * ldg + j] = (float)c0;
+    if (two) {
+      Pd[i1 * ldg + j] = (float)p1;
+      Ad[i1 * ldg + j] = (float)a1;
+      if (j < n) ATd[j * ldg + i1] = (float)a1;
+      Cd[i1 * ldg + j] = (float)c1;
+    }
   }
   double* Rhat = L.Rhat + st * m * m;
   float* Shat = L.Shat + st * m * n;
