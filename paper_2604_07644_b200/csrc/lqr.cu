@@ -636,11 +636,19 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
   for (int e = threadIdx.x; e < n * m; e += blockDim.x) Bst[e] = Bg[e];
   cp_async_wait<0>();
   __syncthreads();
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+  const int mh = (m + 1) >> 1;
+  for (int e = threadIdx.x; e < mh * n; e += blockDim.x) {  // B' P+, rows l and l + mh (one P+ load for both)
     const int l = L.fd_n.div(e), j = e - l * n;
-    double s = 0.0;
-    for (int i = 0; i < n; ++i) s = fma(Bst[i * m + l], (double)Pns[i * ldg + j], s);
-    BtP[e] = s;
+    const bool two = l + mh < m;
+    const int l1 = two ? l + mh : l;
+    double s0 = 0.0, s1 = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double pv = (double)Pns[i * ldg + j];
+      s0 = fma(Bst[i * m + l], pv, s0);
+      s1 = fma(Bst[i * m + l1], pv, s1);
+    }
+    BtP[l * n + j] = s0;
+    if (two) BtP[l1 * n + j] = s1;
   }
   __syncthreads();
   const float* Ag = qp.A + st * n * n;
@@ -686,17 +694,30 @@ __global__ void __launch_bounds__(256) k_gains(DevLqr L, gsls_qp_t qp, const dou
   // closed loop Abar = A + B K -> COT leaf k (leaf 0 carries A = 0, lqr.py:354)
   float* Ad = L.cotA + ((size_t)inst * L.cot_nslots + k) * MS;
   float* ATd = L.cotAT + ((size_t)inst * L.cot_nslots + k) * MS;
-  for (int e = threadIdx.x; e < n * ldg; e += blockDim.x) {
+  const int nh = (n + 1) >> 1;
+  for (int e = threadIdx.x; e < nh * ldg; e += blockDim.x) {  // rows i and i + nh (one K load for both)
     const int i = L.fd_ldg.div(e), j = e - i * ldg;
-    double v = 0.0;
+    const bool two = i + nh < n;
+    const int i1 = two ? i + nh : i;
+    double v0 = 0.0, v1 = 0.0;
     if (j < n) {
-      double s = 0.0;
-      for (int l = 0; l < m; ++l) s = fma(Bst[i * m + l], Ks[l * n + j], s);
-      v = (double)Ag[i * n + j] + s;
+      double s0 = 0.0, s1 = 0.0;
+      for (int l = 0; l < m; ++l) {
+        const double kv = Ks[l * n + j];
+        s0 = fma(Bst[i * m + l], kv, s0);
+        s1 = fma(Bst[i1 * m + l], kv, s1);
+      }
+      v0 = (double)Ag[i * n + j] + s0;
+      v1 = (double)Ag[i1 * n + j] + s1;
     }
-    Abar[e] = (float)v;
-    Ad[e] = (k == 0) ? 0.f : (float)v;
-    if (j < n) ATd[j * ldg + i] = (k == 0) ? 0.f : (float)v;
+    Abar[i * ldg + j] = (float)v0;
+    Ad[i * ldg + j] = (k == 0) ? 0.f : (float)v0;
+    if (j < n) ATd[j * ldg + i] = (k == 0) ? 0.f : (float)v0;
+    if (two) {
+      Abar[i1 * ldg + j] = (float)v1;
+      Ad[i1 * ldg + j] = (k == 0) ? 0.f : (float)v1;
+      if (j < n) ATd[j * ldg + i1] = (k == 0) ? 0.f : (float)v1;
+    }
   }
   // fused feedforward / constraint operators (ctx.h):
   //   kf = kk0 + X5 p+ + X4 w with X5 = -Gamma B', X4 = -rho Gamma D', kk0 = -Gamma (B' cvec + r)
